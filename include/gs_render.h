@@ -1,0 +1,182 @@
+/*
+ * gs_render.h -- C-ABI of the B200 (sm_100a) forward 3DGS renderer with
+ * GEMM-compatible alpha blending (GEMM-GS, arXiv 2604.02120).
+ *
+ * Citations: P:n = PAPER.md line n (the paper's LaTeX source).
+ *
+ * The library computes, for one camera, the four stages of the forward
+ * render path the paper names:
+ *   (a) preprocessing  -- project 3D Gaussians to 2D ellipses, tile
+ *       intersection, depth d and RGB colour c;
+ *   (b) duplication    -- one copy per touched 16x16 tile, key = tile index
+ *       concatenated with depth;
+ *   (c) sorting        -- per-tile depth order;
+ *   (d) blending       -- Eq. (1) front-to-back compositing with the
+ *       exponent computed as the GEMM of Eq. (6)-(8) on
+ *       tcgen05 tensor cores, alpha = o*exp(power), alpha-skip below 1/255,
+ *       alpha cap 0.99, early termination at T < 1e-4 (Alg. 1-2, P:128-191,
+ *       P:309-383; readings R-1..R-5 in DESIGN.md).
+ *
+ * Conventions (all entry points):
+ *  - Return GS_OK (0) or a negative gs_status. Nothing is silently truncated:
+ *    if the duplicated key count K exceeds the context's max_keys the call
+ *    fails with GS_ERR_CAPACITY (reported by gs_last_stats / GS_SYNC).
+ *  - Unless stated otherwise every array pointer is a DEVICE pointer on the
+ *    context's device, owned by the caller, 16-byte aligned, contiguous,
+ *    float32 little-endian. The library never frees caller memory.
+ *  - Inputs are ACTIVATED values: scales > 0, rotations as unit-norm
+ *    quaternions (w,x,y,z) (renormalised in-kernel), opacity in (0,1).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); all work is
+ *    enqueued on it, asynchronously. One gs_ctx per (device, host thread).
+ *  - Determinism: outputs are bit-identical across runs, batch sizes and GPU
+ *    counts for identical inputs.
+ */
+#ifndef GS_RENDER_H_
+#define GS_RENDER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GS_OK = 0,
+    GS_ERR_INVALID_ARG = -1,      /* null pointer, N < 0, W/H <= 0 or above ctx max, sh_degree > 3 */
+    GS_ERR_ALIGNMENT = -2,        /* a pointer is not 16-byte aligned                               */
+    GS_ERR_CAPACITY = -3,         /* N > max_points or K > max_keys (nothing truncated)             */
+    GS_ERR_CUDA = -4,             /* a CUDA runtime call failed                                     */
+    GS_ERR_UNSUPPORTED_ARCH = -5, /* device is not sm_100 (B200)                                    */
+    GS_ERR_NO_DEVICE = -6
+} gs_status;
+
+/* Pinhole camera, OpenCV axes (x right, y down, z forward). A world point p
+ * maps to camera space as R p + t (R row-major). Pixel (i,j) has its centre
+ * at integer coordinates (R-15); the projected mean is (fx x/z + cx, fy y/z + cy).
+ * tan_fovx / tan_fovy bound the EWA Jacobian clamp (1.3 tan_fov, R-14);
+ * campos is the origin of the SH view direction. Gaussians with camera depth
+ * z <= znear are culled. 22 floats, in this order. */
+typedef struct {
+    float R[9];
+    float t[3];
+    float fx, fy, cx, cy;
+    float znear;
+    float tan_fovx, tan_fovy;
+    float campos[3];
+} gs_camera;
+
+enum {
+    GS_BLEND_TC = 0,      /* tcgen05 TF32 hi/lo exponent GEMM (the paper's method, default) */
+    GS_BLEND_DIRECT = 1   /* CUDA-core direct Eq. (3) (vanilla Alg. 1), A/B baseline        */
+};
+
+enum {
+    GS_FLAG_SYNC = 1u     /* synchronise the stream at the end and report device errors     */
+};
+
+typedef struct {
+    float bg[3];           /* background colour added as T*bg (R-17)                         */
+    int sh_degree;         /* 0..3; -1 => shs_or_colors holds plain colours [N,3]            */
+    int sh_stride;         /* SH coefficients per Gaussian in shs (>= (deg+1)^2)             */
+    float scale_modifier;  /* multiplies every scale (1.0)                                   */
+    int blend;             /* GS_BLEND_TC | GS_BLEND_DIRECT                                  */
+    unsigned flags;        /* GS_FLAG_*                                                      */
+} gs_opts;
+
+typedef struct {
+    int64_t n_points;      /* N of the last call                                             */
+    int64_t n_visible;     /* Gaussians with tiles_touched > 0                              */
+    int64_t n_keys;        /* K = number of (Gaussian, tile) pairs                          */
+    int64_t capacity_keys; /* max_keys of the context                                       */
+    int status;            /* gs_status of the last frame (device-side checks included)     */
+} gs_stats;
+
+typedef struct gs_ctx gs_ctx;
+
+/* Creates a context owning device workspace for up to max_points Gaussians,
+ * max_keys duplicated keys and max_w x max_h images on `device`.
+ * Fails with GS_ERR_UNSUPPORTED_ARCH unless the device is sm_100. */
+int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys,
+                  int max_w, int max_h);
+int gs_ctx_destroy(gs_ctx *ctx);
+
+/* Renders one view. means3D [N,3], scales [N,3], rots [N,4] (w,x,y,z),
+ * opacity [N], shs_or_colors [N,sh_stride,3] (or [N,3] if sh_degree == -1).
+ * out_rgb [3,H,W] planar, out_T [H,W] final transmittance; every in-frame pixel
+ * of both is written: out_rgb[c] = C_c + T*bg_c (Eq. 1 plus background). */
+int gs_render(gs_ctx *ctx, void *stream, int N, const float *means3D, const float *scales,
+              const float *rots, const float *opacity, const float *shs_or_colors,
+              const gs_camera *cam, int W, int H, const gs_opts *opts,
+              float *out_rgb, float *out_T);
+
+/* Renders n_views cameras (host array cams[n_views]) of the same scene into
+ * out_rgb [n_views,3,H,W] and out_T [n_views,H,W] (device), back to back on
+ * `stream`. Equivalent to n_views gs_render calls. */
+int gs_render_views(gs_ctx *ctx, void *stream, int N, const float *means3D, const float *scales,
+                    const float *rots, const float *opacity, const float *shs_or_colors,
+                    const gs_camera *cams, int n_views, int W, int H, const gs_opts *opts,
+                    float *out_rgb, float *out_T);
+
+/* End-to-end variant with HOST buffers (pinned memory recommended): copies the
+ * scene host->device, renders n_views, copies the frames device->host and
+ * synchronises `stream` before returning. Scene staging uses the context's own
+ * device buffers (sized by max_points). */
+int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
+                         const float *scales, const float *rots, const float *opacity,
+                         const float *shs_or_colors, const gs_camera *cams, int n_views,
+                         int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
+
+/* Synchronises the last stream used by ctx and reports counts and the status
+ * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */
+int gs_last_stats(gs_ctx *ctx, gs_stats *out);
+
+const char *gs_status_string(int status);
+
+/* Compute capability of `device` as 10*major+minor, or a negative gs_status. */
+int gs_device_arch(int device);
+
+/* ---- test-only entry points (bit-exact stage checks, precision study) ---- */
+
+/* Stage (a) only. Outputs [N]: depth, xy [N,2], conic [N,3] = (A,B,C) of the
+ * inverse 2D covariance, rgb [N,3], rect [N,4] int32 (xmin,ymin,xmax,ymax,
+ * half-open tile ranges), radius [N] int32, touched [N] uint32 (0 = culled;
+ * culled rows are all zero). Operation order: docs/preprocess_order.md. */
+int gs_debug_preprocess(gs_ctx *ctx, void *stream, int N, const float *means3D,
+                        const float *scales, const float *rots, const float *opacity,
+                        const float *shs_or_colors, const gs_camera *cam, int W, int H,
+                        const gs_opts *opts, float *depth, float *xy, float *conic, float *rgb,
+                        int32_t *rect, int32_t *radius, uint32_t *touched);
+
+/* Stages (a)-(c). Writes sorted keys [K] (tile << 32 | depth bits), vals [K]
+ * (Gaussian index), ranges [tiles,2] ([start,end) per tile, empty = (0,0)) and
+ * the host int64 *n_keys = K. keys/vals must hold `capacity` entries; if
+ * K > capacity only *n_keys is written and GS_ERR_CAPACITY returned.
+ * Synchronises `stream`. */
+int gs_debug_binning(gs_ctx *ctx, void *stream, int N, const float *means3D,
+                     const float *scales, const float *rots, const float *opacity,
+                     const float *shs_or_colors, const gs_camera *cam, int W, int H,
+                     const gs_opts *opts, uint64_t *keys, uint32_t *vals, uint32_t *ranges,
+                     int64_t capacity, int64_t *n_keys);
+
+/* Stage (d) alone from caller-supplied splats: xy [N,2], conic [N,3] (A,B,C),
+ * opacity [N], rgb [N,3], vals [K] and ranges [tiles,2] as produced by
+ * binning. opts->blend selects the kernel. */
+int gs_debug_blend(gs_ctx *ctx, void *stream, int N, const float *xy, const float *conic,
+                   const float *opacity, const float *rgb, const uint32_t *vals, int64_t K,
+                   const uint32_t *ranges, int W, int H, const gs_opts *opts,
+                   float *out_rgb, float *out_T);
+
+/* The exponent GEMM of Eq. (8) alone, as the tensor-core blend computes it:
+ * for every list entry e of every tile, m[e][p] = log2(alpha) before the 0.99
+ * cap, i.e. log2(e)*power + log2(o), for the 256 pixels p of the tile
+ * (p = 32*w + lane, pixel (x,y) = (8*(w%2) + lane%8, 4*(w/2) + lane/8)).
+ * out_m [K,256] float32. Used to measure |d ln alpha| against the oracle. */
+int gs_debug_exponents(gs_ctx *ctx, void *stream, int N, const float *xy, const float *conic,
+                       const float *opacity, const uint32_t *vals, int64_t K,
+                       const uint32_t *ranges, int W, int H, float *out_m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_RENDER_H_ */

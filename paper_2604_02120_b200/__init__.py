@@ -1,0 +1,11 @@
+"""B200-native (sm_100a) forward 3DGS renderer with GEMM-compatible alpha
+blending (GEMM-GS, arXiv 2604.02120).
+
+The render path lives in hand-written CUDA kernels behind the C-ABI of
+include/gs_render.h (libgsrender.so, built in-tree by build.py); this package
+holds only the thin ctypes binding (_binding.py) and the seeded synthetic
+input generators (synth.py).
+"""
+from . import synth  # noqa: F401
+from ._binding import (GS_BLEND_DIRECT, GS_BLEND_TC, GS_FLAG_SYNC, Context, GsError,  # noqa: F401
+                       camera, load, opts, scene_to_device, scene_to_host)

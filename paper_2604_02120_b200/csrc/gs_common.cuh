@@ -1,0 +1,209 @@
+// gs_common.cuh -- shared definitions of the CUDA path (device workspace,
+// constants, PTX wrappers for mbarrier / tcgen05 / TMEM on sm_100a).
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gs_render.h"
+
+#define GS_TILE 16
+#define GS_TILE_PIX 256
+
+namespace gs {
+
+// ---- per-frame device counters (zeroed once per frame) --------------------
+struct Counters {
+    uint32_t n_visible;        // compaction output
+    uint32_t err;              // device-side error bits (1 = key capacity)
+    uint64_t n_keys;           // K (64-bit: the capacity check is exact)
+    uint32_t tickets[16];      // onesweep / scan chunk tickets, one per pass
+    uint32_t tile_queue;       // blend persistent work queue
+    uint32_t pad[7];
+    uint32_t hist_depth[4][256];
+    uint32_t hist_tile[4][256];
+};
+
+// ---- device workspace owned by the context ---------------------------------
+struct Workspace {
+    // per Gaussian (max_points)
+    uint32_t *depth_bits;      // [N] raw IEEE bits of the camera depth
+    float2 *xy;                // [N] projected mean (pixels)
+    float4 *conic_o;           // [N] (A, B, C, opacity)
+    float4 *rgb;               // [N] (r, g, b, 0)
+    ushort4 *rect;             // [N] (xmin, ymin, xmax, ymax) tiles, half-open
+    uint32_t *touched;         // [N] tiles touched (0 = culled)
+    int32_t *radius;           // [N] pixel radius (debug output)
+    uint32_t *sk[2];           // [N] depth-sort keys, ping-pong
+    uint32_t *sv[2];           // [N] depth-sort values (Gaussian index)
+    uint32_t *offsets;         // [N] exclusive scan of touched in depth order
+    // per key (max_keys)
+    uint32_t *kt[2];           // [K] tile ids, ping-pong
+    uint32_t *kv[2];           // [K] Gaussian indices, ping-pong
+    // per tile
+    uint32_t *tile_count;      // [tiles]
+    uint2 *ranges;             // [tiles]
+    // lookback status (epoch-tagged, never memset)
+    unsigned long long *scan_status;   // [max chunks]
+    unsigned long long *sort_status;   // [max chunks * 256]
+    Counters *counters;
+    // scene staging for the host-pointer entry point
+    float *stage;
+    size_t stage_bytes;
+};
+
+// Chunk geometry of the single-pass scans / onesweep radix passes.
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_CHUNK = SORT_THREADS * SORT_ITEMS;   // 4096 keys per chunk
+
+__host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- small PTX helpers ------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t cnt) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// tcgen05 / TMEM
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_relinquish() {
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, both K-major
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive columns: thread i receives row (lane base + i), cols c..c+31
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major, no swizzle (core matrix = 8 rows x 16 B).
+//   LBO = byte distance between the two core matrices adjacent in K,
+//   SBO = byte distance between core-matrix groups adjacent in M/N.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;     // descriptor version (sm100)
+    // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE
+    return d;
+}
+
+// Instruction descriptor for kind::tf32: D f32, A/B tf32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4)                 // D format f32
+           | (2u << 7)               // A format tf32
+           | (2u << 10)              // B format tf32
+           | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t f32_to_tf32_rna(float x) {
+    uint32_t y;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(x));
+    return y;
+}
+
+// log2(1/255) in binary32: the alpha-skip threshold in the log2 domain (R-1)
+constexpr float LOG2_ALPHA_MIN = -7.99435329f;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float T_MIN = 1e-4f;    // early termination (R-2)
+constexpr float ALPHA_MAX = 0.99f; // alpha cap (R-4)
+
+}  // namespace gs
+
+// host-side launch helpers (defined in the respective .cu files)
+namespace gs {
+void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
+                       const float *rots, const float *opacity, const float *shs, int sh_degree,
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H);
+void launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
+                    uint32_t &epoch);
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
+                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
+                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms);
+void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
+                         const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
+                         const float bg[3], float *out_rgb, float *out_T, const Counters *counters);
+}  // namespace gs

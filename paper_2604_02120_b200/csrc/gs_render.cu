@@ -1,0 +1,388 @@
+// gs_render.cu -- the C-ABI of include/gs_render.h: context / workspace
+// management and the per-frame orchestration of the four stages (PAPER.md
+// P:109-117): preprocess -> compaction + depth sort -> duplication -> tile
+// sort + ranges -> blend. All counts stay on the device (no host sync inside
+// a frame); the only optional synchronisation is GS_FLAG_SYNC / gs_last_stats.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "gs_common.cuh"
+
+struct gs_ctx {
+    int device = 0;
+    int num_sms = 148;
+    int64_t max_points = 0, max_keys = 0;
+    int max_w = 0, max_h = 0, max_tiles = 0;
+    gs::Workspace ws{};
+    uint32_t epoch = 0;
+    cudaStream_t last_stream = nullptr;
+    int64_t last_n = 0;
+    int last_status = GS_OK;
+    float *frame_rgb = nullptr, *frame_T = nullptr;   // staging for the host entry point
+};
+
+namespace {
+
+template <class T>
+cudaError_t alloc(T *&p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void **>(&p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+bool aligned16(const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_cuda(cudaError_t e) {
+    if (e != cudaSuccess) {
+        fprintf(stderr, "gs_render: CUDA error %s\n", cudaGetErrorString(e));
+        return GS_ERR_CUDA;
+    }
+    return GS_OK;
+}
+
+void maybe_reset_epoch(gs_ctx *c, cudaStream_t st) {
+    if (c->epoch > 0xFFFF00u) {   // 24-bit epoch tag in the look-back status words
+        const int64_t nch = gs::ceil_div_i(std::max<int64_t>(c->max_points, c->max_keys), gs::SORT_CHUNK) + 1;
+        cudaMemsetAsync(c->ws.scan_status, 0, sizeof(unsigned long long) * nch, st);
+        cudaMemsetAsync(c->ws.sort_status, 0, sizeof(unsigned long long) * nch * 256, st);
+        c->epoch = 0;
+    }
+}
+
+int validate(gs_ctx *c, int N, const void *means, const void *scales, const void *rots, const void *opacity,
+             const void *shs, const gs_camera *cam, int W, int H, const gs_opts *o) {
+    if (!c || !cam || !o || N < 0 || W <= 0 || H <= 0) return GS_ERR_INVALID_ARG;
+    if (W > c->max_w || H > c->max_h) return GS_ERR_INVALID_ARG;
+    if (N > c->max_points) return GS_ERR_CAPACITY;
+    if (o->sh_degree > 3 || o->sh_degree < -1) return GS_ERR_INVALID_ARG;
+    if (o->sh_degree >= 0 && o->sh_stride < (o->sh_degree + 1) * (o->sh_degree + 1)) return GS_ERR_INVALID_ARG;
+    if (N > 0 && (!means || !scales || !rots || !opacity || !shs)) return GS_ERR_INVALID_ARG;
+    if (!aligned16(rots)) return GS_ERR_ALIGNMENT;
+    return GS_OK;
+}
+
+// preprocess + binning of one view into the workspace (counters zeroed first)
+void enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
+                   const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
+    maybe_reset_epoch(c, st);
+    cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
+    gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
+                          o.scale_modifier, cam, W, H);
+    const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
+    gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch);
+}
+
+void enqueue_blend(gs_ctx *c, cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
+                   const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o, float *out_rgb,
+                   float *out_T, float *dump) {
+    const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
+    if (o.blend == GS_BLEND_DIRECT && !dump)
+        gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+                                c->ws.counters);
+    else
+        gs::launch_blend_tc(c->ws, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+                            dump, c->num_sms);
+}
+
+int finish(gs_ctx *c, cudaStream_t st, const gs_opts &o, int64_t N) {
+    c->last_stream = st;
+    c->last_n = N;
+    c->last_status = GS_OK;
+    int rc = check_cuda(cudaGetLastError());
+    if (rc) return c->last_status = rc;
+    if (o.flags & GS_FLAG_SYNC) {
+        gs_stats s;
+        rc = gs_last_stats(c, &s);
+        if (rc) return rc;
+        return s.status;
+    }
+    return GS_OK;
+}
+
+// ---- small packing kernels for the debug / split entry points ------------
+__global__ void k_pack_splats(int N, const float *xy, const float *conic, const float *opacity, const float *rgb,
+                              float2 *oxy, float4 *oco, float4 *orgb) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    oxy[i] = make_float2(xy[2 * i], xy[2 * i + 1]);
+    oco[i] = make_float4(conic[3 * i], conic[3 * i + 1], conic[3 * i + 2], opacity[i]);
+    if (rgb) orgb[i] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
+}
+
+__global__ void k_unpack_pre(int N, gs::Workspace ws, float *depth, float *xy, float *conic, float *rgb,
+                             int32_t *rect, int32_t *radius, uint32_t *touched) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    depth[i] = __uint_as_float(ws.depth_bits[i]);
+    xy[2 * i] = ws.xy[i].x;
+    xy[2 * i + 1] = ws.xy[i].y;
+    const float4 co = ws.conic_o[i];
+    conic[3 * i] = co.x; conic[3 * i + 1] = co.y; conic[3 * i + 2] = co.z;
+    const float4 c = ws.rgb[i];
+    rgb[3 * i] = c.x; rgb[3 * i + 1] = c.y; rgb[3 * i + 2] = c.z;
+    const ushort4 r = ws.rect[i];
+    rect[4 * i] = r.x; rect[4 * i + 1] = r.y; rect[4 * i + 2] = r.z; rect[4 * i + 3] = r.w;
+    radius[i] = ws.radius[i];
+    touched[i] = ws.touched[i];
+}
+
+__global__ void k_keys_out(int64_t K, const uint32_t *tiles, const uint32_t *idx, const uint32_t *depth_bits,
+                           uint64_t *keys, uint32_t *vals) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = idx[k];
+        keys[k] = ((uint64_t)tiles[k] << 32) | depth_bits[i];
+        vals[k] = i;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *gs_status_string(int s) {
+    switch (s) {
+        case GS_OK: return "ok";
+        case GS_ERR_INVALID_ARG: return "invalid argument";
+        case GS_ERR_ALIGNMENT: return "pointer not 16-byte aligned";
+        case GS_ERR_CAPACITY: return "capacity exceeded (N > max_points or K > max_keys)";
+        case GS_ERR_CUDA: return "CUDA runtime error";
+        case GS_ERR_UNSUPPORTED_ARCH: return "device is not sm_100 (B200)";
+        case GS_ERR_NO_DEVICE: return "no CUDA device";
+    }
+    return "unknown status";
+}
+
+int gs_device_arch(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return GS_ERR_NO_DEVICE;
+    if (device < 0 || device >= n) return GS_ERR_INVALID_ARG;
+    int ma = 0, mi = 0;
+    cudaDeviceGetAttribute(&ma, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&mi, cudaDevAttrComputeCapabilityMinor, device);
+    return 10 * ma + mi;
+}
+
+int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys, int max_w, int max_h) {
+    if (!out || max_points < 0 || max_keys < 0 || max_w <= 0 || max_h <= 0) return GS_ERR_INVALID_ARG;
+    if (max_keys >= (int64_t)1 << 32 || max_points >= (int64_t)1 << 31) return GS_ERR_INVALID_ARG;
+    *out = nullptr;
+    const int arch = gs_device_arch(device);
+    if (arch < 0) return arch;
+    if (arch != 100) return GS_ERR_UNSUPPORTED_ARCH;
+    if (check_cuda(cudaSetDevice(device))) return GS_ERR_CUDA;
+    gs_ctx *c = new (std::nothrow) gs_ctx();
+    if (!c) return GS_ERR_INVALID_ARG;
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->max_points = max_points;
+    c->max_keys = max_keys;
+    c->max_w = max_w;
+    c->max_h = max_h;
+    c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
+    const size_t N = (size_t)max_points, K = (size_t)max_keys;
+    const size_t nch = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1;
+    gs::Workspace &w = c->ws;
+    cudaError_t e = cudaSuccess;
+#define A(ptr, n) \
+    if (e == cudaSuccess) e = alloc(ptr, n)
+    A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
+    A(w.radius, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.offsets, N);
+    A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K);
+    A(w.tile_count, c->max_tiles); A(w.ranges, c->max_tiles);
+    A(w.scan_status, nch); A(w.sort_status, nch * 256);
+    A(w.counters, 1);
+#undef A
+    if (e == cudaSuccess) e = cudaMemset(w.scan_status, 0, sizeof(unsigned long long) * nch);
+    if (e == cudaSuccess) e = cudaMemset(w.sort_status, 0, sizeof(unsigned long long) * nch * 256);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        gs_ctx_destroy(c);
+        return check_cuda(e);
+    }
+    *out = c;
+    return GS_OK;
+}
+
+int gs_ctx_destroy(gs_ctx *c) {
+    if (!c) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    gs::Workspace &w = c->ws;
+    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+                    w.sv[0], w.sv[1], w.offsets, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.tile_count,
+                    w.ranges, w.scan_status, w.sort_status, w.counters, w.stage, c->frame_rgb, c->frame_T};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    delete c;
+    return GS_OK;
+}
+
+int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales, const float *rots,
+              const float *opacity, const float *shs, const gs_camera *cam, int W, int H, const gs_opts *o,
+              float *out_rgb, float *out_T) {
+    int rc = validate(c, N, means3D, scales, rots, opacity, shs, cam, W, H, o);
+    if (rc) return rc;
+    if (!out_rgb || !out_T) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
+    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb, out_T,
+                  nullptr);
+    return finish(c, st, *o, N);
+}
+
+int gs_render_views(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales, const float *rots,
+                    const float *opacity, const float *shs, const gs_camera *cams, int n_views, int W, int H,
+                    const gs_opts *o, float *out_rgb, float *out_T) {
+    if (!cams || n_views < 0) return GS_ERR_INVALID_ARG;
+    const size_t plane = (size_t)W * H;
+    for (int v = 0; v < n_views; v++) {
+        gs_opts ov = *o;
+        ov.flags &= ~GS_FLAG_SYNC;
+        int rc = gs_render(c, stream, N, means3D, scales, rots, opacity, shs, &cams[v], W, H, &ov,
+                           out_rgb + (size_t)v * 3 * plane, out_T + (size_t)v * plane);
+        if (rc) return rc;
+    }
+    return finish(c, reinterpret_cast<cudaStream_t>(stream), *o, N);
+}
+
+int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
+                         const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
+                         int n_views, int W, int H, const gs_opts *o, float *h_out_rgb, float *h_out_T) {
+    if (!c || !o || !cams || n_views < 0 || N < 0) return GS_ERR_INVALID_ARG;
+    if (N > c->max_points) return GS_ERR_CAPACITY;
+    if (W <= 0 || H <= 0 || W > c->max_w || H > c->max_h) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int ncoef = o->sh_degree < 0 ? 1 : o->sh_stride;
+    const size_t f_means = 3 * (size_t)N, f_scales = 3 * (size_t)N, f_rots = 4 * (size_t)N, f_op = (size_t)N,
+                 f_sh = 3 * (size_t)N * ncoef;
+    auto pad4 = [](size_t x) { return (x + 3) & ~size_t(3); };
+    const size_t total = pad4(f_means) + pad4(f_scales) + pad4(f_rots) + pad4(f_op) + pad4(f_sh);
+    if (total * sizeof(float) > c->ws.stage_bytes) {
+        if (c->ws.stage) cudaFree(c->ws.stage);
+        c->ws.stage = nullptr;
+        if (check_cuda(cudaMalloc(&c->ws.stage, total * sizeof(float)))) return GS_ERR_CUDA;
+        c->ws.stage_bytes = total * sizeof(float);
+    }
+    if (!c->frame_rgb) {
+        const size_t plane = (size_t)c->max_w * c->max_h;
+        if (check_cuda(cudaMalloc(&c->frame_rgb, 2 * 3 * plane * sizeof(float)))) return GS_ERR_CUDA;
+        if (check_cuda(cudaMalloc(&c->frame_T, 2 * plane * sizeof(float)))) return GS_ERR_CUDA;
+    }
+    float *d = c->ws.stage;
+    float *dm = d, *ds = dm + pad4(f_means), *dr = ds + pad4(f_scales), *dop = dr + pad4(f_rots),
+          *dsh = dop + pad4(f_op);
+    cudaMemcpyAsync(dm, means3D, f_means * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(ds, scales, f_scales * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, st);
+    const size_t plane = (size_t)W * H;
+    gs_opts ov = *o;
+    ov.flags &= ~GS_FLAG_SYNC;
+    for (int v = 0; v < n_views; v++) {
+        float *frgb = c->frame_rgb + (size_t)(v & 1) * 3 * (size_t)c->max_w * c->max_h;
+        float *fT = c->frame_T + (size_t)(v & 1) * (size_t)c->max_w * c->max_h;
+        int rc = gs_render(c, st, N, dm, ds, dr, dop, dsh, &cams[v], W, H, &ov, frgb, fT);
+        if (rc) return rc;
+        cudaMemcpyAsync(h_out_rgb + (size_t)v * 3 * plane, frgb, 3 * plane * 4, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(h_out_T + (size_t)v * plane, fT, plane * 4, cudaMemcpyDeviceToHost, st);
+    }
+    int rc = check_cuda(cudaStreamSynchronize(st));
+    if (rc) return rc;
+    gs_opts os = *o;
+    os.flags |= GS_FLAG_SYNC;
+    return finish(c, st, os, N);
+}
+
+int gs_last_stats(gs_ctx *c, gs_stats *out) {
+    if (!c || !out) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (check_cuda(cudaStreamSynchronize(c->last_stream))) return GS_ERR_CUDA;
+    gs::Counters h;
+    if (check_cuda(cudaMemcpy(&h, c->ws.counters, sizeof(h), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
+    out->n_points = c->last_n;
+    out->n_visible = h.n_visible;
+    out->n_keys = (int64_t)h.n_keys;
+    out->capacity_keys = c->max_keys;
+    out->status = (h.err & 1u) ? GS_ERR_CAPACITY : c->last_status;
+    c->last_status = out->status;
+    return GS_OK;
+}
+
+int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
+                        const float *rots, const float *opacity, const float *shs, const gs_camera *cam, int W,
+                        int H, const gs_opts *o, float *depth, float *xy, float *conic, float *rgb, int32_t *rect,
+                        int32_t *radius, uint32_t *touched) {
+    int rc = validate(c, N, means3D, scales, rots, opacity, shs, cam, W, H, o);
+    if (rc) return rc;
+    cudaSetDevice(c->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    gs::launch_preprocess(c->ws, st, N, means3D, scales, rots, opacity, shs, o->sh_degree, o->sh_stride,
+                          o->scale_modifier, *cam, W, H);
+    if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
+    return finish(c, st, *o, N);
+}
+
+int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales, const float *rots,
+                     const float *opacity, const float *shs, const gs_camera *cam, int W, int H, const gs_opts *o,
+                     uint64_t *keys, uint32_t *vals, uint32_t *ranges, int64_t capacity, int64_t *n_keys) {
+    int rc = validate(c, N, means3D, scales, rots, opacity, shs, cam, W, H, o);
+    if (rc) return rc;
+    if (!n_keys || !ranges) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
+    c->last_stream = st;
+    gs_stats s;
+    rc = gs_last_stats(c, &s);
+    if (rc) return rc;
+    *n_keys = s.n_keys;
+    if (s.status) return s.status;
+    if (s.n_keys > capacity) return GS_ERR_CAPACITY;
+    const int ntiles = gs::ceil_div_i(W, GS_TILE) * gs::ceil_div_i(H, GS_TILE);
+    if (s.n_keys > 0)
+        k_keys_out<<<c->num_sms * 4, 256, 0, st>>>(s.n_keys, c->ws.kt[0], c->ws.kv[0], c->ws.depth_bits, keys, vals);
+    cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
+    if (check_cuda(cudaStreamSynchronize(st))) return GS_ERR_CUDA;
+    return GS_OK;
+}
+
+static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, const float *conic,
+                              const float *opacity, const float *rgb, const uint32_t *vals, int64_t K,
+                              const uint32_t *ranges, int W, int H, const gs_opts *o, float *out_rgb, float *out_T,
+                              float *dump) {
+    if (!c || !o || N < 0 || N > c->max_points || W <= 0 || H <= 0 || W > c->max_w || H > c->max_h || K < 0)
+        return GS_ERR_INVALID_ARG;
+    if (!ranges || (N > 0 && (!xy || !conic || !opacity))) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
+    if (N > 0)
+        k_pack_splats<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, xy, conic, opacity, rgb, c->ws.xy, c->ws.conic_o,
+                                                              c->ws.rgb);
+    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
+                  *o, out_rgb, out_T, dump);
+    return finish(c, st, *o, N);
+}
+
+int gs_debug_blend(gs_ctx *c, void *stream, int N, const float *xy, const float *conic, const float *opacity,
+                   const float *rgb, const uint32_t *vals, int64_t K, const uint32_t *ranges, int W, int H,
+                   const gs_opts *o, float *out_rgb, float *out_T) {
+    if (!out_rgb || !out_T || (N > 0 && !rgb)) return GS_ERR_INVALID_ARG;
+    return debug_blend_common(c, stream, N, xy, conic, opacity, rgb, vals, K, ranges, W, H, o, out_rgb, out_T,
+                              nullptr);
+}
+
+int gs_debug_exponents(gs_ctx *c, void *stream, int N, const float *xy, const float *conic, const float *opacity,
+                       const uint32_t *vals, int64_t K, const uint32_t *ranges, int W, int H, float *out_m) {
+    if (!out_m) return GS_ERR_INVALID_ARG;
+    gs_opts o{};
+    o.blend = GS_BLEND_TC;
+    o.flags = GS_FLAG_SYNC;
+    return debug_blend_common(c, stream, N, xy, conic, opacity, nullptr, vals, K, ranges, W, H, &o, nullptr, nullptr,
+                              out_m);
+}
+
+}  // extern "C"

@@ -42,7 +42,7 @@ class Camera:
     H: int
 
     def packed(self) -> np.ndarray:
-        """21 float32 in the order of `gs_camera` (include/gs_render.h)."""
+        """22 float32 in the order of `gs_camera` (include/gs_render.h)."""
         return np.concatenate([
             np.asarray(self.R, np.float32).reshape(9),
             np.asarray(self.t, np.float32).reshape(3),

@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * preprocess outputs, sorted keys, values and tile ranges: bit-exact;
+  * pixels: max |d| <= 2e-3 per channel on pixels the oracle does not flag as
+    decision-ambiguous (margin mask, reading R-21), PSNR >= 50 dB over all
+    pixels; every pixel above 2e-3 must be flagged and within its flip bound.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_TC, GsError, synth
+
+from gpu_util import (MAX_ABS, MIN_PSNR, compare, gpu_binning, gpu_blend_from, gpu_preprocess, gpu_render,
+                      make_ctx)
+
+pytestmark = pytest.mark.gpu
+
+BIT_EXACT_KEYS = ("depth", "xy", "conic", "rgb", "rect", "radius", "touched")
+
+
+def _cfg(name, n=None):
+    scene, cams, bg = synth.make_config(name, n_override=n)
+    return scene, cams[0], bg
+
+
+def _ragged():
+    """77x45 image (ragged edge tiles), object scene with SH degree 2."""
+    scene = synth.object_scene(3000, 11, sh_degree=2)
+    cam = synth.look_at((0.5, -0.8, -3.5), (0, 0, 0), 77, 45, 0.8)
+    return scene, cam, np.array([0.2, 0.5, 0.9], np.float32)
+
+
+def _adversarial():
+    """Needles (anisotropy to 300), near-plane points, huge splats, border straddlers."""
+    rng = np.random.default_rng(100)
+    parts = []
+    s1 = synth.unbounded_scene(4000, 101, sh_degree=3, aniso_cap=300.0)
+    parts.append(s1)
+    n = 200
+    near = synth.object_scene(n, 102, sh_degree=3)
+    near.means[:] = np.array([0.0, 0.0, -3.75], np.float32) + rng.normal(0, 0.05, (n, 3)).astype(np.float32)
+    parts.append(near)
+    huge = synth.object_scene(20, 103, sh_degree=3)
+    huge.scales[:] = 0.8
+    parts.append(huge)
+    scene = synth.Scene(*[np.concatenate([getattr(p, f) for p in parts]) for f in
+                          ("means", "scales", "rots", "opacity", "shs")], 3)
+    cam = synth.look_at((0.0, 0.0, -4.0), (0, 0, 0), 160, 120, 1.0)
+    return scene, cam, np.array([0.0, 0.0, 0.0], np.float32)
+
+
+CASES = {"C1": lambda: _cfg("C1"), "C2": lambda: _cfg("C2"), "ragged": _ragged, "adversarial": _adversarial}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_preprocess_bit_exact(case):
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    got = gpu_preprocess(ctx, scene, cam)
+    ref = oracle.preprocess(scene, cam)
+    assert (ref["touched"] > 0).sum() > 0
+    for k in BIT_EXACT_KEYS:
+        a, b = got[k], ref[k]
+        a = a.view(np.uint32) if a.dtype == np.float32 else a.astype(np.int64)
+        b = b.view(np.uint32) if b.dtype == np.float32 else b.astype(np.int64)
+        bad = np.nonzero((a != b).reshape(len(a), -1).any(1))[0]
+        assert len(bad) == 0, f"{k}: {len(bad)} Gaussians differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_binning_bit_exact(case):
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    code, K, got = gpu_binning(ctx, scene, cam)
+    assert code == 0
+    pre = oracle.preprocess(scene, cam)
+    ref = oracle.binning(pre, cam.W, cam.H)
+    assert K == ref["K"]
+    assert np.array_equal(got["keys"], ref["keys"])
+    assert np.array_equal(got["vals"], ref["vals"])
+    assert np.array_equal(got["ranges"], ref["ranges"])
+
+
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT], ids=["tc", "direct"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_blend_parity_on_oracle_binning(case, blend):
+    """Stage (d) alone: oracle splats + oracle binning uploaded by the harness."""
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    pre, b, ref = oracle.render(scene, cam, bg)
+    rgb, T = gpu_blend_from(ctx, pre, b, cam.W, cam.H, bg, blend)
+    m = compare(rgb, T, ref)
+    assert m["max_unflagged"] <= MAX_ABS, m
+    assert m["psnr"] >= MIN_PSNR, m
+    assert m["over_within_bound"], m
+    assert m["T_max"] <= MAX_ABS, m
+
+
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT], ids=["tc", "direct"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_render_parity_end_to_end(case, blend):
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    rgb, T = gpu_render(ctx, scene, cam, bg, blend)
+    assert np.isfinite(rgb).all() and np.isfinite(T).all()
+    _, _, ref = oracle.render(scene, cam, bg)
+    m = compare(rgb, T, ref)
+    print(case, blend, m)
+    assert m["max_unflagged"] <= MAX_ABS, m
+    assert m["psnr"] >= MIN_PSNR, m
+    assert m["over_within_bound"], m
+
+
+def test_exponent_precision_bound():
+    """|d ln alpha| of the tensor-core exponent (TF32 hi/lo, reading R-11) stays
+    below the delta_a the margin mask assumes, on every pair the oracle keeps."""
+    import torch
+    scene, cam, bg = _cfg("C2")
+    ctx = make_ctx(scene, cam)
+    pre = oracle.preprocess(scene, cam)
+    b = oracle.binning(pre, cam.W, cam.H)
+    gx = (cam.W + 15) // 16
+    # a sample of tiles keeps the dump small
+    rng = np.random.default_rng(0)
+    ranges = np.zeros_like(b["ranges"])
+    sel = rng.choice(len(ranges), 64, replace=False)
+    ranges[sel] = b["ranges"][sel]
+    K = b["K"]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out_m = torch.full((K, 256), float("nan"), device="cuda")
+    ctx.gs_debug_exponents(scene.n, t(pre["xy"]), t(pre["conic"]), t(pre["opacity"]), t(b["vals"].view(np.int32)),
+                           K, t(ranges.view(np.int32)), cam.W, cam.H, out_m)
+    m = out_m.cpu().numpy()
+    worst, n_pairs = 0.0, 0
+    lanes = np.arange(256)
+    w, l = lanes // 32, lanes % 32
+    px_in = 8 * (w % 2) + l % 8
+    py_in = 4 * (w // 2) + l // 8
+    for tsel in sel:
+        s, e = b["ranges"][tsel]
+        if e == s:
+            continue
+        tx, ty = tsel % gx, tsel // gx
+        px = 16 * tx + px_in
+        py = 16 * ty + py_in
+        idx = b["vals"][s:e]
+        xy = pre["xy"][idx].astype(np.float64)
+        co = pre["conic"][idx].astype(np.float64)
+        o = pre["opacity"][idx].astype(np.float64)
+        dx = xy[:, 0:1] - px[None, :]
+        dy = xy[:, 1:2] - py[None, :]
+        power = -0.5 * (co[:, 0:1] * dx * dx + co[:, 2:3] * dy * dy) - co[:, 1:2] * dx * dy
+        ln_a = np.log(o)[:, None] + power
+        keep = ln_a >= np.log(1 / 255.0)
+        got = m[s:e] * np.log(2.0)
+        d = np.abs(got - ln_a)[keep]
+        n_pairs += d.size
+        if d.size:
+            worst = max(worst, float(d.max()))
+    print(f"max |d ln alpha| = {worst:.3e} over {n_pairs} kept pairs")
+    assert n_pairs > 10000
+    assert worst <= oracle.DELTA_A
+
+
+def test_determinism_and_tc_vs_direct():
+    scene, cam, bg = _cfg("C2")
+    ctx = make_ctx(scene, cam)
+    a, ta = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC)
+    b, tb = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC)
+    assert np.array_equal(a, b) and np.array_equal(ta, tb)
+    c, _ = gpu_render(ctx, scene, cam, bg, GS_BLEND_DIRECT)
+    assert 10 * np.log10(1 / max(((a - c) ** 2).mean(), 1e-30)) >= MIN_PSNR
+
+
+def test_empty_scene_is_background():
+    scene = synth.object_scene(0, 0, sh_degree=0)
+    cam = synth.look_at((0, 0, -4), (0, 0, 0), 40, 24, 0.7)
+    ctx = make_ctx(scene, cam, max_keys=1024)
+    rgb, T = gpu_render(ctx, scene, cam, (0.1, 0.2, 0.3))
+    for ch, v in enumerate((0.1, 0.2, 0.3)):
+        assert (rgb[ch] == np.float32(v)).all()
+    assert (T == 1.0).all()
+
+
+def test_all_culled_scene_is_background():
+    scene = synth.object_scene(500, 3, sh_degree=1)
+    scene.means[:] = np.array([0, 0, -10], np.float32)        # behind the camera at z=-4
+    cam = synth.look_at((0, 0, -4), (0, 0, 0), 48, 48, 0.7)
+    ctx = make_ctx(scene, cam, max_keys=1024)
+    rgb, T = gpu_render(ctx, scene, cam, (0.5, 0.5, 0.5))
+    assert (rgb == np.float32(0.5)).all() and (T == 1.0).all()
+
+
+def test_capacity_error_is_reported_not_truncated():
+    scene, cam, bg = _cfg("C1")
+    ctx = make_ctx(scene, cam, max_keys=100)
+    with pytest.raises(GsError) as e:
+        gpu_render(ctx, scene, cam, bg)
+    assert e.value.code == -3
+    st = ctx.gs_last_stats()
+    assert st.n_keys == oracle.binning(oracle.preprocess(scene, cam), cam.W, cam.H)["K"]
+
+
+@pytest.mark.slow
+def test_full_size_c5_view_sampled_parity():
+    """BASELINE.json configs[4] shape at full size (6M Gaussians, 1920x1080), the
+    launch configuration bench.py times: preprocess and binning bit-exact over
+    everything; pixels on 48 sampled tiles against the oracle."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device
+    scene, cams, bg = synth.make_config("C5", views=64)
+    cam = cams[0]
+    ctx = Context(0, max_points=scene.n, max_keys=64 << 20, max_w=cam.W, max_h=cam.H)
+    st = scene_to_device(scene)
+    got = gpu_preprocess(ctx, scene, cam, st)
+    pre = oracle.preprocess(scene, cam)
+    for k in BIT_EXACT_KEYS:
+        a = got[k].view(np.uint32) if got[k].dtype == np.float32 else got[k].astype(np.int64)
+        b = pre[k].view(np.uint32) if pre[k].dtype == np.float32 else pre[k].astype(np.int64)
+        assert np.array_equal(a, b), k
+    code, K, gb = gpu_binning(ctx, scene, cam, capacity=64 << 20, st=st)
+    assert code == 0
+    ref_b = oracle.binning(pre, cam.W, cam.H)
+    assert K == ref_b["K"]
+    assert np.array_equal(gb["keys"], ref_b["keys"]) and np.array_equal(gb["vals"], ref_b["vals"])
+    assert np.array_equal(gb["ranges"], ref_b["ranges"])
+    rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st)
+    rng = np.random.default_rng(7)
+    ntiles = len(ref_b["ranges"])
+    sel = rng.choice(ntiles, 48, replace=False)
+    r2 = np.zeros_like(ref_b["ranges"])
+    r2[sel] = ref_b["ranges"][sel]
+    b2 = dict(ref_b); b2["ranges"] = r2
+    ref = oracle.blend(pre, b2, cam.W, cam.H, bg)
+    gx = (cam.W + 15) // 16
+    mask = np.zeros((cam.H, cam.W), bool)
+    for t in sel:
+        mask[16 * (t // gx):16 * (t // gx) + 16, 16 * (t % gx):16 * (t % gx) + 16] = True
+    err = np.abs(rgb - ref["rgb"])[:, mask]
+    ok = ~ref["flag"][mask]
+    assert err[:, ok].max() <= MAX_ABS
+    mse = float((err ** 2).mean())
+    assert 10 * np.log10(1 / max(mse, 1e-30)) >= MIN_PSNR
