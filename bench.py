@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark: forward 3DGS render with GEMM-compatible blending on B200.
+
+Workload (BASELINE.json configs[4]): 6M Gaussians (SH degree 3) rendered at
+1920x1080 from a 64-view camera orbit, views partitioned across the GPUs of
+one node (one process per GPU), finished frames gathered to rank 0 over NCCL.
+A step = the whole 64-view orbit (strong scaling: total work is fixed).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints one JSON line (rank 0). `--impl reference` times the CPU oracle (the
+only reference this tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1080p per B200 and 8-GPU; tensor-pipe % and HBM GB/s"
+UNIT = "frames/s"
+WORKLOAD = "C5: 6M Gaussians SH3, 1920x1080, 64-view orbit (BASELINE.json configs[4])"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    """The oracle (oracle/, plain CPU) on a bounded sample of the same workload:
+    each step renders one full 1920x1080 view of the C5 scene (preprocess,
+    binning, f64 blending) on all host cores. Rank 0 only."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import oracle
+    from paper_2604_02120_b200 import synth
+    scene, cams, bg = synth.make_config("C5", views=args.views)
+    threads = os.cpu_count() or 1
+    times = []
+    for k in range(args.warmup + args.steps):
+        cam = cams[(k * 16) % len(cams)]
+        t0 = time.perf_counter()
+        oracle.render(scene, cam, bg, threads=threads, mask=False)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    mean = sum(times) / len(times)
+    value = 1.0 / mean
+    sample = f"one full 1920x1080 view of the C5 scene per step (views 0,16,32,48 cycled), {threads} threads"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "views": args.views, "sample": "1 view per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(scene, cam, bg):
+    """Oracle timed on the host cores on one view of the same workload (~10-20 s)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.render(scene, cam, bg, threads=threads, mask=False)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"one 1920x1080 view (view 0) of the C5 scene, {dt:.1f} s with {threads} threads"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIMING, Context,
+                                       camera, opts, scene_to_device, scene_to_host, synth)
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert args.views % ws == 0, "views must divide evenly across ranks"
+    scene, cams, bg = synth.make_config("C5", views=args.views)
+    W, H = cams[0].W, cams[0].H
+    per = args.views // ws
+    my_cams = [camera(c) for c in cams[rank * per:(rank + 1) * per]]
+    blend = GS_BLEND_DIRECT if args.blend == "direct" else GS_BLEND_TC
+    ctx = Context(local, max_points=scene.n, max_keys=args.max_keys, max_w=W, max_h=H)
+    st = scene_to_device(scene)
+    out_rgb = torch.empty((per, 3, H, W), device="cuda")
+    out_T = torch.empty((per, H, W), device="cuda")
+    gather_rgb = gather_T = None
+    if ws > 1 and rank == 0:
+        gather_rgb = [torch.empty_like(out_rgb) for _ in range(ws)]
+        gather_T = [torch.empty_like(out_T) for _ in range(ws)]
+    o_plain = opts(bg, sh_degree=scene.sh_degree, blend=blend)
+    o_timed = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=GS_FLAG_TIMING)
+    stream = torch.cuda.current_stream()
+
+    def step(o):
+        ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
+        if ws > 1:
+            dist.gather(out_rgb, gather_rgb, dst=0)
+            dist.gather(out_T, gather_T, dst=0)
+
+    for _ in range(args.warmup):
+        step(o_plain)
+    torch.cuda.synchronize()
+    ctx.gs_last_stats()
+    ctx.gs_stage_times()                       # reset
+    launches0 = ctx.gs_last_stats().launches
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(o_timed)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    stage_ms, frames = ctx.gs_stage_times()
+    launches = ctx.gs_last_stats().launches - launches0
+    if ws > 1:
+        t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = args.views * args.steps / (elapsed_ms / 1e3)
+
+    # --- per-frame work counts for the roofline (one counting pass, untimed) ---
+    o_stats = opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_TC, flags=GS_FLAG_STATS)
+    n_eval = n_kept = n_keys = n_vis = 0
+    sample_views = my_cams[:: max(1, per // 8)]
+    for c in sample_views:
+        ctx.gs_render(st, c, W, H, o_stats, out_rgb[0], out_T[0], stream)
+        s = ctx.gs_last_stats()
+        n_eval += s.pairs_evaluated
+        n_kept += s.pairs_kept
+        n_keys += s.n_keys
+        n_vis += s.n_visible
+    nv = len(sample_views)
+    n_eval, n_kept, n_keys, n_vis = n_eval / nv, n_kept / nv, n_keys / nv, n_vis / nv
+    pre_ms, bin_ms, blend_ms = (m / max(frames, 1) for m in stage_ms)
+
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs") or 6650.0
+    smax = peaks.get("sm_max_mhz") or 1965.0
+    fp32_peak = 148 * 128 * 2 * smax * 1e6 / 1e12        # TFLOP/s, FP32 FMA on the CUDA cores
+    N = scene.n
+    M = scene.shs.shape[1]
+    # algorithmic bytes: preprocess reads the means of every
+    # Gaussian and the rest of the inputs of the projected ones, writes 60 B each
+    pre_bytes = N * 12 + n_vis * (12 + 16 + 4 + 12 * M) + N * 60
+    # binning: compaction (read touched+depth, write 8 B/vis), 4 depth passes (16 B/vis each
+    # + a histogram read), duplication (8 B/key written), tile sort 2 passes (16 B/key each
+    # + histogram read), ranges (4 B/key)
+    bin_bytes = N * 8 + n_vis * 8 + 4 * 16 * n_vis + 4 * n_vis + n_vis * 12 + n_keys * 8 + \
+        2 * 16 * n_keys + 4 * n_keys + 4 * n_keys
+    # blend: 13 flop per evaluated (Gaussian, pixel) exponent (Eq. 6 dot product + skip
+    # test) and 12 flop per kept pair (alpha, clamp, T update, stop test, colour)
+    blend_flop = 13.0 * n_eval + 12.0 * n_kept
+    stages = {
+        "preprocess": {"ms": pre_ms, "bound": "hbm", "achieved": pre_bytes / (pre_ms * 1e-3) / 1e9,
+                       "peak": hbm, "unit": "GB/s"},
+        "binning": {"ms": bin_ms, "bound": "hbm", "achieved": bin_bytes / (bin_ms * 1e-3) / 1e9, "peak": hbm,
+                    "unit": "GB/s", "kernels": "compaction, 4 depth passes, duplication, tile sort, ranges"},
+        "blend": {"ms": blend_ms, "bound": "alu", "achieved": blend_flop / (blend_ms * 1e-3) / 1e12,
+                  "peak": fp32_peak, "unit": "TFLOP/s", "pairs_evaluated": n_eval, "pairs_kept": n_kept},
+    }
+    for v in stages.values():
+        v["frac"] = v["achieved"] / v["peak"]
+    dom = max(stages, key=lambda k: stages[k]["ms"])
+    roof = dict(stages[dom])
+    roof = {"kernel": dom, "bound": roof["bound"], "achieved": roof["achieved"], "peak": roof["peak"],
+            "unit": roof["unit"], "frac": roof["frac"], "traffic": None}
+
+    # --- end to end through the host-pointer C-ABI entry point ---------------
+    e2e = None
+    if not args.no_e2e:
+        hs = scene_to_host(scene, pinned=True)
+        h_rgb = torch.empty((per, 3, H, W), pin_memory=True)
+        h_T = torch.empty((per, H, W), pin_memory=True)
+        ctx.gs_render_views_host(hs, my_cams, W, H, o_plain, h_rgb, h_T, stream)   # warm
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.gs_render_views_host(hs, my_cams, W, H, o_plain, h_rgb, h_T, stream)
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        in_bytes = sum(int(np.prod(a.shape)) * 4 for a in (scene.means, scene.scales, scene.rots,
+                                                              scene.opacity, scene.shs))
+        e2e = {"value": args.views * args.e2e_steps / dt, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
+               "d2h_bytes_per_step": per * 4 * W * H * 4, "steps": args.e2e_steps,
+               "note": "gs_render_views_host: pinned scene H2D + 64/N renders + frames D2H per rank per step"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cams[0], bg)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "views": args.views, "n_gaussians": N, "W": W, "H": H,
+                           "sh_degree": scene.sh_degree, "blend": args.blend,
+                           "parallelism": f"view-partition x{ws}" + (" + NCCL gather" if ws > 1 else ""),
+                           "l2": "inputs larger than L2 (1.42 GB scene, 2.1 GB of frames per step)"},
+                "ms_per_frame": elapsed_ms / args.steps / per, "stage_ms_per_frame": {
+                    k: v["ms"] for k, v in stages.items()},
+                "roofline": roof, "stages": stages, "clocks": clk,
+                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu,
+                "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
+                                   "pairs_kept": n_kept}}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--views", type=int, default=64)
+    ap.add_argument("--blend", default="tc", choices=["tc", "direct"])
+    ap.add_argument("--max-keys", type=int, default=48 << 20)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,7 +72,9 @@ enum {
 };
 
 enum {
-    GS_FLAG_SYNC = 1u     /* synchronise the stream at the end and report device errors     */
+    GS_FLAG_SYNC = 1u,    /* synchronise the stream at the end and report device errors     */
+    GS_FLAG_TIMING = 2u,  /* record CUDA events around the stages (read by gs_stage_times)  */
+    GS_FLAG_STATS = 4u    /* count blend work (pairs evaluated / kept) into gs_stats        */
 };
 
 typedef struct {
@@ -90,6 +92,9 @@ typedef struct {
     int64_t n_keys;        /* K = number of (Gaussian, tile) pairs                          */
     int64_t capacity_keys; /* max_keys of the context                                       */
     int status;            /* gs_status of the last frame (device-side checks included)     */
+    int64_t launches;      /* kernels launched by this context since creation              */
+    int64_t pairs_evaluated;  /* GS_FLAG_STATS: (Gaussian, pixel) exponents computed, last frame */
+    int64_t pairs_kept;       /* GS_FLAG_STATS: of those, alpha >= 1/255 on a live pixel       */
 } gs_stats;
 
 typedef struct gs_ctx gs_ctx;
@@ -130,6 +135,12 @@ int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
 /* Synchronises the last stream used by ctx and reports counts and the status
  * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */
 int gs_last_stats(gs_ctx *ctx, gs_stats *out);
+
+/* Sums of the per-stage device times (ms) of all frames rendered with
+ * GS_FLAG_TIMING since the previous call (synchronises): ms[0] preprocess,
+ * ms[1] binning (compaction, sorts, duplication, ranges), ms[2] blend.
+ * *frames receives the number of frames summed. Resets the sums. */
+int gs_stage_times(gs_ctx *ctx, double *ms, int64_t *frames);
 
 const char *gs_status_string(int status);
 

@@ -26,11 +26,13 @@ GS_ERR_NO_DEVICE = -6
 GS_BLEND_TC = 0
 GS_BLEND_DIRECT = 1
 GS_FLAG_SYNC = 1
+GS_FLAG_TIMING = 2
+GS_FLAG_STATS = 4
 
 # every entry point declared in include/gs_render.h
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
-           "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents")
+           "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times")
 
 
 class GsError(RuntimeError):
@@ -53,7 +55,8 @@ class gs_opts(ctypes.Structure):
 
 class gs_stats(ctypes.Structure):
     _fields_ = [("n_points", ctypes.c_int64), ("n_visible", ctypes.c_int64), ("n_keys", ctypes.c_int64),
-                ("capacity_keys", ctypes.c_int64), ("status", ctypes.c_int)]
+                ("capacity_keys", ctypes.c_int64), ("status", ctypes.c_int), ("launches", ctypes.c_int64),
+                ("pairs_evaluated", ctypes.c_int64), ("pairs_kept", ctypes.c_int64)]
 
 
 _lib = None
@@ -83,6 +86,7 @@ def load():
                              ctypes.POINTER(I64)],
         "gs_debug_blend": [P, P, I, P, P, P, P, P, I64, P, I, I, opt_p, P, P],
         "gs_debug_exponents": [P, P, I, P, P, P, P, I64, P, I, I, P],
+        "gs_stage_times": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -195,6 +199,13 @@ class Context:
         st = gs_stats()
         _check(self.lib.gs_last_stats(self.h, ctypes.byref(st)), "gs_last_stats")
         return st
+
+    def gs_stage_times(self):
+        """(preprocess_ms, binning_ms, blend_ms) summed over GS_FLAG_TIMING frames, and the frame count."""
+        ms = (ctypes.c_double * 3)()
+        fr = ctypes.c_int64(0)
+        _check(self.lib.gs_stage_times(self.h, ms, ctypes.byref(fr)), "gs_stage_times")
+        return tuple(ms), fr.value
 
     # --- test entry points ---------------------------------------------------
     def gs_debug_preprocess(self, scene_t, cam, W, H, o, outs, stream=None):

@@ -63,12 +63,13 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                  : "memory");
 }
 
-template <bool DUMP>
+template <bool DUMP, bool STATS>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W,
                int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
-               float *__restrict__ dump_m, uint32_t *tile_queue) {
+               float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
+               unsigned long long *stat_kept) {
     extern __shared__ uint8_t smem_raw[];
     SmemTC &sm = *reinterpret_cast<SmemTC *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         const uint32_t b_base = smem_u32(&sm.B[0][0]);
         uint32_t s = 0, ph = 0;
         uint32_t seq = 0;
+        unsigned long long n_eval = 0;
         for (;;) {
             int tile = 0;
             if (lane == 0) tile = (int)atomicAdd(tile_queue, 1u);
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 if (lane == 0) sm.hdr[s] = make_int4(-1, 0, 0, 0);
                 mbar_arrive(&sm.full[s]);
                 if (lane == 0) mbar_arrive(&sm.full[s]);
+                if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
                 break;
             }
             seq++;
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                     sm.rgb[s][lane] = col;
                 }
                 if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, (int)cnt, (int)b0);
+                if (STATS && lane == 0) n_eval += (unsigned long long)cnt * GS_TILE_PIX;
                 fence_proxy_async_smem();
                 mbar_arrive(&sm.full[s]);
                 __syncwarp();
@@ -202,12 +206,21 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         uint32_t s = 0, ph = 0;
         float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
         bool done = false, wdone = false;
+        uint32_t n_kept = 0;
         for (;;) {
             mbar_wait(&sm.full[s], ph);
             tc_fence_after();
             const int4 hd = sm.hdr[s];
             if (hd.z == 0) {
-                if (hd.x < 0) break;
+                if (hd.x < 0) {
+                    if (STATS) {
+                        unsigned long long k = n_kept;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+                        if (lane == 0) atomicAdd(stat_kept, k);
+                    }
+                    break;
+                }
                 if (!DUMP) {
                     const int px = GS_TILE * (hd.x % gx) + x, py = GS_TILE * (hd.x / gx) + y;
                     if (px < W && py < H) {
@@ -237,6 +250,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                                 const float a = fminf(ALPHA_MAX, ex2_approx(mj));
                                 const float tT = T * (1.0f - a);
                                 if (live) {
+                                    if (STATS) n_kept++;
                                     if (tT < T_MIN) {
                                         done = true;
                                     } else {
@@ -272,22 +286,31 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
-                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms) {
+                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
+                     bool stats) {
     const size_t smem = sizeof(SmemTC) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_blend_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     const int grid = std::max(1, std::min(2 * num_sms, ntiles));
     uint32_t *queue = &ws.counters->tile_queue;
+    unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
     if (dump_m)
-        k_blend_tc<true><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0],
-                                                          bg[1], bg[2], out_rgb, out_T, dump_m, queue);
+        k_blend_tc<true, false><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
+                                                                 bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
+                                                                 se, sk);
+    else if (stats)
+        k_blend_tc<false, true><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
+                                                                 bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
+                                                                 se, sk);
     else
-        k_blend_tc<false><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0],
-                                                           bg[1], bg[2], out_rgb, out_T, dump_m, queue);
+        k_blend_tc<false, false><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
+                                                                  bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
+                                                                  se, sk);
 }
 
 // ===========================================================================

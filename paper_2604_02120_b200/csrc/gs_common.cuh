@@ -17,12 +17,15 @@ struct Counters {
     uint32_t n_visible;        // compaction output
     uint32_t err;              // device-side error bits (1 = key capacity)
     uint64_t n_keys;           // K (64-bit: the capacity check is exact)
-    uint32_t tickets[16];      // onesweep / scan chunk tickets, one per pass
+    uint32_t n_big;            // tiles whose list exceeds the small-sort capacity
+    uint32_t n_huge;           // tiles whose list exceeds the big-sort capacity
     uint32_t tile_queue;       // blend persistent work queue
-    uint32_t pad[7];
-    uint32_t hist_depth[4][256];
-    uint32_t hist_tile[4][256];
+    uint32_t pad[5];
+    unsigned long long pairs_eval;   // GS_FLAG_STATS: exponents computed by the blend
+    unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
+
+constexpr int MAX_TILES = 32768;   // shared-memory tile histograms (128 KB)
 
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
@@ -34,18 +37,17 @@ struct Workspace {
     ushort4 *rect;             // [N] (xmin, ymin, xmax, ymax) tiles, half-open
     uint32_t *touched;         // [N] tiles touched (0 = culled)
     int32_t *radius;           // [N] pixel radius (debug output)
-    uint32_t *sk[2];           // [N] depth-sort keys, ping-pong
-    uint32_t *sv[2];           // [N] depth-sort values (Gaussian index)
-    uint32_t *offsets;         // [N] exclusive scan of touched in depth order
     // per key (max_keys)
-    uint32_t *kt[2];           // [K] tile ids, ping-pong
-    uint32_t *kv[2];           // [K] Gaussian indices, ping-pong
+    uint32_t *kv[2];           // [K] Gaussian indices: kv[0] scattered per tile, kv[1] sorted
+    uint32_t *kt[2];           // [K] key scratch for the rare over-long tile lists
     // per tile
-    uint32_t *tile_count;      // [tiles]
-    uint2 *ranges;             // [tiles]
-    // lookback status (epoch-tagged, never memset)
-    unsigned long long *scan_status;   // [max chunks]
-    unsigned long long *sort_status;   // [max chunks * 256]
+    uint32_t *cnt;             // [count_blocks][tiles] block-private counts -> prefixes
+    uint32_t *tile_total;      // [tiles]
+    uint32_t *tile_start;      // [tiles]
+    uint2 *ranges;             // [tiles] [start, end) into kv[1]
+    uint32_t *big_list;        // [tiles]
+    uint32_t *huge_list;       // [tiles]
+    int count_blocks;          // fixed partition of the Gaussians for count/scatter
     Counters *counters;
     // scene staging for the host-pointer entry point
     float *stage;
@@ -198,11 +200,12 @@ namespace gs {
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
                        int sh_stride, float scale_mod, const gs_camera &cam, int W, int H);
-void launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
-                    uint32_t &epoch);
+int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
+                   uint32_t &epoch);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
-                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms);
+                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
+                     bool stats);
 void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
                          const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *counters);

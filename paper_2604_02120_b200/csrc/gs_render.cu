@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "gs_common.cuh"
 
@@ -21,7 +22,15 @@ struct gs_ctx {
     int64_t last_n = 0;
     int last_status = GS_OK;
     float *frame_rgb = nullptr, *frame_T = nullptr;   // staging for the host entry point
+    int64_t launches = 0;                             // kernels launched (gs_stats.launches)
+    // GS_FLAG_TIMING: a pool of 4 events per frame, drained by gs_stage_times
+    std::vector<cudaEvent_t> ev;
+    int ev_used = 0;
+    double stage_ms[3] = {0, 0, 0};
+    int64_t timed_frames = 0;
 };
+
+static constexpr int kEventFrames = 256;
 
 namespace {
 
@@ -40,15 +49,6 @@ int check_cuda(cudaError_t e) {
     return GS_OK;
 }
 
-void maybe_reset_epoch(gs_ctx *c, cudaStream_t st) {
-    if (c->epoch > 0xFFFF00u) {   // 24-bit epoch tag in the look-back status words
-        const int64_t nch = gs::ceil_div_i(std::max<int64_t>(c->max_points, c->max_keys), gs::SORT_CHUNK) + 1;
-        cudaMemsetAsync(c->ws.scan_status, 0, sizeof(unsigned long long) * nch, st);
-        cudaMemsetAsync(c->ws.sort_status, 0, sizeof(unsigned long long) * nch * 256, st);
-        c->epoch = 0;
-    }
-}
-
 int validate(gs_ctx *c, int N, const void *means, const void *scales, const void *rots, const void *opacity,
              const void *shs, const gs_camera *cam, int W, int H, const gs_opts *o) {
     if (!c || !cam || !o || N < 0 || W <= 0 || H <= 0) return GS_ERR_INVALID_ARG;
@@ -62,14 +62,41 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
 }
 
 // preprocess + binning of one view into the workspace (counters zeroed first)
+void drain_events(gs_ctx *c) {
+    for (int f = 0; f < c->ev_used; f++) {
+        cudaEventSynchronize(c->ev[4 * f + 3]);
+        for (int k = 0; k < 3; k++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev[4 * f + k], c->ev[4 * f + k + 1]);
+            c->stage_ms[k] += ms;
+        }
+    }
+    c->timed_frames += c->ev_used;
+    c->ev_used = 0;
+}
+
+void mark(gs_ctx *c, cudaStream_t st, const gs_opts &o, int k) {
+    if (!(o.flags & GS_FLAG_TIMING)) return;
+    if (c->ev.empty()) {
+        c->ev.resize(4 * kEventFrames);
+        for (auto &e : c->ev) cudaEventCreate(&e);
+    }
+    if (k == 0 && c->ev_used == kEventFrames) drain_events(c);
+    cudaEventRecord(c->ev[4 * c->ev_used + k], st);
+    if (k == 3) c->ev_used++;
+}
+
 void enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
                    const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
-    maybe_reset_epoch(c, st);
+    mark(c, st, o, 0);
     cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
                           o.scale_modifier, cam, W, H);
+    c->launches += N > 0 ? 1 : 0;
+    mark(c, st, o, 1);
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
-    gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch);
+    c->launches += gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch);
+    mark(c, st, o, 2);
 }
 
 void enqueue_blend(gs_ctx *c, cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
@@ -81,7 +108,8 @@ void enqueue_blend(gs_ctx *c, cudaStream_t st, const float2 *xy, const float4 *c
                                 c->ws.counters);
     else
         gs::launch_blend_tc(c->ws, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
-                            dump, c->num_sms);
+                            dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
+    c->launches += 1;
 }
 
 int finish(gs_ctx *c, cudaStream_t st, const gs_opts &o, int64_t N) {
@@ -126,11 +154,12 @@ __global__ void k_unpack_pre(int N, gs::Workspace ws, float *depth, float *xy, f
     touched[i] = ws.touched[i];
 }
 
-__global__ void k_keys_out(int64_t K, const uint32_t *tiles, const uint32_t *idx, const uint32_t *depth_bits,
-                           uint64_t *keys, uint32_t *vals) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_keys_out(const uint2 *ranges, const uint32_t *idx, const uint32_t *depth_bits, uint64_t *keys,
+                           uint32_t *vals) {
+    const uint2 rg = ranges[blockIdx.x];
+    for (uint32_t k = rg.x + threadIdx.x; k < rg.y; k += blockDim.x) {
         const uint32_t i = idx[k];
-        keys[k] = ((uint64_t)tiles[k] << 32) | depth_bits[i];
+        keys[k] = ((uint64_t)blockIdx.x << 32) | depth_bits[i];
         vals[k] = i;
     }
 }
@@ -165,6 +194,8 @@ int gs_device_arch(int device) {
 int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys, int max_w, int max_h) {
     if (!out || max_points < 0 || max_keys < 0 || max_w <= 0 || max_h <= 0) return GS_ERR_INVALID_ARG;
     if (max_keys >= (int64_t)1 << 32 || max_points >= (int64_t)1 << 31) return GS_ERR_INVALID_ARG;
+    if ((int64_t)gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE) > gs::MAX_TILES)
+        return GS_ERR_INVALID_ARG;
     *out = nullptr;
     const int arch = gs_device_arch(device);
     if (arch < 0) return arch;
@@ -179,21 +210,19 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     c->max_w = max_w;
     c->max_h = max_h;
     c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
-    const size_t N = (size_t)max_points, K = (size_t)max_keys;
-    const size_t nch = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1;
+    const size_t N = (size_t)max_points, K = (size_t)max_keys, T = (size_t)c->max_tiles;
     gs::Workspace &w = c->ws;
+    w.count_blocks = 2 * c->num_sms;
     cudaError_t e = cudaSuccess;
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
     A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
-    A(w.radius, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.offsets, N);
-    A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K);
-    A(w.tile_count, c->max_tiles); A(w.ranges, c->max_tiles);
-    A(w.scan_status, nch); A(w.sort_status, nch * 256);
+    A(w.radius, N);
+    A(w.kv[0], K); A(w.kv[1], K); A(w.kt[0], K); A(w.kt[1], K);
+    A(w.cnt, (size_t)w.count_blocks * T); A(w.tile_total, T); A(w.tile_start, T); A(w.ranges, T);
+    A(w.big_list, T); A(w.huge_list, T);
     A(w.counters, 1);
 #undef A
-    if (e == cudaSuccess) e = cudaMemset(w.scan_status, 0, sizeof(unsigned long long) * nch);
-    if (e == cudaSuccess) e = cudaMemset(w.sort_status, 0, sizeof(unsigned long long) * nch * 256);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         gs_ctx_destroy(c);
@@ -208,11 +237,12 @@ int gs_ctx_destroy(gs_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     gs::Workspace &w = c->ws;
-    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
-                    w.sv[0], w.sv[1], w.offsets, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.tile_count,
-                    w.ranges, w.scan_status, w.sort_status, w.counters, w.stage, c->frame_rgb, c->frame_T};
+    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.kv[0], w.kv[1],
+                    w.kt[0], w.kt[1], w.cnt, w.tile_total, w.tile_start, w.ranges, w.big_list, w.huge_list,
+                    w.counters, w.stage, c->frame_rgb, c->frame_T};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (auto &e : c->ev) cudaEventDestroy(e);
     delete c;
     return GS_OK;
 }
@@ -226,8 +256,9 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
-    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb, out_T,
+    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[1], c->ws.ranges, W, H, *o, out_rgb, out_T,
                   nullptr);
+    mark(c, st, *o, 3);
     return finish(c, st, *o, N);
 }
 
@@ -307,8 +338,24 @@ int gs_last_stats(gs_ctx *c, gs_stats *out) {
     out->n_keys = (int64_t)h.n_keys;
     out->capacity_keys = c->max_keys;
     out->status = (h.err & 1u) ? GS_ERR_CAPACITY : c->last_status;
+    out->launches = c->launches;
+    out->pairs_evaluated = (int64_t)h.pairs_eval;
+    out->pairs_kept = (int64_t)h.pairs_kept;
     c->last_status = out->status;
     return GS_OK;
+}
+
+int gs_stage_times(gs_ctx *c, double *ms, int64_t *frames) {
+    if (!c || !ms) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    drain_events(c);
+    for (int k = 0; k < 3; k++) {
+        ms[k] = c->stage_ms[k];
+        c->stage_ms[k] = 0;
+    }
+    if (frames) *frames = c->timed_frames;
+    c->timed_frames = 0;
+    return check_cuda(cudaGetLastError());
 }
 
 int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
@@ -342,8 +389,7 @@ int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const
     if (s.status) return s.status;
     if (s.n_keys > capacity) return GS_ERR_CAPACITY;
     const int ntiles = gs::ceil_div_i(W, GS_TILE) * gs::ceil_div_i(H, GS_TILE);
-    if (s.n_keys > 0)
-        k_keys_out<<<c->num_sms * 4, 256, 0, st>>>(s.n_keys, c->ws.kt[0], c->ws.kv[0], c->ws.depth_bits, keys, vals);
+    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[1], c->ws.depth_bits, keys, vals);
     cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
     if (check_cuda(cudaStreamSynchronize(st))) return GS_ERR_CUDA;
     return GS_OK;
@@ -359,9 +405,11 @@ static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, c
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
-    if (N > 0)
+    if (N > 0) {
         k_pack_splats<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, xy, conic, opacity, rgb, c->ws.xy, c->ws.conic_o,
                                                               c->ws.rgb);
+        c->launches++;
+    }
     enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
                   *o, out_rgb, out_T, dump);
     return finish(c, st, *o, N);

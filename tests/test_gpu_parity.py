@@ -51,7 +51,24 @@ def _adversarial():
     return scene, cam, np.array([0.0, 0.0, 0.0], np.float32)
 
 
-CASES = {"C1": lambda: _cfg("C1"), "C2": lambda: _cfg("C2"), "ragged": _ragged, "adversarial": _adversarial}
+def _dense():
+    """Tile lists longer than the shared-memory sort capacities: ~40k Gaussians in
+    a few tiles (global chunked sort path) and ~8k in others (1024-thread path)."""
+    rng = np.random.default_rng(104)
+    a = synth.object_scene(40000, 105, sh_degree=1)
+    a.means[:] = rng.normal(0.0, 0.02, (40000, 3)).astype(np.float32)
+    a.scales[:] = 0.004
+    b = synth.object_scene(8000, 106, sh_degree=1)
+    b.means[:] = (np.array([0.9, 0.6, 0.0]) + rng.normal(0.0, 0.03, (8000, 3))).astype(np.float32)
+    b.scales[:] = 0.004
+    scene = synth.Scene(*[np.concatenate([getattr(p, f) for p in (a, b)]) for f in
+                          ("means", "scales", "rots", "opacity", "shs")], 1)
+    cam = synth.look_at((0.0, 0.0, -4.0), (0, 0, 0), 96, 96, 0.7)
+    return scene, cam, np.array([0.3, 0.3, 0.3], np.float32)
+
+
+CASES = {"C1": lambda: _cfg("C1"), "C2": lambda: _cfg("C2"), "ragged": _ragged, "adversarial": _adversarial,
+         "dense": _dense}
 
 
 @pytest.mark.parametrize("case", list(CASES))
