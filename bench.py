@@ -145,33 +145,28 @@ def run_ours(args):
 
     from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIMING, Context,
                                        camera, opts, scene_to_device, scene_to_host, synth)
+    from paper_2604_02120_b200.orbit import gather_frames, partition_views
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    assert args.views % ws == 0, "views must divide evenly across ranks"
     scene, cams, bg = synth.make_config("C5", views=args.views)
     W, H = cams[0].W, cams[0].H
-    per = args.views // ws
-    my_cams = [camera(c) for c in cams[rank * per:(rank + 1) * per]]
+    mine = partition_views(args.views, ws, rank)
+    per = len(mine)
+    my_cams = [camera(cams[v]) for v in mine]
     blend = GS_BLEND_DIRECT if args.blend == "direct" else GS_BLEND_TC
     ctx = Context(local, max_points=scene.n, max_keys=args.max_keys, max_w=W, max_h=H)
     st = scene_to_device(scene)
     out_rgb = torch.empty((per, 3, H, W), device="cuda")
     out_T = torch.empty((per, H, W), device="cuda")
-    gather_rgb = gather_T = None
-    if ws > 1 and rank == 0:
-        gather_rgb = [torch.empty_like(out_rgb) for _ in range(ws)]
-        gather_T = [torch.empty_like(out_T) for _ in range(ws)]
     o_plain = opts(bg, sh_degree=scene.sh_degree, blend=blend)
     o_timed = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=GS_FLAG_TIMING)
     stream = torch.cuda.current_stream()
 
     def step(o):
         ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
-        if ws > 1:
-            dist.gather(out_rgb, gather_rgb, dst=0)
-            dist.gather(out_T, gather_T, dst=0)
+        gather_frames(out_rgb, out_T, ws, rank, dist)    # NCCL frame gather to rank 0
 
     for _ in range(args.warmup):
         step(o_plain)

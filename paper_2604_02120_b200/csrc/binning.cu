@@ -1,34 +1,35 @@
 // binning.cu -- stages (b) "Duplication" and (c) "Sorting"
-// and the per-tile ranges, as hand-written kernels (no CUB, no host sync).
+// and the per-tile ranges, as hand-written kernels (no CUB, no host
+// synchronisation: every count stays on the device, so a frame is
+// graph-capturable).
 //
-// Canonical result (R-12/R-13): per tile, the indices of the
-// Gaussians whose rectangle contains it, ascending in (depth bits, index);
-// key = tile << 32 | depth bits. The paper's "duplicate with a concatenated
-// key, then radix-sort" is realised B200-first as a bucket sort
-// on the tile (the high key half) followed by per-tile shared-memory sorts on
-// the depth (the low half), which yields exactly the same sorted key array:
-//   1. k_count    : block-private shared-memory histograms of tile hits over a
-//                   fixed contiguous partition of the Gaussians -> cnt[block][tile]
-//   2. k_colscan  : per tile, exclusive prefix over blocks (coalesced over tiles)
-//   3. k_tilescan : exclusive scan over tiles -> ranges, K, capacity check
-//   4. k_scatter  : same partition; shared-memory cursors give every (Gaussian,
-//                   tile) pair a slot inside its tile's segment (order within a
-//                   segment is arbitrary at this point)
-//   5. k_sort_*   : per tile, LSD radix sort of (depth bits, slot) pairs in
-//                   shared memory (<= 4096 and <= 16384 entries), or a chunked
-//                   global-memory block sort for longer lists; equal-depth runs
-//                   are then ordered by Gaussian index.
-// Traffic: ~24 B per Gaussian + ~16 B per key (vs ~150 B/key for a 6-pass LSD
-// sort of 64-bit keys).
+// Canonical result (R-12/R-13): the (Gaussian, tile) pairs sorted by
+// key = tile << 32 | depth bits, ties by Gaussian index. The paper's
+// "duplicate with a concatenated key, then radix-sort" over 64-bit
+// keys costs ~6 LSD passes over every pair; here the depth half is sorted once
+// per *Gaussian* instead of once per pair:
+//   1. compaction of the visible Gaussians (order-preserving scan)
+//   2. stable LSD sort of the N_vis depth keys, 4 passes of 8 bits (ties keep
+//      index order)
+//   3. scan of tiles_touched in depth order -> pair offsets, K, capacity check,
+//      and the first Gaussian of every 4096-pair chunk
+//   4. stable LSD sort of the pairs on the tile id (1-2 passes of 8 bits); the
+//      first pass *generates* the pairs in depth order from the offsets
+//      (load-balanced expansion: max-scan of segment heads), so the duplicated
+//      array is never materialised unsorted
+//   5. tile ranges by boundary detection.
+// Every scan / radix pass is reduce-then-scan over 4096-element chunks:
+// count (per-warp ballot multisplit, no atomics) -> scan of the
+// [digit][chunk] count matrix -> stable scatter through shared memory. No
+// block ever waits on another block (a decoupled look-back variant spent
+// most of its time spinning on its predecessors).
 #include <algorithm>
 
 #include "gs_common.cuh"
 
 namespace gs {
 
-constexpr int CNT_THREADS = 512;
-constexpr int SMALL_CAP = 4096, SMALL_THREADS = 256;
-constexpr int BIG_CAP = 16384, BIG_THREADS = 1024;
+constexpr int NWARP = SORT_THREADS / 32;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -36,69 +37,131 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// ---------------------------------------------------------------------------
-// 1. per-block tile histograms
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CNT_THREADS) k_count(int N, const uint32_t *__restrict__ touched,
-                                                       const ushort4 *__restrict__ rect, int gx, int ntiles,
-                                                       uint32_t *__restrict__ cnt) {
-    extern __shared__ uint32_t s_h[];
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_h[t] = 0;
-    __syncthreads();
-    const int per = ceil_div_i(N, gridDim.x);
-    const int i0 = blockIdx.x * per, i1 = min(N, i0 + per);
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        if (touched[i] == 0) continue;
-        const ushort4 r = rect[i];
-        for (int ty = r.y; ty < r.w; ty++)
-            for (int tx = r.x; tx < r.z; tx++) atomicAdd(&s_h[ty * gx + tx], 1u);
+// Element e of a 4096-element chunk lives in warp e/512, round (e/32)%16, lane e%32:
+// each warp owns a contiguous range, so warp-local ranking in round order is stable.
+__device__ __forceinline__ int elem_of(int w, int r, int lane) { return w * (SORT_ITEMS * 32) + r * 32 + lane; }
+
+// Warp multisplit on an 8-bit digit: mask of the lanes holding the same digit.
+// 8 ballots: 0.46 ns/element/SM on sm_100a with distinct digits, vs 1.0 for
+// match.any (tools/microbench_rank.cu); counting alone uses shared atomics
+// (0.04 ns/element/SM).
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    if (!valid) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
     }
-    __syncthreads();
-    uint32_t *row = cnt + (size_t)blockIdx.x * ntiles;
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) row[t] = s_h[t];
+    return peers;
 }
 
 // ---------------------------------------------------------------------------
-// 2. per tile: exclusive prefix over the count blocks
+// element counts (device-resident)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_colscan(uint32_t *__restrict__ cnt, int nblocks, int ntiles,
-                                                 uint32_t *__restrict__ total) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles) return;
-    uint32_t run = 0;
-    int b = 0;
-    for (; b + 8 <= nblocks; b += 8) {
-        uint32_t c[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) c[j] = cnt[(size_t)(b + j) * ntiles + t];
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            cnt[(size_t)(b + j) * ntiles + t] = run;
-            run += c[j];
+enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2 };
+__device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint32_t n_points, uint64_t max_keys) {
+    if (which == CNT_POINTS) return n_points;
+    if (which == CNT_VISIBLE) return c->n_visible;
+    const uint64_t k = c->n_keys;
+    return c->err ? 0u : (uint32_t)(k < max_keys ? k : max_keys);
+}
+
+// ---------------------------------------------------------------------------
+// order-preserving scans (reduce -> scan sums -> apply)
+// ---------------------------------------------------------------------------
+struct CompactOp {   // visible flags -> (depth bits, index) of the visible Gaussians, index order
+    const uint32_t *touched, *depth_bits;
+    uint32_t *out_k, *out_v;
+    Counters *cnt;
+    static constexpr int WHICH = CNT_POINTS;
+    struct Aux {
+        uint32_t depth;
+    };
+    __device__ uint32_t load(uint32_t i) const { return touched[i] > 0 ? 1u : 0u; }
+    __device__ uint32_t load(uint32_t i, Aux &a) const {
+        a.depth = depth_bits[i];
+        return touched[i] > 0 ? 1u : 0u;
+    }
+    __device__ void emit(uint32_t i, uint64_t pos, uint32_t v, const Aux &a) const {
+        if (v) {
+            out_k[pos] = a.depth;
+            out_v[pos] = i;
         }
     }
-    for (; b < nblocks; b++) {
-        const uint32_t c = cnt[(size_t)b * ntiles + t];
-        cnt[(size_t)b * ntiles + t] = run;
-        run += c;
+    __device__ void finish(uint64_t total) const { cnt->n_visible = (uint32_t)total; }
+};
+
+struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ gathered rects, chunk heads)
+    const uint32_t *sorted_idx, *touched;
+    const ushort4 *rect;
+    uint32_t *off;
+    ushort4 *rect_r;
+    uint32_t *chunk_first;
+    Counters *cnt;
+    uint64_t max_keys;
+    static constexpr int WHICH = CNT_VISIBLE;
+    struct Aux {
+        ushort4 rc;
+    };
+    __device__ uint32_t load(uint32_t r) const { return touched[sorted_idx[r]]; }
+    __device__ uint32_t load(uint32_t r, Aux &a) const {
+        const uint32_t i = sorted_idx[r];
+        a.rc = rect[i];
+        return touched[i];
     }
-    total[t] = run;
+    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &a) const {
+        off[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
+        rect_r[r] = a.rc;
+        // every 4096-pair chunk boundary inside [o, o+v) belongs to Gaussian r
+        for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
+            if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
+    }
+    __device__ void finish(uint64_t total) const {
+        cnt->n_keys = total;
+        if (total > max_keys) atomicOr(&cnt->err, 1u);
+    }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(SORT_THREADS) k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums) {
+    __shared__ uint32_t s_w[NWARP];
+    const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            const uint32_t e = c * SORT_CHUNK + elem_of(warp, r, lane);
+            if (e < n) acc += op.load(e);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s_w[warp] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < NWARP; w++) t += s_w[w];
+            sums[c] = t;
+        }
+        __syncthreads();
+    }
 }
 
-// ---------------------------------------------------------------------------
-// 3. exclusive scan over tiles (one block) -> ranges, K, capacity flag
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_tilescan(const uint32_t *__restrict__ total, int ntiles,
-                                                   uint2 *__restrict__ ranges, uint32_t *__restrict__ start,
-                                                   Counters *cnt, uint64_t max_keys) {
+// one block: exclusive scan of the chunk sums in place; op.finish(total)
+template <class Op>
+__global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, uint32_t *sums) {
     __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long s_carry;
+    const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
-    for (int base = 0; base < ntiles; base += 1024) {
-        const int t = base + threadIdx.x;
-        const unsigned long long v = t < ntiles ? total[t] : 0;
+    for (uint32_t base = 0; base < nchunks; base += 1024) {
+        const uint32_t c = base + threadIdx.x;
+        const unsigned long long v = c < nchunks ? sums[c] : 0;
         unsigned long long x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -113,359 +176,432 @@ __global__ void __launch_bounds__(1024) k_tilescan(const uint32_t *__restrict__ 
             tot += s_w[w];
         }
         const unsigned long long ex = s_carry + wb + x - v;
-        if (t < ntiles) {
-            const uint32_t s = (uint32_t)(ex < 0xFFFFFFFFull ? ex : 0xFFFFFFFFull);
-            const unsigned long long e2 = ex + v;
-            start[t] = s;
-            ranges[t] = v ? make_uint2(s, (uint32_t)(e2 < 0xFFFFFFFFull ? e2 : 0xFFFFFFFFull)) : make_uint2(0u, 0u);
-        }
+        if (c < nchunks) sums[c] = (uint32_t)(ex < 0xFFFFFFFFull ? ex : 0xFFFFFFFFull);
         __syncthreads();
         if (threadIdx.x == 0) s_carry += tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        cnt->n_keys = s_carry;
-        if (s_carry > max_keys) atomicOr(&cnt->err, 1u);
-    }
+    if (threadIdx.x == 0) op.finish(s_carry);
 }
 
-// ---------------------------------------------------------------------------
-// 4. scatter Gaussian indices into their tiles' segments
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CNT_THREADS) k_scatter(int N, const uint32_t *__restrict__ touched,
-                                                         const ushort4 *__restrict__ rect, int gx, int ntiles,
-                                                         const uint32_t *__restrict__ cnt,
-                                                         const uint32_t *__restrict__ start,
-                                                         uint32_t *__restrict__ vals, const Counters *counters) {
-    extern __shared__ uint32_t s_cur[];
-    if (counters->err) return;
-    const uint32_t *row = cnt + (size_t)blockIdx.x * ntiles;
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cur[t] = start[t] + row[t];
-    __syncthreads();
-    const int per = ceil_div_i(N, gridDim.x);
-    const int i0 = blockIdx.x * per, i1 = min(N, i0 + per);
-    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-        if (touched[i] == 0) continue;
-        const ushort4 r = rect[i];
-        for (int ty = r.y; ty < r.w; ty++)
-            for (int tx = r.x; tx < r.z; tx++) {
-                const uint32_t pos = atomicAdd(&s_cur[ty * gx + tx], 1u);
-                vals[pos] = (uint32_t)i;
-            }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// 5. per-tile sort by (depth bits, Gaussian index)
-// ---------------------------------------------------------------------------
-// One stable LSD pass over an n-element chunk held by the block, 8-bit digit.
-// Element e belongs to warp e / (ITEMS*32), round (e / 32) % ITEMS, lane e % 32,
-// so a warp ranks a contiguous range in order (stability).
-template <int NW, int ITEMS>
-struct BlockRanker {
-    uint16_t whist[NW][256];   // per-warp digit counts, then exclusive prefix over warps
-    uint32_t tot[256];         // chunk digit totals
-    uint32_t dstart[256];      // chunk exclusive digit starts
-    uint32_t wsum[8];
-    int all_same;
-
-    // ranks keys src[e] (e < n); returns the chunk-local destination of each
-    // item in pos[]; must be called by all NW*32 threads
-    __device__ void rank(const uint32_t *src, int n, int shift, uint32_t (&key)[ITEMS], uint32_t (&pos)[ITEMS]) {
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int i = threadIdx.x; i < NW * 256; i += NW * 32) (&whist[0][0])[i] = 0;
-        if (threadIdx.x == 0) all_same = 0;
-        __syncthreads();
-        uint32_t rk[ITEMS];
+template <class Op>
+__global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
+    __shared__ uint32_t s_w[NWARP];
+    const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        uint32_t v[SORT_ITEMS], rex[SORT_ITEMS], wrun = 0;
+        typename Op::Aux aux[SORT_ITEMS];
 #pragma unroll
-        for (int r = 0; r < ITEMS; r++) {
-            const int e = w * (ITEMS * 32) + r * 32 + lane;
-            const bool valid = e < n;
-            key[r] = valid ? src[e] : 0u;
-            const uint32_t d = valid ? ((key[r] >> shift) & 255u) : 0xFFFFFFFFu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            uint32_t before = 0;
-            if (valid) before = whist[w][d];
-            __syncwarp();
-            if (valid && (__ffs(peers) - 1) == lane) whist[w][d] = (uint16_t)(before + __popc(peers));
-            __syncwarp();
-            rk[r] = before + __popc(peers & lanemask_lt());
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            const uint32_t e = c * SORT_CHUNK + elem_of(warp, r, lane);
+            v[r] = e < n ? op.load(e, aux[r]) : 0u;
         }
-        __syncthreads();
-        // per digit: exclusive over warps, totals
-        for (int d = threadIdx.x; d < 256; d += NW * 32) {
-            uint32_t run = 0;
 #pragma unroll
-            for (int ww = 0; ww < NW; ww++) {
-                const uint32_t c = whist[ww][d];
-                whist[ww][d] = (uint16_t)run;
-                run += c;
-            }
-            tot[d] = run;
-            if ((int)run == n) all_same = 1;
-        }
-        __syncthreads();
-        // exclusive scan of the 256 totals (first 8 warps)
-        if (threadIdx.x < 256) {
-            const uint32_t v = tot[threadIdx.x];
-            uint32_t x = v;
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            uint32_t x = v[r];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            if (lane == 31) wsum[w] = x;
-            dstart[threadIdx.x] = x - v;   // warp-local for now
+            rex[r] = wrun + x - v[r];
+            wrun += __shfl_sync(0xffffffffu, x, 31);
         }
+        if (lane == 0) s_w[warp] = wrun;
         __syncthreads();
-        if (threadIdx.x < 256) {
-            uint32_t add = 0;
-            for (int ww = 0; ww < (int)(threadIdx.x >> 5); ww++) add += wsum[ww];
-            dstart[threadIdx.x] += add;
-        }
-        __syncthreads();
+        uint64_t base = sums[c];
+        for (int w = 0; w < warp; w++) base += s_w[w];
 #pragma unroll
-        for (int r = 0; r < ITEMS; r++) {
-            const int e = w * (ITEMS * 32) + r * 32 + lane;
-            if (e < n) {
-                const uint32_t d = (key[r] >> shift) & 255u;
-                pos[r] = dstart[d] + whist[w][d] + rk[r];
-            }
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            const uint32_t e = c * SORT_CHUNK + elem_of(warp, r, lane);
+            if (e < n) op.emit(e, base + rex[r], v[r], aux[r]);
         }
-    }
-};
-
-// order runs of equal keys by Gaussian index (insertion sort; runs are rare and short)
-__device__ __forceinline__ void fix_ties(const uint32_t *keys, uint32_t *g, int n) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const bool head = (j == 0 || keys[j - 1] != keys[j]);
-        if (!head || j + 1 >= n || keys[j + 1] != keys[j]) continue;
-        int e = j + 1;
-        while (e < n && keys[e] == keys[j]) e++;
-        for (int a = j + 1; a < e; a++) {
-            const uint32_t v = g[a];
-            int b = a - 1;
-            while (b >= j && g[b] > v) {
-                g[b + 1] = g[b];
-                b--;
-            }
-            g[b + 1] = v;
-        }
-    }
-}
-
-template <int NW, int ITEMS>
-struct SortSmem {
-    static constexpr int CAP = NW * 32 * ITEMS;
-    uint32_t k[2][CAP];
-    uint16_t p[2][CAP];
-    BlockRanker<NW, ITEMS> rk;
-};
-
-// Sorts one tile list of n <= CAP entries: keys = depth bits of vals_in[start + j].
-template <int NW, int ITEMS>
-__device__ void sort_tile_smem(SortSmem<NW, ITEMS> &sm, const uint32_t *__restrict__ vals_in,
-                               uint32_t *__restrict__ vals_out, const uint32_t *__restrict__ depth_bits,
-                               uint32_t start, int n) {
-    for (int j = threadIdx.x; j < n; j += NW * 32) {
-        sm.k[0][j] = __ldg(&depth_bits[vals_in[start + j]]);
-        sm.p[0][j] = (uint16_t)j;
-    }
-    __syncthreads();
-    int cur = 0;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int pass = 0; pass < 4; pass++) {
-        uint32_t key[ITEMS], pos[ITEMS];
-        sm.rk.rank(sm.k[cur], n, 8 * pass, key, pos);
-        if (sm.rk.all_same) {   // every key has the same digit: the pass is the identity
-            __syncthreads();
-            continue;
-        }
-        uint16_t pv[ITEMS];
-#pragma unroll
-        for (int r = 0; r < ITEMS; r++) {
-            const int e = w * (ITEMS * 32) + r * 32 + lane;
-            if (e < n) pv[r] = sm.p[cur][e];
-        }
-#pragma unroll
-        for (int r = 0; r < ITEMS; r++) {
-            const int e = w * (ITEMS * 32) + r * 32 + lane;
-            if (e < n) {
-                sm.k[cur ^ 1][pos[r]] = key[r];
-                sm.p[cur ^ 1][pos[r]] = pv[r];
-            }
-        }
-        cur ^= 1;
-        __syncthreads();
-    }
-    // gather the Gaussian indices in sorted order into k[cur^1] (reused), fix ties, write out
-    uint32_t *g = sm.k[cur ^ 1];
-    for (int j = threadIdx.x; j < n; j += NW * 32) g[j] = vals_in[start + sm.p[cur][j]];
-    __syncthreads();
-    fix_ties(sm.k[cur], g, n);
-    __syncthreads();
-    for (int j = threadIdx.x; j < n; j += NW * 32) vals_out[start + j] = g[j];
-}
-
-__global__ void __launch_bounds__(SMALL_THREADS) k_sort_small(const uint2 *__restrict__ ranges,
-                                                              const uint32_t *__restrict__ vals_in,
-                                                              uint32_t *__restrict__ vals_out,
-                                                              const uint32_t *__restrict__ depth_bits,
-                                                              uint32_t *__restrict__ big_list, Counters *counters) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    auto &sm = *reinterpret_cast<SortSmem<SMALL_THREADS / 32, SMALL_CAP / SMALL_THREADS> *>(smem_raw);
-    if (counters->err) return;
-    const int tile = blockIdx.x;
-    const uint2 rg = ranges[tile];
-    const int n = (int)(rg.y - rg.x);
-    if (n <= 0) return;
-    if (n > SMALL_CAP) {
-        if (threadIdx.x == 0) big_list[atomicAdd(&counters->n_big, 1u)] = (uint32_t)tile;
-        return;
-    }
-    if (n == 1) {
-        if (threadIdx.x == 0) vals_out[rg.x] = vals_in[rg.x];
-        return;
-    }
-    sort_tile_smem(sm, vals_in, vals_out, depth_bits, rg.x, n);
-}
-
-__global__ void __launch_bounds__(BIG_THREADS, 1) k_sort_big(const uint2 *__restrict__ ranges,
-                                                             const uint32_t *__restrict__ vals_in,
-                                                             uint32_t *__restrict__ vals_out,
-                                                             const uint32_t *__restrict__ depth_bits,
-                                                             const uint32_t *__restrict__ big_list,
-                                                             uint32_t *__restrict__ huge_list, Counters *counters) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    auto &sm = *reinterpret_cast<SortSmem<BIG_THREADS / 32, BIG_CAP / BIG_THREADS> *>(smem_raw);
-    if (counters->err) return;
-    const uint32_t nbig = counters->n_big;
-    for (uint32_t b = blockIdx.x; b < nbig; b += gridDim.x) {
-        const int tile = (int)big_list[b];
-        const uint2 rg = ranges[tile];
-        const int n = (int)(rg.y - rg.x);
-        if (n > BIG_CAP) {
-            if (threadIdx.x == 0) huge_list[atomicAdd(&counters->n_huge, 1u)] = (uint32_t)tile;
-            continue;
-        }
-        sort_tile_smem(sm, vals_in, vals_out, depth_bits, rg.x, n);
-        __syncthreads();
-    }
-}
-
-// Lists longer than BIG_CAP: chunked LSD sort in global memory by one block.
-// Keys ping-pong between kbuf[0]/kbuf[1]; values between vals_in (used as
-// scratch for its own segment) and vals_out (same segment offsets).
-__global__ void __launch_bounds__(BIG_THREADS, 1) k_sort_huge(const uint2 *__restrict__ ranges,
-                                                              uint32_t *vals_in, uint32_t *vals_out,
-                                                              const uint32_t *__restrict__ depth_bits,
-                                                              const uint32_t *__restrict__ huge_list, uint32_t *ka,
-                                                              uint32_t *kb, Counters *counters) {
-    constexpr int NW = BIG_THREADS / 32, ITEMS = BIG_CAP / BIG_THREADS;
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    auto &sm = *reinterpret_cast<SortSmem<NW, ITEMS> *>(smem_raw);
-    __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_hist[256];
-    __shared__ int s_same;
-    if (counters->err) return;
-    const uint32_t nh = counters->n_huge;
-    for (uint32_t hI = blockIdx.x; hI < nh; hI += gridDim.x) {
-        const uint2 rg = ranges[huge_list[hI]];
-        const uint32_t s0 = rg.x;
-        const int n = (int)(rg.y - rg.x);
-        uint32_t *K[2] = {ka + s0, kb + s0};
-        uint32_t *V[2] = {vals_in + s0, vals_out + s0};
-        for (int j = threadIdx.x; j < n; j += BIG_THREADS) K[0][j] = depth_bits[V[0][j]];
-        __syncthreads();
-        int cur = 0;
-        for (int pass = 0; pass < 4; pass++) {
-            const int shift = 8 * pass;
-            for (int d = threadIdx.x; d < 256; d += BIG_THREADS) s_hist[d] = 0;
-            if (threadIdx.x == 0) s_same = 0;
-            __syncthreads();
-            for (int j = threadIdx.x; j < n; j += BIG_THREADS) atomicAdd(&s_hist[(K[cur][j] >> shift) & 255u], 1u);
-            __syncthreads();
-            if (threadIdx.x < 256) {
-                uint32_t ex = 0;
-                for (int d = 0; d < (int)threadIdx.x; d++) ex += s_hist[d];
-                s_base[threadIdx.x] = ex;
-                if ((int)s_hist[threadIdx.x] == n) s_same = 1;
-            }
-            __syncthreads();
-            if (s_same) continue;
-            for (int c0 = 0; c0 < n; c0 += BIG_CAP) {
-                const int cn = min(BIG_CAP, n - c0);
-                for (int j = threadIdx.x; j < cn; j += BIG_THREADS) sm.k[0][j] = K[cur][c0 + j];
-                __syncthreads();
-                uint32_t key[ITEMS], pos[ITEMS];
-                sm.rk.rank(sm.k[0], cn, shift, key, pos);
-                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-                for (int r = 0; r < ITEMS; r++) {
-                    const int e = w * (ITEMS * 32) + r * 32 + lane;
-                    if (e < cn) {
-                        const uint32_t d = (key[r] >> shift) & 255u;
-                        const uint32_t g = s_base[d] + (pos[r] - sm.rk.dstart[d]);
-                        K[cur ^ 1][g] = key[r];
-                        V[cur ^ 1][g] = V[cur][c0 + e];
-                    }
-                }
-                __syncthreads();
-                if (threadIdx.x < 256) s_base[threadIdx.x] += sm.rk.tot[threadIdx.x];
-                __syncthreads();
-            }
-            cur ^= 1;
-            __syncthreads();
-        }
-        if (cur == 0)
-            for (int j = threadIdx.x; j < n; j += BIG_THREADS) V[1][j] = V[0][j];
-        __syncthreads();
-        fix_ties(K[cur], V[1], n);
         __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
+// loaders: a chunk's keys (and values) into shared memory
+// ---------------------------------------------------------------------------
+struct PlainLoader {
+    const uint32_t *keys, *vals;
+    static constexpr int SCRATCH_WORDS = 0;
+    __device__ uint32_t key(uint32_t i) const { return __ldcs(keys + i); }
+    __device__ void load(uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
+        uint32_t k[SORT_ITEMS], v[SORT_ITEMS];   // all loads in flight before the first use
+#pragma unroll
+        for (int q = 0; q < SORT_ITEMS; q++) {
+            const uint32_t e = threadIdx.x + q * SORT_THREADS;
+            if (e < cvalid) {
+                k[q] = __ldcs(keys + cbase + e);
+                if (sv) v[q] = __ldcs(vals + cbase + e);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < SORT_ITEMS; q++) {
+            const uint32_t e = threadIdx.x + q * SORT_THREADS;
+            if (e < cvalid) {
+                sk[e] = k[q];
+                if (sv) sv[e] = v[q];
+            }
+        }
+    }
+};
+
+// Pairs cbase .. cbase+cvalid-1 of the depth-ordered duplication: pair p belongs
+// to the Gaussian r with off[r] <= p < off[r+1]; it is the (p - off[r])-th tile
+// of rect_r[r] in row-major order; value = sorted_idx[r].
+struct Expander {
+    const uint32_t *off, *sorted_idx, *chunk_first;
+    const ushort4 *rect_r;
+    const Counters *cnt;
+    int gx;
+    static constexpr int STAGE = 1024;                            // Gaussians staged in shared memory
+    static constexpr int SCRATCH_WORDS = SORT_CHUNK + 4 * STAGE;  // owner map + (off, rect, idx)
+    __device__ void load(uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *scratch) const {
+        uint32_t *s_owner = scratch;
+        uint32_t *s_off = scratch + SORT_CHUNK;
+        ushort4 *s_rect = reinterpret_cast<ushort4 *>(scratch + SORT_CHUNK + STAGE);
+        uint32_t *s_idx = scratch + SORT_CHUNK + 3 * STAGE;
+        const uint32_t nv = cnt->n_visible;
+        const uint32_t chunk = cbase / SORT_CHUNK;
+        const uint32_t nchunks = (uint32_t)((cnt->n_keys + SORT_CHUNK - 1) / SORT_CHUNK);
+        const uint32_t r_lo = chunk_first[chunk];
+        const uint32_t r_hi = chunk + 1 < nchunks ? min(nv - 1, chunk_first[chunk + 1]) : nv - 1;
+        const uint32_t n_g = r_hi - r_lo + 1;
+        const bool staged = n_g <= (uint32_t)STAGE;
+        for (uint32_t e = threadIdx.x; e < SORT_CHUNK; e += SORT_THREADS) s_owner[e] = 0u;
+        if (staged) {
+            for (uint32_t j = threadIdx.x; j < n_g; j += SORT_THREADS) {
+                s_off[j] = off[r_lo + j];
+                s_rect[j] = rect_r[r_lo + j];
+                s_idx[j] = sorted_idx[r_lo + j];
+            }
+        }
+        __syncthreads();
+        // segment heads: the Gaussian starting at pair cbase+e owns e, e+1, ...
+        for (uint32_t j = 1 + threadIdx.x; j < n_g; j += SORT_THREADS) {
+            const uint32_t o = staged ? s_off[j] : off[r_lo + j];
+            if (o < cbase + cvalid) s_owner[o - cbase] = j;   // >= 1 pair each: heads are distinct
+        }
+        __syncthreads();
+        {   // inclusive max-scan over the chunk (thread-blocked, 16 consecutive each)
+            __shared__ uint32_t s_w[NWARP];
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            const int e0 = threadIdx.x * SORT_ITEMS;
+            uint32_t m = 0, loc[SORT_ITEMS];
+#pragma unroll
+            for (int q = 0; q < SORT_ITEMS; q++) {
+                m = max(m, s_owner[e0 + q]);
+                loc[q] = m;
+            }
+            uint32_t x = m;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x = max(x, y);
+            }
+            if (lane == 31) s_w[w] = x;
+            __syncthreads();
+            uint32_t pre = __shfl_up_sync(0xffffffffu, x, 1);
+            if (lane == 0) pre = 0;
+            for (int ww = 0; ww < w; ww++) pre = max(pre, s_w[ww]);
+#pragma unroll
+            for (int q = 0; q < SORT_ITEMS; q++) s_owner[e0 + q] = max(pre, loc[q]);
+            __syncthreads();
+        }
+        for (uint32_t e = threadIdx.x; e < cvalid; e += SORT_THREADS) {
+            const uint32_t j = s_owner[e];
+            const uint32_t o = staged ? s_off[j] : off[r_lo + j];
+            const ushort4 rc = staged ? s_rect[j] : rect_r[r_lo + j];
+            const uint32_t q = cbase + e - o;
+            const uint32_t w = (uint32_t)(rc.z - rc.x);
+            // q / w through a float reciprocal (q < 2^24), corrected to the exact quotient
+            uint32_t qy = (uint32_t)((float)q * __frcp_rn((float)w));
+            if (qy * w > q) qy--;
+            else if ((qy + 1) * w <= q) qy++;
+            const uint32_t ty = rc.y + qy, tx = rc.x + (q - qy * w);
+            sk[cbase + e] = ty * (uint32_t)gx + tx;
+            sv[cbase + e] = staged ? s_idx[j] : sorted_idx[r_lo + j];
+        }
+    }
+};
+
+// writes the K (tile, index) pairs in depth order: one 4096-pair chunk per iteration
+__global__ void __launch_bounds__(SORT_THREADS) k_expand(Expander ex, uint64_t max_keys, uint32_t *kout,
+                                                         uint32_t *vout) {
+    extern __shared__ uint32_t dyn[];
+    const uint32_t n = count_of(ex.cnt, CNT_KEYS, 0, max_keys);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t cbase = c * SORT_CHUNK, cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+        ex.load(cbase, cvalid, kout, vout, dyn);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// radix pass, step 1: per-chunk digit counts -> cmat[digit][chunk]
+// ---------------------------------------------------------------------------
+template <class Loader>
+__global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Counters *cnt, int which,
+                                                           uint64_t max_keys, int shift, uint32_t *cmat,
+                                                           uint32_t ldm) {
+    constexpr int NH = 4;   // privatised histograms (warp % NH)
+    __shared__ uint32_t s_h[NH][256];
+    const uint32_t n = count_of(cnt, which, 0, max_keys);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const int warp = threadIdx.x >> 5;
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t cbase = c * SORT_CHUNK, cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+#pragma unroll
+        for (int h = 0; h < NH; h++) s_h[h][threadIdx.x] = 0;
+        uint32_t k[SORT_ITEMS];
+#pragma unroll
+        for (int q = 0; q < SORT_ITEMS; q++) {
+            const uint32_t e = threadIdx.x + q * SORT_THREADS;
+            k[q] = e < cvalid ? ld.key(cbase + e) : 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < SORT_ITEMS; q++) {
+            const uint32_t e = threadIdx.x + q * SORT_THREADS;
+            if (e < cvalid) atomicAdd(&s_h[warp % NH][(k[q] >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        uint32_t t = 0;
+#pragma unroll
+        for (int h = 0; h < NH; h++) t += s_h[h][threadIdx.x];
+        cmat[(size_t)threadIdx.x * ldm + c] = t;
+        __syncthreads();
+    }
+}
+
+// step 2: one block per digit: exclusive scan of its row over the chunks; row totals
+__global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int which, uint64_t max_keys,
+                                                      uint32_t *cmat, uint32_t ldm, uint32_t *row_total) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_carry;
+    const uint32_t n = count_of(cnt, which, 0, max_keys);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *row = cmat + (size_t)blockIdx.x * ldm;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nchunks; base += 1024) {
+        const uint32_t c = base + threadIdx.x;
+        const uint32_t v = c < nchunks ? row[c] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        uint32_t wb = 0, tot = 0;
+        for (int w = 0; w < 32; w++) {
+            if (w < warp) wb += s_w[w];
+            tot += s_w[w];
+        }
+        if (c < nchunks) row[c] = s_carry + wb + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) row_total[blockIdx.x] = s_carry;
+}
+
+// step 3: stable scatter. position = (all smaller digits) + (this digit in
+// earlier chunks) + (rank among this chunk's elements of the digit)
+template <class Loader>
+__global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint32_t *__restrict__ kout,
+                                                             uint32_t *__restrict__ vout, const Counters *cnt,
+                                                             int which, uint64_t max_keys, int shift,
+                                                             const uint32_t *__restrict__ cmat, uint32_t ldm,
+                                                             const uint32_t *__restrict__ row_total) {
+    extern __shared__ uint32_t dyn[];
+    uint32_t *s_k = dyn, *s_v = dyn + SORT_CHUNK;                                   // loaded chunk
+    uint32_t *s_ok = dyn + 2 * SORT_CHUNK, *s_ov = dyn + 3 * SORT_CHUNK;            // digit-ordered chunk
+    uint32_t *s_scr = dyn + 4 * SORT_CHUNK;                                         // loader scratch
+    __shared__ uint16_t s_whist[NWARP][256];
+    __shared__ uint32_t s_dbase[256], s_blk[256], s_base[256], s_tot[NWARP];
+    const uint32_t n = count_of(cnt, which, 0, max_keys);
+    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int d_own = threadIdx.x;
+    auto block_excl_scan = [&](uint32_t v) -> uint32_t {   // over the 256 threads (one value each)
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_tot[warp] = x;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (int w = 0; w < warp; w++) wb += s_tot[w];
+        __syncthreads();
+        return wb + x - v;
+    };
+    s_dbase[d_own] = block_excl_scan(row_total[d_own]);
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t cbase = c * SORT_CHUNK, cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+#pragma unroll
+        for (int w = 0; w < NWARP; w++) s_whist[w][d_own] = 0;
+        s_base[d_own] = s_dbase[d_own] + cmat[(size_t)d_own * ldm + c];
+        ld.load(cbase, cvalid, s_k, s_v, s_scr);
+        __syncthreads();
+        // warp-local stable ranks
+        uint32_t rank[SORT_ITEMS];
+#pragma unroll
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            const int e = elem_of(warp, r, lane);
+            const bool valid = (uint32_t)e < cvalid;
+            const uint32_t d = valid ? ((s_k[e] >> shift) & 255u) : 0u;
+            const uint32_t peers = peers_of(d, valid);
+            uint32_t before = 0;
+            if (valid) before = s_whist[warp][d];
+            __syncwarp();
+            if (valid && (__ffs(peers) - 1) == lane) s_whist[warp][d] = (uint16_t)(before + __popc(peers));
+            __syncwarp();
+            rank[r] = before + __popc(peers & lanemask_lt());
+        }
+        __syncthreads();
+        uint32_t total = 0;
+#pragma unroll
+        for (int w = 0; w < NWARP; w++) {
+            const uint32_t t = s_whist[w][d_own];
+            s_whist[w][d_own] = (uint16_t)total;
+            total += t;
+        }
+        s_blk[d_own] = block_excl_scan(total);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < SORT_ITEMS; r++) {
+            const int e = elem_of(warp, r, lane);
+            if ((uint32_t)e < cvalid) {
+                const uint32_t k = s_k[e];
+                const uint32_t d = (k >> shift) & 255u;
+                const uint32_t pos = s_blk[d] + s_whist[warp][d] + rank[r];
+                s_ok[pos] = k;
+                s_ov[pos] = s_v[e];
+            }
+        }
+        __syncthreads();
+        // runs of one digit are consecutive in shared and in global memory
+#pragma unroll 4
+        for (uint32_t p = threadIdx.x; p < cvalid; p += SORT_THREADS) {
+            const uint32_t k = s_ok[p];
+            const uint32_t d = (k >> shift) & 255u;
+            const uint32_t g = s_base[d] + (p - s_blk[d]);
+            kout[g] = k;
+            vout[g] = s_ov[p];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tile ranges: boundary detection over the sorted tile ids
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tiles, const Counters *cnt,
+                                                uint64_t max_keys, uint2 *ranges) {
+    const uint32_t n = count_of(cnt, CNT_KEYS, 0, max_keys);
+    const uint32_t stride = gridDim.x * blockDim.x * 4;
+    for (uint32_t k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; k0 < n; k0 += stride) {
+        uint32_t t[6];
+        t[0] = k0 > 0 ? tiles[k0 - 1] : 0xFFFFFFFFu;
+        if (k0 + 4 <= n) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(tiles + k0);
+            t[1] = v.x; t[2] = v.y; t[3] = v.z; t[4] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) t[1 + j] = k0 + j < n ? tiles[k0 + j] : 0xFFFFFFFFu;
+        }
+        t[5] = k0 + 4 < n ? tiles[k0 + 4] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t k = k0 + j;
+            if (k >= n) break;
+            if (t[j + 1] != t[j]) ranges[t[j + 1]].x = k;
+            if (t[j + 1] != t[j + 2]) ranges[t[j + 1]].y = k + 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <class Loader>
+static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout, uint32_t *vout,
+                      int which, uint64_t mk, int shift) {
+    const size_t ldm = ws.max_chunks;
+    const size_t sc_smem = (4 * SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t);
+    static bool attrs = false;
+    if (!attrs) {
+        cudaFuncSetAttribute(k_rs_scatter<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
+        attrs = true;
+    }
+    k_rs_count<Loader><<<grid, SORT_THREADS, 0, st>>>(ld, ws.counters, which, mk, shift, ws.cmat, (uint32_t)ldm);
+    k_rs_scanrows<<<256, 1024, 0, st>>>(ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
+    k_rs_scatter<Loader><<<grid, SORT_THREADS, sc_smem, st>>>(ld, kout, vout, ws.counters, which, mk, shift,
+                                                              ws.cmat, (uint32_t)ldm, ws.row_total);
+    return 3;
+}
+
+template <class Op>
+static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint32_t n_points) {
+    k_scan_reduce<Op><<<grid, SORT_THREADS, 0, st>>>(op, n_points, ws.sums);
+    k_scan_sums<Op><<<1, 1024, 0, st>>>(op, n_points, ws.sums);
+    k_scan_apply<Op><<<grid, SORT_THREADS, 0, st>>>(op, n_points, ws.sums);
+    return 3;
+}
+
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &) {
     Counters *cnt = ws.counters;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    static bool attrs = false;
-    const size_t small_smem = sizeof(SortSmem<SMALL_THREADS / 32, SMALL_CAP / SMALL_THREADS>);
-    const size_t big_smem = sizeof(SortSmem<BIG_THREADS / 32, BIG_CAP / BIG_THREADS>);
-    if (!attrs) {
-        cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * MAX_TILES);
-        cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * MAX_TILES);
-        cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem);
-        cudaFuncSetAttribute(k_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem);
-        cudaFuncSetAttribute(k_sort_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem);
-        attrs = true;
-    }
-    const int G = ws.count_blocks;
-    const size_t hsmem = sizeof(uint32_t) * (size_t)ntiles;
+    const int grid_n = std::max(1, std::min(nsm * 8, ceil_div_i(N, SORT_CHUNK)));
+    const int grid_k = std::max(1, std::min(nsm * 8, ceil_div_i(max_keys, SORT_CHUNK)));
+    const uint64_t mk = (uint64_t)max_keys;
+    cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
     int launches = 0;
-    if (N > 0) {
-        k_count<<<G, CNT_THREADS, hsmem, st>>>(N, ws.touched, ws.rect, gx, ntiles, ws.cnt);
+    // 1. compaction of the visible Gaussians (index order)
+    launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[0], ws.sv[0], cnt}, (uint32_t)N);
+    // 2. depth sort: 4 stable passes of 8 bits; the result is back in sk[0]/sv[0]
+    for (int p = 0; p < 4; p++)
+        launches += radix_pass(ws, st, grid_n, PlainLoader{ws.sk[p & 1], ws.sv[p & 1]}, ws.sk[(p + 1) & 1],
+                               ws.sv[(p + 1) & 1], CNT_VISIBLE, mk, 8 * p);
+    // 3. pair offsets in depth order
+    launches += scan_pass(ws, st, grid_n,
+                          OffsetsOp{ws.sv[0], ws.touched, ws.rect, ws.off, ws.rect_r, ws.chunk_first, cnt, mk},
+                          (uint32_t)N);
+    // 4. tile sort with the expansion fused into the first pass; final order in kt[0]/kv[0]
+    int tbits = 0;
+    while ((1 << tbits) < ntiles) tbits++;
+    const int tpasses = tbits <= 8 ? 1 : 2;
+    {
+        const size_t xs = Expander::SCRATCH_WORDS * sizeof(uint32_t);
+        static bool xattr = false;
+        if (!xattr) {
+            cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
+            xattr = true;
+        }
+        const int e = tpasses & 1;   // the passes alternate buffers and end in kt[0]/kv[0]
+        k_expand<<<grid_k, SORT_THREADS, xs, st>>>(Expander{ws.off, ws.sv[0], ws.chunk_first, ws.rect_r, cnt, gx}, mk,
+                                                   ws.kt[e], ws.kv[e]);
         launches++;
-    } else {
-        cudaMemsetAsync(ws.cnt, 0, sizeof(uint32_t) * (size_t)G * ntiles, st);
+        for (int p = 0; p < tpasses; p++) {
+            const int src = (e + p) & 1;
+            launches += radix_pass(ws, st, grid_k, PlainLoader{ws.kt[src], ws.kv[src]}, ws.kt[src ^ 1],
+                                   ws.kv[src ^ 1], CNT_KEYS, mk, 8 * p);
+        }
     }
-    k_colscan<<<ceil_div_i(ntiles, 256), 256, 0, st>>>(ws.cnt, G, ntiles, ws.tile_total);
-    k_tilescan<<<1, 1024, 0, st>>>(ws.tile_total, ntiles, ws.ranges, ws.tile_start, cnt, (uint64_t)max_keys);
-    launches += 2;
-    if (N > 0) {
-        k_scatter<<<G, CNT_THREADS, hsmem, st>>>(N, ws.touched, ws.rect, gx, ntiles, ws.cnt, ws.tile_start,
-                                                  ws.kv[0], cnt);
-        k_sort_small<<<ntiles, SMALL_THREADS, small_smem, st>>>(ws.ranges, ws.kv[0], ws.kv[1], ws.depth_bits,
-                                                                 ws.big_list, cnt);
-        k_sort_big<<<nsm, BIG_THREADS, big_smem, st>>>(ws.ranges, ws.kv[0], ws.kv[1], ws.depth_bits, ws.big_list,
-                                                       ws.huge_list, cnt);
-        k_sort_huge<<<nsm, BIG_THREADS, big_smem, st>>>(ws.ranges, ws.kv[0], ws.kv[1], ws.depth_bits,
-                                                        ws.huge_list, ws.kt[0], ws.kt[1], cnt);
-        launches += 4;
-    }
-    return launches;
+    // 5. tile ranges
+    k_ranges<<<nsm * 4, 256, 0, st>>>(ws.kt[0], cnt, mk, ws.ranges);
+    return launches + 1;
 }
 
 }  // namespace gs

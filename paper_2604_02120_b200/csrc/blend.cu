@@ -63,6 +63,25 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                  : "memory");
 }
 
+struct Rec {
+    float2 m;     // projected mean
+    float4 co;    // (A, B, C, opacity)
+    float4 col;   // (r, g, b, 0)
+};
+
+__device__ __forceinline__ void gather(Rec &r, const float2 *__restrict__ xy, const float4 *__restrict__ conic_o,
+                                       const float4 *__restrict__ rgb, uint32_t gi, bool ok) {
+    if (ok) {
+        r.m = __ldg(xy + gi);
+        r.co = __ldg(conic_o + gi);
+        r.col = __ldg(rgb + gi);
+    } else {
+        r.m = make_float2(0.f, 0.f);
+        r.co = make_float4(0.f, 0.f, 0.f, 1.f);
+        r.col = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 template <bool DUMP, bool STATS>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
@@ -110,16 +129,57 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
     if (warp == NCW) {
         // =================== producer + MMA issuer ===================
+        // Software pipeline over the flattened stream of (tile, batch):
+        //   indices of batch k+1 and the records of batch k were requested one
+        //   iteration earlier, and the first batch of the next tile is fetched
+        //   in four steps spread over the current tile's iterations, so the
+        //   compositors never wait for a full gather latency (~1 us).
         constexpr uint32_t IDESC = idesc_tf32(128, NB);
         const uint32_t a_base = smem_u32(&sm.A[0][0]);
         const uint32_t b_base = smem_u32(&sm.B[0][0]);
         uint32_t s = 0, ph = 0;
-        uint32_t seq = 0;
         unsigned long long n_eval = 0;
+        // current tile
+        int tile = 0;
+        if (lane == 0) tile = (int)atomicAdd(tile_queue, 1u);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        uint2 rg = tile < ntiles ? ranges[tile] : make_uint2(0u, 0u);
+        uint32_t seq = 1;
+        uint32_t b = rg.x;
+        Rec cur;
+        uint32_t inext;
+        {
+            const uint32_t i0 = (b + lane < rg.y) ? vals[b + lane] : 0u;
+            inext = (b + NB + lane < rg.y) ? vals[b + NB + lane] : 0u;
+            gather(cur, xy, conic_o, rgb, i0, b + lane < rg.y);
+        }
+        // next-tile head
+        int hstate = 0, ntile = 0, ntile_l0 = 0;
+        uint2 nrg = make_uint2(0u, 0u);
+        uint32_t hidx0 = 0, hidx1 = 0;
+        Rec h0;
+        auto head_step = [&]() {
+            switch (hstate) {
+                case 0:
+                    if (lane == 0) ntile_l0 = (int)atomicAdd(tile_queue, 1u);
+                    break;
+                case 1:
+                    ntile = __shfl_sync(0xffffffffu, ntile_l0, 0);
+                    nrg = ntile < ntiles ? ranges[ntile] : make_uint2(0u, 0u);
+                    break;
+                case 2:
+                    hidx0 = (nrg.x + lane < nrg.y) ? vals[nrg.x + lane] : 0u;
+                    hidx1 = (nrg.x + NB + lane < nrg.y) ? vals[nrg.x + NB + lane] : 0u;
+                    break;
+                case 3:
+                    gather(h0, xy, conic_o, rgb, hidx0, nrg.x + lane < nrg.y);
+                    break;
+                default:
+                    return;
+            }
+            hstate++;
+        };
         for (;;) {
-            int tile = 0;
-            if (lane == 0) tile = (int)atomicAdd(tile_queue, 1u);
-            tile = __shfl_sync(0xffffffffu, tile, 0);
             if (tile >= ntiles) {
                 mbar_wait(&sm.empty[s], ph ^ 1);
                 if (lane == 0) sm.hdr[s] = make_int4(-1, 0, 0, 0);
@@ -128,73 +188,89 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
                 break;
             }
-            seq++;
-            const uint2 rg = ranges[tile];
+            head_step();
+            bool end = b >= rg.y;
+            if (!DUMP && !end) {
+                const uint32_t dseq = lane < NCW ? *((volatile uint32_t *)&sm.warp_done_seq[lane]) : seq;
+                end = __all_sync(0xffffffffu, dseq >= seq);   // every pixel of the tile terminated
+            }
+            if (end) {
+                mbar_wait(&sm.empty[s], ph ^ 1);
+                if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, 0, 0);
+                mbar_arrive(&sm.full[s]);
+                if (lane == 0) mbar_arrive(&sm.full[s]);
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+                while (hstate < 4) head_step();
+                tile = ntile;
+                rg = nrg;
+                b = rg.x;
+                seq++;
+                cur = h0;
+                inext = hidx1;
+                hstate = 0;
+                continue;
+            }
+            // prefetch: records of batch b+NB, indices of batch b+2NB
+            Rec nx;
+            gather(nx, xy, conic_o, rgb, inext, b + NB + lane < rg.y);
+            const uint32_t inext2 = (b + 2 * NB + lane < rg.y) ? vals[b + 2 * NB + lane] : 0u;
+            const uint32_t cnt = min((uint32_t)NB, rg.y - b);
             const float xc = (float)(GS_TILE * (tile % gx)) + 7.5f;
             const float yc = (float)(GS_TILE * (tile / gx)) + 7.5f;
-            for (uint32_t b0 = rg.x; b0 < rg.y; b0 += NB) {
-                if (!DUMP) {
-                    const uint32_t dseq = lane < NCW ? *((volatile uint32_t *)&sm.warp_done_seq[lane]) : seq;
-                    if (__all_sync(0xffffffffu, dseq >= seq)) break;   // every pixel of the tile terminated
+            uint32_t u[16];
+            if ((uint32_t)lane < cnt) {
+                // Eq. (6): v_g with xh = x_g - x_c, yh = y_g - y_c, times log2(e); + log2(o)
+                const float xh = cur.m.x - xc, yh = cur.m.y - yc;
+                const float A = cur.co.x, B = cur.co.y, C = cur.co.z;
+                float v[6];
+                v[0] = -0.5f * A * LOG2E;
+                v[1] = -0.5f * C * LOG2E;
+                v[2] = -B * LOG2E;
+                v[3] = -(A * xh + B * yh) * LOG2E;
+                v[4] = -(C * yh + B * xh) * LOG2E;
+                v[5] = -(0.5f * A * xh * xh + 0.5f * C * yh * yh + B * xh * yh) * LOG2E + lg2_approx(cur.co.w);
+#pragma unroll
+                for (int k = 0; k < 6; k++) {
+                    const uint32_t hi = f32_to_tf32_rna(v[k]);
+                    const uint32_t lo = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
+                    u[k] = hi;
+                    u[6 + k] = lo;
                 }
-                mbar_wait(&sm.empty[s], ph ^ 1);
-                const uint32_t cnt = min((uint32_t)NB, rg.y - b0);
-                if ((uint32_t)lane < cnt) {
-                    const uint32_t gi = vals[b0 + lane];
-                    const float2 m = xy[gi];
-                    const float4 co = conic_o[gi];
-                    const float4 col = rgb[gi];
-                    // Eq. (6): v_g with xh = x_g - x_c, yh = y_g - y_c, times log2(e); + log2(o)
-                    const float xh = m.x - xc, yh = m.y - yc;
-                    const float A = co.x, B = co.y, C = co.z;
-                    float v[6];
-                    v[0] = -0.5f * A * LOG2E;
-                    v[1] = -0.5f * C * LOG2E;
-                    v[2] = -B * LOG2E;
-                    v[3] = -(A * xh + B * yh) * LOG2E;
-                    v[4] = -(C * yh + B * xh) * LOG2E;
-                    v[5] = -(0.5f * A * xh * xh + 0.5f * C * yh * yh + B * xh * yh) * LOG2E + lg2_approx(co.w);
-                    uint32_t u[16];
+            } else {
+                // padding column: exponent -1e30, never kept by any pixel
 #pragma unroll
-                    for (int k = 0; k < 6; k++) {
-                        const uint32_t hi = f32_to_tf32_rna(v[k]);
-                        const uint32_t lo = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
-                        u[k] = hi;
-                        u[6 + k] = lo;
-                    }
-                    u[12] = u[13] = u[14] = u[15] = 0u;
-                    const uint32_t rb = b_base + s * (NB * 64);
-#pragma unroll
-                    for (int c = 0; c < 4; c++)
-                        st_shared_v4(rb + op_off(lane, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
-                    sm.rgb[s][lane] = col;
-                }
-                if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, (int)cnt, (int)b0);
-                if (STATS && lane == 0) n_eval += (unsigned long long)cnt * GS_TILE_PIX;
-                fence_proxy_async_smem();
-                mbar_arrive(&sm.full[s]);
-                __syncwarp();
-                if (lane == 0) {
-                    tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < 2; kk++)
-#pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            const uint64_t ad = umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512);
-                            const uint64_t bd = umma_desc(b_base + s * (NB * 64) + kk * 256, 128, 512);
-                            mma_tf32(tmem + s * (2 * NB) + h * NB, ad, bd, IDESC, kk);
-                        }
-                    mma_commit(&sm.full[s]);
-                }
-                __syncwarp();
-                if (++s == STAGES) { s = 0; ph ^= 1; }
+                for (int k = 0; k < 12; k++) u[k] = 0u;
+                u[5] = __float_as_uint(-1e30f);
             }
-            // end-of-tile marker
+            u[12] = u[13] = u[14] = u[15] = 0u;
             mbar_wait(&sm.empty[s], ph ^ 1);
-            if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, 0, 0);
+            const uint32_t rb = b_base + s * (NB * 64);
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                st_shared_v4(rb + op_off(lane, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+            sm.rgb[s][lane] = cur.col;
+            if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, (int)cnt, (int)b);
+            if (STATS && lane == 0) n_eval += (unsigned long long)cnt * GS_TILE_PIX;
+            fence_proxy_async_smem();
             mbar_arrive(&sm.full[s]);
-            if (lane == 0) mbar_arrive(&sm.full[s]);
+            __syncwarp();
+            if (lane == 0) {
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint64_t ad = umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512);
+                        const uint64_t bd = umma_desc(b_base + s * (NB * 64) + kk * 256, 128, 512);
+                        mma_tf32(tmem + s * (2 * NB) + h * NB, ad, bd, IDESC, kk);
+                    }
+                mma_commit(&sm.full[s]);
+            }
+            __syncwarp();
             if (++s == STAGES) { s = 0; ph ^= 1; }
+            cur = nx;
+            inext = inext2;
+            b += NB;
         }
     } else {
         // =================== compositors ===================
@@ -240,26 +316,25 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 if (DUMP) {
                     for (int j = 0; j < cnt; j++) dump_m[((size_t)hd.w + j) * GS_TILE_PIX + p] = m[j];
                 } else {
+                    // columns j >= cnt hold the padding exponent -1e30: no count checks needed
 #pragma unroll
                     for (int j = 0; j < NB; j++) {
-                        if (j < cnt) {
-                            const float mj = m[j];
-                            const bool live = (mj >= LOG2_ALPHA_MIN) && !done;
-                            if (__any_sync(0xffffffffu, live)) {
-                                const float4 c = sm.rgb[s][j];
-                                const float a = fminf(ALPHA_MAX, ex2_approx(mj));
-                                const float tT = T * (1.0f - a);
-                                if (live) {
-                                    if (STATS) n_kept++;
-                                    if (tT < T_MIN) {
-                                        done = true;
-                                    } else {
-                                        const float wgt = a * T;
-                                        C0 += wgt * c.x;
-                                        C1 += wgt * c.y;
-                                        C2 += wgt * c.z;
-                                        T = tT;
-                                    }
+                        const float mj = m[j];
+                        const bool live = (mj >= LOG2_ALPHA_MIN) && !done;
+                        if (__any_sync(0xffffffffu, live)) {
+                            const float4 c = sm.rgb[s][j];
+                            const float a = fminf(ALPHA_MAX, ex2_approx(mj));
+                            const float tT = T * (1.0f - a);
+                            if (live) {
+                                if (STATS) n_kept++;
+                                if (tT < T_MIN) {
+                                    done = true;
+                                } else {
+                                    const float wgt = a * T;
+                                    C0 += wgt * c.x;
+                                    C1 += wgt * c.y;
+                                    C2 += wgt * c.z;
+                                    T = tT;
                                 }
                             }
                         }

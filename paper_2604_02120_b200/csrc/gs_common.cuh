@@ -17,15 +17,13 @@ struct Counters {
     uint32_t n_visible;        // compaction output
     uint32_t err;              // device-side error bits (1 = key capacity)
     uint64_t n_keys;           // K (64-bit: the capacity check is exact)
-    uint32_t n_big;            // tiles whose list exceeds the small-sort capacity
-    uint32_t n_huge;           // tiles whose list exceeds the big-sort capacity
     uint32_t tile_queue;       // blend persistent work queue
-    uint32_t pad[5];
+    uint32_t pad[3];
     unsigned long long pairs_eval;   // GS_FLAG_STATS: exponents computed by the blend
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
 
-constexpr int MAX_TILES = 32768;   // shared-memory tile histograms (128 KB)
+constexpr int MAX_TILES = 65536;   // tile ids sorted in two 8-bit passes
 
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
@@ -37,17 +35,21 @@ struct Workspace {
     ushort4 *rect;             // [N] (xmin, ymin, xmax, ymax) tiles, half-open
     uint32_t *touched;         // [N] tiles touched (0 = culled)
     int32_t *radius;           // [N] pixel radius (debug output)
+    uint32_t *sk[2];           // [N] depth keys of the visible Gaussians, ping-pong
+    uint32_t *sv[2];           // [N] their indices; sv[0] = depth order after the sort
+    uint32_t *off;             // [N] first pair of each depth-ordered Gaussian
+    ushort4 *rect_r;           // [N] rect of each depth-ordered Gaussian
     // per key (max_keys)
-    uint32_t *kv[2];           // [K] Gaussian indices: kv[0] scattered per tile, kv[1] sorted
-    uint32_t *kt[2];           // [K] key scratch for the rare over-long tile lists
+    uint32_t *kt[2];           // [K] tile ids, ping-pong; kt[0] final
+    uint32_t *kv[2];           // [K] Gaussian indices, ping-pong; kv[0] final
+    uint32_t *chunk_first;     // [K/4096+1] Gaussian holding the first pair of each chunk
     // per tile
-    uint32_t *cnt;             // [count_blocks][tiles] block-private counts -> prefixes
-    uint32_t *tile_total;      // [tiles]
-    uint32_t *tile_start;      // [tiles]
-    uint2 *ranges;             // [tiles] [start, end) into kv[1]
-    uint32_t *big_list;        // [tiles]
-    uint32_t *huge_list;       // [tiles]
-    int count_blocks;          // fixed partition of the Gaussians for count/scatter
+    uint2 *ranges;             // [tiles] [start, end) into kv[0]
+    // reduce-then-scan scratch (4096-element chunks)
+    uint32_t *sums;            // [max_chunks] chunk sums of the order-preserving scans
+    uint32_t *cmat;            // [256][max_chunks] per-chunk digit counts -> offsets
+    uint32_t *row_total;       // [256] digit totals
+    size_t max_chunks;
     Counters *counters;
     // scene staging for the host-pointer entry point
     float *stage;

@@ -212,15 +212,14 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
     const size_t N = (size_t)max_points, K = (size_t)max_keys, T = (size_t)c->max_tiles;
     gs::Workspace &w = c->ws;
-    w.count_blocks = 2 * c->num_sms;
+    w.max_chunks = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1;
     cudaError_t e = cudaSuccess;
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
     A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
-    A(w.radius, N);
-    A(w.kv[0], K); A(w.kv[1], K); A(w.kt[0], K); A(w.kt[1], K);
-    A(w.cnt, (size_t)w.count_blocks * T); A(w.tile_total, T); A(w.tile_start, T); A(w.ranges, T);
-    A(w.big_list, T); A(w.huge_list, T);
+    A(w.radius, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
+    A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
+    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 256); A(w.row_total, 256);
     A(w.counters, 1);
 #undef A
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -237,9 +236,9 @@ int gs_ctx_destroy(gs_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     gs::Workspace &w = c->ws;
-    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.kv[0], w.kv[1],
-                    w.kt[0], w.kt[1], w.cnt, w.tile_total, w.tile_start, w.ranges, w.big_list, w.huge_list,
-                    w.counters, w.stage, c->frame_rgb, c->frame_T};
+    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+                    w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
+                    w.ranges, w.sums, w.cmat, w.row_total, w.counters, w.stage, c->frame_rgb, c->frame_T};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &e : c->ev) cudaEventDestroy(e);
@@ -256,7 +255,7 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
-    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[1], c->ws.ranges, W, H, *o, out_rgb, out_T,
+    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb, out_T,
                   nullptr);
     mark(c, st, *o, 3);
     return finish(c, st, *o, N);
@@ -389,7 +388,7 @@ int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const
     if (s.status) return s.status;
     if (s.n_keys > capacity) return GS_ERR_CAPACITY;
     const int ntiles = gs::ceil_div_i(W, GS_TILE) * gs::ceil_div_i(H, GS_TILE);
-    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[1], c->ws.depth_bits, keys, vals);
+    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[0], c->ws.depth_bits, keys, vals);
     cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
     if (check_cuda(cudaStreamSynchronize(st))) return GS_ERR_CUDA;
     return GS_OK;

@@ -1,0 +1,59 @@
+"""N > 1 host path on CPU: view partition and the frame gather (gloo, world size 2)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2604_02120_b200.orbit import gather_frames, partition_views
+
+
+def test_partition_covers_views_once():
+    for world in (1, 2, 4, 8):
+        seen = [v for r in range(world) for v in partition_views(64, world, r)]
+        assert seen == list(range(64))
+    with pytest.raises(ValueError):
+        partition_views(64, 3, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    views = partition_views(8, world, rank)
+    H, W = 3, 5
+    # frame content encodes its view id, as a render of view v would
+    rgb = torch.stack([torch.full((3, H, W), float(v)) for v in views])
+    T = torch.stack([torch.full((H, W), -float(v)) for v in views])
+    a, b = gather_frames(rgb, T, world, rank)
+    if rank == 0:
+        q.put((a.clone(), b.clone()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_frames_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    rgb, T = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert rgb.shape == (8, 3, 3, 5) and T.shape == (8, 3, 5)
+    for v in range(8):
+        assert (rgb[v] == v).all() and (T[v] == -v).all()
