@@ -187,6 +187,13 @@ int gs_debug_exponents(gs_ctx *ctx, void *stream, int N, const float *xy, const 
                        const float *opacity, const uint32_t *vals, int64_t K,
                        const uint32_t *ranges, int W, int H, float *out_m);
 
+/* Debug: while `trace` is non-NULL, the tensor-core blend of CTA 0 records
+ * clock64() timestamps of its per-batch pipeline events into trace[b*16 + e]
+ * (b < 1024; e: 0/1 producer push begin/end, 2/3/4 builder got-raw /
+ * stage-free / done, 5/6 MMA rows-ready / issue, 7/8 and 9/10 compositor warps
+ * 0 and 7 start / release). Device buffer of 16384 int64. NULL disables. */
+int gs_debug_set_trace(gs_ctx *ctx, long long *trace);
+
 #ifdef __cplusplus
 }
 #endif

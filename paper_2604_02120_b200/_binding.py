@@ -32,7 +32,8 @@ GS_FLAG_STATS = 4
 # every entry point declared in include/gs_render.h
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
-           "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times")
+           "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times",
+           "gs_debug_set_trace")
 
 
 class GsError(RuntimeError):
@@ -87,6 +88,7 @@ def load():
         "gs_debug_blend": [P, P, I, P, P, P, P, P, I64, P, I, I, opt_p, P, P],
         "gs_debug_exponents": [P, P, I, P, P, P, P, I64, P, I, I, P],
         "gs_stage_times": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
+        "gs_debug_set_trace": [P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -229,6 +231,9 @@ class Context:
         _check(self.lib.gs_debug_blend(self.h, _stream(stream), n, _ptr(xy), _ptr(conic), _ptr(opacity),
                                        _ptr(rgb), _ptr(vals), int(K), _ptr(ranges), W, H, ctypes.byref(o),
                                        _ptr(out_rgb), _ptr(out_T)), "gs_debug_blend")
+
+    def gs_debug_set_trace(self, trace):
+        _check(self.lib.gs_debug_set_trace(self.h, _ptr(trace)), "gs_debug_set_trace")
 
     def gs_debug_exponents(self, n, xy, conic, opacity, vals, K, ranges, W, H, out_m, stream=None):
         _check(self.lib.gs_debug_exponents(self.h, _stream(stream), n, _ptr(xy), _ptr(conic), _ptr(opacity),

@@ -28,19 +28,45 @@
 namespace gs {
 
 constexpr int NB = 32;        // Gaussians per batch (MMA N)
-constexpr int STAGES = 4;     // smem / TMEM ring depth
+constexpr int STAGES = 4;     // M_g / TMEM ring depth
 constexpr int NCW = 8;        // compositor warps: 256 pixels
-constexpr int TC_THREADS = (NCW + 1) * 32;
+constexpr int NBLD = 2;       // builder warps (alternate batches)
+constexpr int RAW = 4;        // raw-record ring (producer -> builders): gathers in flight
+constexpr int PF = 4;         // index lookahead of the producer (batches)
+constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
+constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_MMA = NCW + 1 + NBLD;
+constexpr int TC_THREADS = (NCW + 2 + NBLD) * 32;
 constexpr int TMEM_COLS = STAGES * 2 * NB;   // 256
 static_assert(TMEM_COLS == 256, "TMEM allocation must be a power of two");
+// Batch b of a CTA's stream (data batch, end-of-tile marker or terminal)
+//   raw slot b % RAW  (producer -> builder b % NBLD),
+//   M_g/TMEM stage b % STAGES (builder -> MMA warp -> compositors),
+//   colour/header slot b % RING. A builder writes stage/slot of batch b only
+// after the MMA of batch b - STAGES completed, which required every compositor
+// warp to release batch b - 2*STAGES: RING = 2*STAGES slots need no extra wait.
+// Header: {tile, seq, count, list offset}; count 0 = end-of-tile marker,
+// count -1 = batch of an already terminated tile (skipped), tile -1 = terminal.
+
+struct RawRec {        // one gathered Gaussian (cp.async destinations)
+    float2 m;          // projected mean
+    float2 pad;
+    float4 co;         // (A, B, C, opacity)
+    float4 col;        // (r, g, b, 0)
+};
 
 struct __align__(1024) SmemTC {
     uint8_t A[2][128 * 64];       // M_p halves: 128 rows x 16 tf32, interleaved core matrices
     uint8_t B[STAGES][NB * 64];   // M_g rows
-    float4 rgb[STAGES][NB];
-    int4 hdr[STAGES];             // {tile, seq, count, list offset}
-    uint64_t full[STAGES];
-    uint64_t empty[STAGES];
+    float4 rgb[RING][NB];
+    int4 hdr[RING];
+    RawRec raw[RAW][NB];
+    int4 raw_hdr[RAW];
+    uint64_t full[STAGES];        // MMA done (commit), or marker -> compositors
+    uint64_t empty[STAGES];       // compositors released the TMEM stage -> MMA warp
+    uint64_t rows_ready[STAGES];  // M_g rows built -> MMA warp
+    uint64_t slot_ready[RING];    // colours/header written -> compositors
+    uint64_t raw_full[RAW];       // producer -> builder
+    uint64_t raw_empty[RAW];      // builder -> producer
     uint32_t tmem_base;
     uint32_t warp_done_seq[NCW];
 };
@@ -56,6 +82,12 @@ __device__ __forceinline__ void pixel_of(int p, int &x, int &y) {
     const int w = p >> 5, l = p & 31;
     x = 8 * (w & 1) + (l & 7);
     y = 4 * (w >> 1) + (l >> 3);
+}
+
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -82,13 +114,61 @@ __device__ __forceinline__ void gather(Rec &r, const float2 *__restrict__ xy, co
     }
 }
 
-template <bool DUMP, bool STATS>
+__device__ __forceinline__ bool tile_done(const SmemTC &sm, int lane, uint32_t seq) {
+    const uint32_t dseq = lane < NCW ? *((volatile const uint32_t *)&sm.warp_done_seq[lane]) : seq;
+    return __all_sync(0xffffffffu, dseq >= seq);
+}
+
+// Row j of M_g for batch `hd` (lane j): Eq. (6) v_g with xh = x_g - x_c, yh = y_g - y_c,
+// scaled by log2(e), log2(o) folded into the constant term (R-10), split into TF32
+// hi + lo (R-11); padding rows get the exponent -1e30 (never kept).
+__device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const int4 &hd, const RawRec &rr, int lane,
+                                          int gx) {
+    uint32_t u[16];
+    if (lane < hd.z) {
+        const float xc = (float)(GS_TILE * (hd.x % gx)) + 7.5f;
+        const float yc = (float)(GS_TILE * (hd.x / gx)) + 7.5f;
+        const float xh = rr.m.x - xc, yh = rr.m.y - yc;
+        const float A = rr.co.x, B = rr.co.y, C = rr.co.z;
+        float v[6];
+        v[0] = -0.5f * A * LOG2E;
+        v[1] = -0.5f * C * LOG2E;
+        v[2] = -B * LOG2E;
+        v[3] = -(A * xh + B * yh) * LOG2E;
+        v[4] = -(C * yh + B * xh) * LOG2E;
+        v[5] = -(0.5f * A * xh * xh + 0.5f * C * yh * yh + B * xh * yh) * LOG2E + lg2_approx(rr.co.w);
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+            const uint32_t hi = f32_to_tf32_rna(v[k]);
+            const uint32_t lo = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
+            u[k] = hi;
+            u[6 + k] = lo;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 12; k++) u[k] = 0u;
+        u[5] = __float_as_uint(-1e30f);
+    }
+    u[12] = u[13] = u[14] = u[15] = 0u;
+    const uint32_t rb = smem_u32(&sm.B[stage][0]);
+#pragma unroll
+    for (int c = 0; c < 4; c++) st_shared_v4(rb + op_off(lane, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
+    sm.rgb[slot][lane] = rr.col;
+}
+
+// optional per-batch event trace of CTA 0 (debug builds of the timeline): trace[b*16 + ev] = clock64
+#define TRACE_EV(ev, b)                                                                                   \
+    do {                                                                                                  \
+        if (TRACE && blockIdx.x == 0 && (b) < 1024u && lane == 0) trace[(size_t)(b) * 16 + (ev)] = clock64(); \
+    } while (0)
+
+template <bool DUMP, bool STATS, bool TRACE>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W,
                int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
-               unsigned long long *stat_kept) {
+               unsigned long long *stat_kept, long long *trace) {
     extern __shared__ uint8_t smem_raw[];
     SmemTC &sm = *reinterpret_cast<SmemTC *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,8 +176,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     // ---- one-time setup -------------------------------------------------
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(&sm.full[s], 33);          // 32 producer lanes + 1 MMA commit
-            mbar_init(&sm.empty[s], NCW);        // one arrival per compositor warp
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NCW);
+            mbar_init(&sm.rows_ready[s], 1);
+        }
+        for (int r = 0; r < RING; r++) mbar_init(&sm.slot_ready[r], 1);
+        for (int r = 0; r < RAW; r++) {
+            mbar_init(&sm.raw_full[r], 33);      // 32 cp.async completions (noinc) + header
+            mbar_init(&sm.raw_empty[r], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -118,7 +204,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         for (int c = 0; c < 4; c++) st_shared_v4(base + op_off(r, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
         if (lane == 0) sm.warp_done_seq[warp] = 0;
         fence_proxy_async_smem();
-    } else {
+    } else if (warp == WARP_MMA) {
         tmem_alloc(&sm.tmem_base, TMEM_COLS);
         tmem_relinquish();
     }
@@ -127,37 +213,29 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
 
-    if (warp == NCW) {
-        // =================== producer + MMA issuer ===================
-        // Software pipeline over the flattened stream of (tile, batch):
-        //   indices of batch k+1 and the records of batch k were requested one
-        //   iteration earlier, and the first batch of the next tile is fetched
-        //   in four steps spread over the current tile's iterations, so the
-        //   compositors never wait for a full gather latency (~1 us).
-        constexpr uint32_t IDESC = idesc_tf32(128, NB);
-        const uint32_t a_base = smem_u32(&sm.A[0][0]);
-        const uint32_t b_base = smem_u32(&sm.B[0][0]);
-        uint32_t s = 0, ph = 0;
+    if (warp == WARP_PRODUCER) {
+        // =================== producer: asynchronous gathers ===================
+        // Lane j of batch b copies record j (mean, conic+opacity, colour) with
+        // cp.async straight into raw slot b % RAW; the slot's barrier completes
+        // when the copies land, so RAW batches of gathers are in flight. The
+        // indices run PF batches ahead in registers; the next tile's first PF
+        // index vectors are fetched in three steps during the current tile.
+        uint32_t b_idx = 0;
         unsigned long long n_eval = 0;
-        // current tile
         int tile = 0;
         if (lane == 0) tile = (int)atomicAdd(tile_queue, 1u);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         uint2 rg = tile < ntiles ? ranges[tile] : make_uint2(0u, 0u);
         uint32_t seq = 1;
         uint32_t b = rg.x;
-        Rec cur;
-        uint32_t inext;
-        {
-            const uint32_t i0 = (b + lane < rg.y) ? vals[b + lane] : 0u;
-            inext = (b + NB + lane < rg.y) ? vals[b + NB + lane] : 0u;
-            gather(cur, xy, conic_o, rgb, i0, b + lane < rg.y);
-        }
-        // next-tile head
+        uint32_t idx[PF];
+#pragma unroll
+        for (int j = 0; j < PF; j++) idx[j] = (b + j * NB + lane < rg.y) ? vals[b + j * NB + lane] : 0u;
         int hstate = 0, ntile = 0, ntile_l0 = 0;
         uint2 nrg = make_uint2(0u, 0u);
-        uint32_t hidx0 = 0, hidx1 = 0;
-        Rec h0;
+        uint32_t hidx[PF];
+#pragma unroll
+        for (int j = 0; j < PF; j++) hidx[j] = 0u;
         auto head_step = [&]() {
             switch (hstate) {
                 case 0:
@@ -168,109 +246,131 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                     nrg = ntile < ntiles ? ranges[ntile] : make_uint2(0u, 0u);
                     break;
                 case 2:
-                    hidx0 = (nrg.x + lane < nrg.y) ? vals[nrg.x + lane] : 0u;
-                    hidx1 = (nrg.x + NB + lane < nrg.y) ? vals[nrg.x + NB + lane] : 0u;
-                    break;
-                case 3:
-                    gather(h0, xy, conic_o, rgb, hidx0, nrg.x + lane < nrg.y);
+#pragma unroll
+                    for (int j = 0; j < PF; j++)
+                        hidx[j] = (nrg.x + j * NB + lane < nrg.y) ? vals[nrg.x + j * NB + lane] : 0u;
                     break;
                 default:
                     return;
             }
             hstate++;
         };
+        // stage batch b_idx: header (+ records of lanes < hd.z) into raw slot
+        auto push = [&](const int4 &hd, uint32_t gi) {
+            const int r = b_idx % RAW;
+            TRACE_EV(0, b_idx);
+            mbar_wait(&sm.raw_empty[r], ((b_idx / RAW) & 1u) ^ 1u);
+            TRACE_EV(1, b_idx);
+            if (lane < hd.z) {
+                RawRec &d = sm.raw[r][lane];
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&d.m)), "l"(xy + gi) : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.co)), "l"(conic_o + gi)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.col)), "l"(rgb + gi)
+                             : "memory");
+            }
+            if (lane == 0) {
+                sm.raw_hdr[r] = hd;
+                mbar_arrive(&sm.raw_full[r]);
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.raw_full[r]))
+                         : "memory");
+            b_idx++;
+        };
         for (;;) {
             if (tile >= ntiles) {
-                mbar_wait(&sm.empty[s], ph ^ 1);
-                if (lane == 0) sm.hdr[s] = make_int4(-1, 0, 0, 0);
-                mbar_arrive(&sm.full[s]);
-                if (lane == 0) mbar_arrive(&sm.full[s]);
+                for (int t = 0; t < NBLD; t++) push(make_int4(-1, 0, 0, 0), 0u);   // one per builder
                 if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
                 break;
             }
             head_step();
             bool end = b >= rg.y;
-            if (!DUMP && !end) {
-                const uint32_t dseq = lane < NCW ? *((volatile uint32_t *)&sm.warp_done_seq[lane]) : seq;
-                end = __all_sync(0xffffffffu, dseq >= seq);   // every pixel of the tile terminated
-            }
+            if (!DUMP && !end) end = tile_done(sm, lane, seq);
             if (end) {
-                mbar_wait(&sm.empty[s], ph ^ 1);
-                if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, 0, 0);
-                mbar_arrive(&sm.full[s]);
-                if (lane == 0) mbar_arrive(&sm.full[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-                while (hstate < 4) head_step();
+                push(make_int4(tile, (int)seq, 0, 0), 0u);   // end-of-tile marker
+                while (hstate < 3) head_step();
                 tile = ntile;
                 rg = nrg;
                 b = rg.x;
                 seq++;
-                cur = h0;
-                inext = hidx1;
+#pragma unroll
+                for (int j = 0; j < PF; j++) idx[j] = hidx[j];
                 hstate = 0;
                 continue;
             }
-            // prefetch: records of batch b+NB, indices of batch b+2NB
-            Rec nx;
-            gather(nx, xy, conic_o, rgb, inext, b + NB + lane < rg.y);
-            const uint32_t inext2 = (b + 2 * NB + lane < rg.y) ? vals[b + 2 * NB + lane] : 0u;
             const uint32_t cnt = min((uint32_t)NB, rg.y - b);
-            const float xc = (float)(GS_TILE * (tile % gx)) + 7.5f;
-            const float yc = (float)(GS_TILE * (tile / gx)) + 7.5f;
-            uint32_t u[16];
-            if ((uint32_t)lane < cnt) {
-                // Eq. (6): v_g with xh = x_g - x_c, yh = y_g - y_c, times log2(e); + log2(o)
-                const float xh = cur.m.x - xc, yh = cur.m.y - yc;
-                const float A = cur.co.x, B = cur.co.y, C = cur.co.z;
-                float v[6];
-                v[0] = -0.5f * A * LOG2E;
-                v[1] = -0.5f * C * LOG2E;
-                v[2] = -B * LOG2E;
-                v[3] = -(A * xh + B * yh) * LOG2E;
-                v[4] = -(C * yh + B * xh) * LOG2E;
-                v[5] = -(0.5f * A * xh * xh + 0.5f * C * yh * yh + B * xh * yh) * LOG2E + lg2_approx(cur.co.w);
-#pragma unroll
-                for (int k = 0; k < 6; k++) {
-                    const uint32_t hi = f32_to_tf32_rna(v[k]);
-                    const uint32_t lo = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
-                    u[k] = hi;
-                    u[6 + k] = lo;
-                }
-            } else {
-                // padding column: exponent -1e30, never kept by any pixel
-#pragma unroll
-                for (int k = 0; k < 12; k++) u[k] = 0u;
-                u[5] = __float_as_uint(-1e30f);
-            }
-            u[12] = u[13] = u[14] = u[15] = 0u;
-            mbar_wait(&sm.empty[s], ph ^ 1);
-            const uint32_t rb = b_base + s * (NB * 64);
-#pragma unroll
-            for (int c = 0; c < 4; c++)
-                st_shared_v4(rb + op_off(lane, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
-            sm.rgb[s][lane] = cur.col;
-            if (lane == 0) sm.hdr[s] = make_int4(tile, (int)seq, (int)cnt, (int)b);
+            push(make_int4(tile, (int)seq, (int)cnt, (int)b), idx[0]);
             if (STATS && lane == 0) n_eval += (unsigned long long)cnt * GS_TILE_PIX;
-            fence_proxy_async_smem();
-            mbar_arrive(&sm.full[s]);
+#pragma unroll
+            for (int j = 0; j + 1 < PF; j++) idx[j] = idx[j + 1];
+            idx[PF - 1] = (b + PF * NB + lane < rg.y) ? vals[b + PF * NB + lane] : 0u;
+            b += NB;
+        }
+    } else if (warp >= WARP_BUILD0 && warp < WARP_BUILD0 + NBLD) {
+        // =================== builders: M_g rows (Eq. 6-7) ===================
+        for (uint32_t kb = warp - WARP_BUILD0;; kb += NBLD) {
+            const int r = kb % RAW, s = kb % STAGES, slot = kb % RING;
+            mbar_wait(&sm.raw_full[r], (kb / RAW) & 1u);
+            TRACE_EV(2, kb);
+            int4 hd = sm.raw_hdr[r];
+            // stage s / slot are reusable once batch kb-STAGES went through the MMA warp
+            // (for every batch kind: this also keeps the rows_ready / slot_ready phases in step)
+            if (kb >= STAGES) mbar_wait(&sm.full[s], ((kb / STAGES) - 1) & 1u);
+            TRACE_EV(3, kb);
+            if (hd.z > 0) {
+                if (!DUMP && tile_done(sm, lane, (uint32_t)hd.y)) hd.z = -1;   // tile already terminated
+            }
+            if (hd.z > 0) {
+                build_row(sm, s, slot, hd, sm.raw[r][lane], lane, gx);
+                fence_proxy_async_smem();
+            }
+            if (lane == 0) sm.hdr[slot] = hd;
             __syncwarp();
             if (lane == 0) {
-                tc_fence_after();
+                mbar_arrive(&sm.raw_empty[r]);
+                mbar_arrive(&sm.slot_ready[slot]);
+                mbar_arrive(&sm.rows_ready[s]);
+            }
+            TRACE_EV(4, kb);
+            if (hd.x < 0) break;
+        }
+    } else if (warp == WARP_MMA) {
+        // =================== MMA issuer ===================
+        constexpr uint32_t IDESC = idesc_tf32(128, NB);
+        const uint32_t a_base = smem_u32(&sm.A[0][0]);
+        const uint32_t b_base = smem_u32(&sm.B[0][0]);
+        uint64_t adesc[2][2];   // [K-step][pixel half]; B descriptors differ only by the stage offset
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) adesc[kk][h] = umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512);
+        const uint64_t bdesc0 = umma_desc(b_base, 128, 512), bdesc1 = umma_desc(b_base + 256, 128, 512);
+        for (uint32_t k = 0;; k++) {
+            const int s = k % STAGES;
+            const uint32_t ph = (k / STAGES) & 1u;
+            mbar_wait(&sm.rows_ready[s], ph);
+            TRACE_EV(5, k);
+            const int4 hd = sm.hdr[k % RING];
+            if (hd.z <= 0) {                    // marker or skipped batch: no MMA
+                mbar_wait(&sm.empty[s], ph ^ 1u);
+                if (lane == 0) mbar_arrive(&sm.full[s]);
+                if (hd.x < 0) break;
+                continue;
+            }
+            mbar_wait(&sm.empty[s], ph ^ 1u);   // batch k-STAGES no longer read from TMEM
+            TRACE_EV(6, k);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint64_t soff = (uint64_t)((s * (NB * 64)) >> 4);   // start-address field, 16 B units
 #pragma unroll
                 for (int kk = 0; kk < 2; kk++)
 #pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const uint64_t ad = umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512);
-                        const uint64_t bd = umma_desc(b_base + s * (NB * 64) + kk * 256, 128, 512);
-                        mma_tf32(tmem + s * (2 * NB) + h * NB, ad, bd, IDESC, kk);
-                    }
+                    for (int h = 0; h < 2; h++)
+                        mma_tf32(tmem + s * (2 * NB) + h * NB, adesc[kk][h], (kk ? bdesc1 : bdesc0) + soff, IDESC,
+                                 kk);
                 mma_commit(&sm.full[s]);
             }
             __syncwarp();
-            if (++s == STAGES) { s = 0; ph ^= 1; }
-            cur = nx;
-            inext = inext2;
-            b += NB;
         }
     } else {
         // =================== compositors ===================
@@ -279,21 +379,27 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         pixel_of(p, x, y);
         const uint32_t t_lane = (uint32_t)(32 * (warp & 3)) << 16;
         const uint32_t t_half = (uint32_t)(warp >> 2) * NB;
-        uint32_t s = 0, ph = 0;
-        float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-        bool done = false, wdone = false;
+        // Pixel state. Termination is encoded in the skip threshold: thr = +inf once the
+        // pixel has stopped (R-2), so "live" is a single compare and no bool is carried.
+        float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
+        bool wdone = false;
         uint32_t n_kept = 0;
-        for (;;) {
-            mbar_wait(&sm.full[s], ph);
+        for (uint32_t k = 0;; k++) {
+            const int s = k % STAGES;
+            const int c_slot = k % RING;
+            mbar_wait(&sm.slot_ready[c_slot], (k / RING) & 1u);
+            mbar_wait(&sm.full[s], (k / STAGES) & 1u);
+            if (warp == 0) TRACE_EV(7, k);
+            if (warp == 7) TRACE_EV(9, k);
             tc_fence_after();
-            const int4 hd = sm.hdr[s];
+            const int4 hd = sm.hdr[c_slot];
             if (hd.z == 0) {
                 if (hd.x < 0) {
                     if (STATS) {
-                        unsigned long long k = n_kept;
+                        unsigned long long kk = n_kept;
 #pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-                        if (lane == 0) atomicAdd(stat_kept, k);
+                        for (int o = 16; o > 0; o >>= 1) kk += __shfl_xor_sync(0xffffffffu, kk, o);
+                        if (lane == 0) atomicAdd(stat_kept, kk);
                     }
                     break;
                 }
@@ -307,8 +413,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                         out_T[pix] = T;
                     }
                 }
-                T = 1.0f; C0 = C1 = C2 = 0.f; done = false; wdone = false;
-            } else if (!wdone) {
+                T = 1.0f; C0 = C1 = C2 = 0.f; thr = LOG2_ALPHA_MIN; wdone = false;
+            } else if (hd.z > 0 && !wdone) {
                 float m[NB];
                 tmem_ld32(tmem + t_lane + s * (2 * NB) + t_half, m);
                 tmem_wait_ld();
@@ -317,29 +423,26 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                     for (int j = 0; j < cnt; j++) dump_m[((size_t)hd.w + j) * GS_TILE_PIX + p] = m[j];
                 } else {
                     // columns j >= cnt hold the padding exponent -1e30: no count checks needed
+                    const uint32_t crow = smem_u32(&sm.rgb[c_slot][0]);
 #pragma unroll
                     for (int j = 0; j < NB; j++) {
                         const float mj = m[j];
-                        const bool live = (mj >= LOG2_ALPHA_MIN) && !done;
-                        if (__any_sync(0xffffffffu, live)) {
-                            const float4 c = sm.rgb[s][j];
-                            const float a = fminf(ALPHA_MAX, ex2_approx(mj));
-                            const float tT = T * (1.0f - a);
-                            if (live) {
-                                if (STATS) n_kept++;
-                                if (tT < T_MIN) {
-                                    done = true;
-                                } else {
-                                    const float wgt = a * T;
-                                    C0 += wgt * c.x;
-                                    C1 += wgt * c.y;
-                                    C2 += wgt * c.z;
-                                    T = tT;
-                                }
-                            }
+                        const bool live = mj >= thr;                    // alpha >= 1/255 (R-1), pixel running
+                        if (__any_sync(0xffffffffu, live)) {            // warp-uniform skip
+                            const float4 c = ld_shared_f4(crow + 16 * j);
+                            const float a = fminf(ALPHA_MAX, ex2_approx(mj));   // alpha = 2^m capped (R-4)
+                            const float tT = fmaf(-a, T, T);                    // T (1 - alpha)
+                            const float w = a * T;
+                            const bool acc = live && tT >= T_MIN;               // composite (Eq. 1, R-3)
+                            if (STATS) n_kept += live ? 1u : 0u;
+                            C0 = acc ? fmaf(w, c.x, C0) : C0;
+                            C1 = acc ? fmaf(w, c.y, C1) : C1;
+                            C2 = acc ? fmaf(w, c.z, C2) : C2;
+                            T = acc ? tT : T;
+                            thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;   // stop (R-2)
                         }
                     }
-                    if (__all_sync(0xffffffffu, done)) {
+                    if (__all_sync(0xffffffffu, thr > 0.f)) {
                         wdone = true;
                         if (lane == 0) *((volatile uint32_t *)&sm.warp_done_seq[warp]) = (uint32_t)hd.y;
                     }
@@ -347,17 +450,20 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             }
             tc_fence_before();
             __syncwarp();
+            if (warp == 0) TRACE_EV(8, k);
+            if (warp == 7) TRACE_EV(10, k);
             if (lane == 0) mbar_arrive(&sm.empty[s]);
-            if (++s == STAGES) { s = 0; ph ^= 1; }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == NCW) {
+    if (warp == WARP_MMA) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
 }
+
+long long *g_blend_trace = nullptr;   // set by gs_debug_set_trace (debug only)
 
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
@@ -366,26 +472,25 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
     const size_t smem = sizeof(SmemTC) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_blend_tc<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
     const int grid = std::max(1, std::min(2 * num_sms, ntiles));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
+#define ARGS xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
-        k_blend_tc<true, false><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
-                                                                 bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
-                                                                 se, sk);
+        k_blend_tc<true, false, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
     else if (stats)
-        k_blend_tc<false, true><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
-                                                                 bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
-                                                                 se, sk);
+        k_blend_tc<false, true, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
+    else if (g_blend_trace)
+        k_blend_tc<false, false, true><<<grid, TC_THREADS, smem, st>>>(ARGS, g_blend_trace);
     else
-        k_blend_tc<false, false><<<grid, TC_THREADS, smem, st>>>(xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
-                                                                  bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue,
-                                                                  se, sk);
+        k_blend_tc<false, false, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
+#undef ARGS
 }
 
 // ===========================================================================

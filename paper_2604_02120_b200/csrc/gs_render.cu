@@ -141,6 +141,16 @@ __global__ void k_unpack_pre(int N, gs::Workspace ws, float *depth, float *xy, f
                              int32_t *rect, int32_t *radius, uint32_t *touched) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
+    if (ws.touched[i] == 0) {   // culled: the preprocess writes only touched = 0
+        depth[i] = 0.f;
+        xy[2 * i] = xy[2 * i + 1] = 0.f;
+        conic[3 * i] = conic[3 * i + 1] = conic[3 * i + 2] = 0.f;
+        rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = 0.f;
+        rect[4 * i] = rect[4 * i + 1] = rect[4 * i + 2] = rect[4 * i + 3] = 0;
+        radius[i] = 0;
+        touched[i] = 0u;
+        return;
+    }
     depth[i] = __uint_as_float(ws.depth_bits[i]);
     xy[2 * i] = ws.xy[i].x;
     xy[2 * i + 1] = ws.xy[i].y;
@@ -420,6 +430,12 @@ int gs_debug_blend(gs_ctx *c, void *stream, int N, const float *xy, const float 
     if (!out_rgb || !out_T || (N > 0 && !rgb)) return GS_ERR_INVALID_ARG;
     return debug_blend_common(c, stream, N, xy, conic, opacity, rgb, vals, K, ranges, W, H, o, out_rgb, out_T,
                               nullptr);
+}
+
+int gs_debug_set_trace(gs_ctx *c, long long *trace) {
+    if (!c) return GS_ERR_INVALID_ARG;
+    gs::g_blend_trace = trace;
+    return GS_OK;
 }
 
 int gs_debug_exponents(gs_ctx *c, void *stream, int N, const float *xy, const float *conic, const float *opacity,

@@ -19,31 +19,38 @@ __device__ __forceinline__ int rect_bound(float v, int g) {
     return (int)c;
 }
 
-__global__ void __launch_bounds__(256) k_preprocess(int N, const float *__restrict__ means,
-                                                    const float *__restrict__ scales,
-                                                    const float4 *__restrict__ rots,
-                                                    const float *__restrict__ opacity,
-                                                    const float *__restrict__ shs, int sh_degree,
-                                                    int sh_stride, float scale_mod, int W, int H,
-                                                    const gs_camera cam, Workspace ws) {
+constexpr int PRE_THREADS = 256;
+
+// Two dependent memory round trips per Gaussian: (means, rotation, scales,
+// opacity) together, then -- only for projected Gaussians -- the SH row.
+// Every output is written for every Gaussian (zeros when culled) so that
+// all stores are full sectors.
+__global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const float *__restrict__ means,
+                                                               const float *__restrict__ scales,
+                                                               const float4 *__restrict__ rots,
+                                                               const float *__restrict__ opacity,
+                                                               const float *__restrict__ shs, int sh_degree,
+                                                               int sh_stride, float scale_mod, int W, int H,
+                                                               const gs_camera cam, Workspace ws) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const float *R = cam.R;
     const int gx = (W + GS_TILE - 1) / GS_TILE, gy = (H + GS_TILE - 1) / GS_TILE;
 
-    bool vis = false;
-    float vz = 0.f, mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f;
-    float col0 = 0.f, col1 = 0.f, col2 = 0.f;
-    int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
+    const float px = __ldcs(means + 3 * i), py = __ldcs(means + 3 * i + 1), pz = __ldcs(means + 3 * i + 2);
+    const float4 q = __ldcs(rots + i);
+    const float s0 = __ldcs(scales + 3 * i), s1 = __ldcs(scales + 3 * i + 1), s2 = __ldcs(scales + 3 * i + 2);
+    const float op = __ldcs(opacity + i);
 
-    const float px = means[3 * i], py = means[3 * i + 1], pz = means[3 * i + 2];
+    bool vis = false;
+    float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f;
+    int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
     // 1. view-space point
     const float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam.t[0];
     const float vy = ((R[3] * px + R[4] * py) + R[5] * pz) + cam.t[1];
-    vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam.t[2];
+    const float vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam.t[2];
     if (vz > cam.znear) {
         // 2. quaternion normalisation
-        const float4 q = rots[i];
         const float n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
         const float nr = sqrtf(n2);
         const float w = q.x / nr, x = q.y / nr, y = q.z / nr, z = q.w / nr;
@@ -56,9 +63,10 @@ __global__ void __launch_bounds__(256) k_preprocess(int N, const float *__restri
         M[2][0] = 2.0f * (xz - wy); M[2][1] = 2.0f * (yz + wx); M[2][2] = 1.0f - 2.0f * (xx + yy);
         // 4. 3D covariance
         float v[3];
+        const float sc[3] = {s0, s1, s2};
 #pragma unroll
         for (int k = 0; k < 3; k++) {
-            const float g = scale_mod * scales[3 * i + k];
+            const float g = scale_mod * sc[k];
             v[k] = g * g;
         }
         float u[3][3], S[3][3];
@@ -126,21 +134,19 @@ __global__ void __launch_bounds__(256) k_preprocess(int N, const float *__restri
         return;
     }
     // 11. colour
+    float col0, col1, col2;
     if (sh_degree < 0) {
         col0 = shs[3 * (size_t)i]; col1 = shs[3 * (size_t)i + 1]; col2 = shs[3 * (size_t)i + 2];
     } else {
-        const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
-        const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
-        const float X = dx / len, Y = dy / len, Z = dz / len;
-        const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
         const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+        const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
         float k[48];
         if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
             const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
 #pragma unroll
             for (int j = 0; j < 12; j++) {
                 if (4 * j < ncoef * 3) {
-                    const float4 t4 = __ldg(sh4 + j);
+                    const float4 t4 = __ldcs(sh4 + j);
                     k[4 * j] = t4.x; k[4 * j + 1] = t4.y; k[4 * j + 2] = t4.z; k[4 * j + 3] = t4.w;
                 }
             }
@@ -149,6 +155,9 @@ __global__ void __launch_bounds__(256) k_preprocess(int N, const float *__restri
             for (int j = 0; j < 48; j++)
                 if (j < ncoef * 3) k[j] = __ldg(sh + j);
         }
+        const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
+        const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+        const float X = dx / len, Y = dy / len, Z = dz / len;
         const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
         const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
                     C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
@@ -186,7 +195,7 @@ __global__ void __launch_bounds__(256) k_preprocess(int N, const float *__restri
     // 12. outputs
     ws.depth_bits[i] = __float_as_uint(vz);
     ws.xy[i] = make_float2(mx, my);
-    ws.conic_o[i] = make_float4(cA, cB, cC, opacity[i]);
+    ws.conic_o[i] = make_float4(cA, cB, cC, op);
     ws.rgb[i] = make_float4(col0, col1, col2, 0.f);
     ws.rect[i] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
                               (unsigned short)ymax);
@@ -198,8 +207,9 @@ void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float 
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
                        int sh_stride, float scale_mod, const gs_camera &cam, int W, int H) {
     if (N <= 0) return;
-    k_preprocess<<<ceil_div_i(N, 256), 256, 0, st>>>(N, means, scales, reinterpret_cast<const float4 *>(rots),
-                                                     opacity, shs, sh_degree, sh_stride, scale_mod, W, H, cam, ws);
+    k_preprocess<<<ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st>>>(
+        N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
+        H, cam, ws);
 }
 
 }  // namespace gs
