@@ -74,7 +74,11 @@ enum {
 enum {
     GS_FLAG_SYNC = 1u,    /* synchronise the stream at the end and report device errors     */
     GS_FLAG_TIMING = 2u,  /* record CUDA events around the stages (read by gs_stage_times)  */
-    GS_FLAG_STATS = 4u    /* count blend work (pairs evaluated / kept) into gs_stats        */
+    GS_FLAG_STATS = 4u,   /* count blend work (pairs evaluated / kept) into gs_stats        */
+    GS_FLAG_TIGHT = 8u    /* tile-exact intersection: drop (Gaussian, tile) pairs whose
+                           * maximum over the tile's pixel box is alpha < 1/255 (with a margin
+                           * larger than the exponent error). Such pairs are alpha-skipped by the
+                           * blend anyway, so the image is bit-identical; binning keeps a subset. */
 };
 
 typedef struct {

@@ -92,27 +92,32 @@ struct CompactOp {   // visible flags -> (depth bits, index) of the visible Gaus
     __device__ void finish(uint64_t total) const { cnt->n_visible = (uint32_t)total; }
 };
 
-struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ gathered rects, chunk heads)
+struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ gathered rects/masks, chunk heads)
     const uint32_t *sorted_idx, *touched;
     const ushort4 *rect;
+    const unsigned long long *tmask;   // GS_FLAG_TIGHT tile masks (nullptr: whole rects)
     uint32_t *off;
     ushort4 *rect_r;
+    unsigned long long *tmask_r;
     uint32_t *chunk_first;
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
     struct Aux {
         ushort4 rc;
+        unsigned long long m;
     };
     __device__ uint32_t load(uint32_t r) const { return touched[sorted_idx[r]]; }
     __device__ uint32_t load(uint32_t r, Aux &a) const {
         const uint32_t i = sorted_idx[r];
         a.rc = rect[i];
+        a.m = tmask ? tmask[i] : ~0ull;
         return touched[i];
     }
     __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &a) const {
         off[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
         rect_r[r] = a.rc;
+        if (tmask) tmask_r[r] = a.m;
         // every 4096-pair chunk boundary inside [o, o+v) belongs to Gaussian r
         for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
             if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
@@ -253,18 +258,27 @@ struct PlainLoader {
 // Pairs cbase .. cbase+cvalid-1 of the depth-ordered duplication: pair p belongs
 // to the Gaussian r with off[r] <= p < off[r+1]; it is the (p - off[r])-th tile
 // of rect_r[r] in row-major order; value = sorted_idx[r].
+// q-th set bit of a 64-bit mask
+__device__ __forceinline__ uint32_t nth_set64(unsigned long long m, uint32_t q) {
+    const uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
+    const uint32_t c = __popc(lo);
+    return q < c ? __fns(lo, 0, (int)q + 1) : 32u + __fns(hi, 0, (int)(q - c) + 1);
+}
+
 struct Expander {
     const uint32_t *off, *sorted_idx, *chunk_first;
     const ushort4 *rect_r;
+    const unsigned long long *tmask_r;   // GS_FLAG_TIGHT: the q-th pair is the q-th kept tile
     const Counters *cnt;
     int gx;
     static constexpr int STAGE = 1024;                            // Gaussians staged in shared memory
-    static constexpr int SCRATCH_WORDS = SORT_CHUNK + 4 * STAGE;  // owner map + (off, rect, idx)
+    static constexpr int SCRATCH_WORDS = SORT_CHUNK + 6 * STAGE;  // owner map + (off, rect, idx, mask)
     __device__ void load(uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *scratch) const {
         uint32_t *s_owner = scratch;
         uint32_t *s_off = scratch + SORT_CHUNK;
         ushort4 *s_rect = reinterpret_cast<ushort4 *>(scratch + SORT_CHUNK + STAGE);
         uint32_t *s_idx = scratch + SORT_CHUNK + 3 * STAGE;
+        unsigned long long *s_msk = reinterpret_cast<unsigned long long *>(scratch + SORT_CHUNK + 4 * STAGE);
         const uint32_t nv = cnt->n_visible;
         const uint32_t chunk = cbase / SORT_CHUNK;
         const uint32_t nchunks = (uint32_t)((cnt->n_keys + SORT_CHUNK - 1) / SORT_CHUNK);
@@ -278,6 +292,7 @@ struct Expander {
                 s_off[j] = off[r_lo + j];
                 s_rect[j] = rect_r[r_lo + j];
                 s_idx[j] = sorted_idx[r_lo + j];
+                s_msk[j] = tmask_r ? tmask_r[r_lo + j] : ~0ull;
             }
         }
         __syncthreads();
@@ -316,8 +331,12 @@ struct Expander {
             const uint32_t j = s_owner[e];
             const uint32_t o = staged ? s_off[j] : off[r_lo + j];
             const ushort4 rc = staged ? s_rect[j] : rect_r[r_lo + j];
-            const uint32_t q = cbase + e - o;
+            uint32_t q = cbase + e - o;
             const uint32_t w = (uint32_t)(rc.z - rc.x);
+            if (tmask_r) {
+                const unsigned long long msk = staged ? s_msk[j] : tmask_r[r_lo + j];
+                if (msk != ~0ull) q = nth_set64(msk, q);   // q-th kept tile of the rect
+            }
             // q / w through a float reciprocal (q < 2^24), corrected to the exact quotient
             uint32_t qy = (uint32_t)((float)q * __frcp_rn((float)w));
             if (qy * w > q) qy--;
@@ -558,7 +577,8 @@ static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint
     return 3;
 }
 
-int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &) {
+int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &,
+                   bool tight) {
     Counters *cnt = ws.counters;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -576,7 +596,8 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
                                ws.sv[(p + 1) & 1], CNT_VISIBLE, mk, 8 * p);
     // 3. pair offsets in depth order
     launches += scan_pass(ws, st, grid_n,
-                          OffsetsOp{ws.sv[0], ws.touched, ws.rect, ws.off, ws.rect_r, ws.chunk_first, cnt, mk},
+                          OffsetsOp{ws.sv[0], ws.touched, ws.rect, tight ? ws.tmask : nullptr, ws.off, ws.rect_r,
+                                    ws.tmask_r, ws.chunk_first, cnt, mk},
                           (uint32_t)N);
     // 4. tile sort with the expansion fused into the first pass; final order in kt[0]/kv[0]
     int tbits = 0;
@@ -590,8 +611,9 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
             xattr = true;
         }
         const int e = tpasses & 1;   // the passes alternate buffers and end in kt[0]/kv[0]
-        k_expand<<<grid_k, SORT_THREADS, xs, st>>>(Expander{ws.off, ws.sv[0], ws.chunk_first, ws.rect_r, cnt, gx}, mk,
-                                                   ws.kt[e], ws.kv[e]);
+        k_expand<<<grid_k, SORT_THREADS, xs, st>>>(
+            Expander{ws.off, ws.sv[0], ws.chunk_first, ws.rect_r, tight ? ws.tmask_r : nullptr, cnt, gx}, mk,
+            ws.kt[e], ws.kv[e]);
         launches++;
         for (int p = 0; p < tpasses; p++) {
             const int src = (e + p) & 1;

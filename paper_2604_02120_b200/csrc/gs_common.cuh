@@ -33,12 +33,14 @@ struct Workspace {
     float4 *conic_o;           // [N] (A, B, C, opacity)
     float4 *rgb;               // [N] (r, g, b, 0)
     ushort4 *rect;             // [N] (xmin, ymin, xmax, ymax) tiles, half-open
-    uint32_t *touched;         // [N] tiles touched (0 = culled)
+    uint32_t *touched;         // [N] tiles touched (0 = culled); with GS_FLAG_TIGHT: tiles kept
+    unsigned long long *tmask; // [N] GS_FLAG_TIGHT: kept tiles of the rect (bit ty*w+tx), ~0 = all
     int32_t *radius;           // [N] pixel radius (debug output)
     uint32_t *sk[2];           // [N] depth keys of the visible Gaussians, ping-pong
     uint32_t *sv[2];           // [N] their indices; sv[0] = depth order after the sort
     uint32_t *off;             // [N] first pair of each depth-ordered Gaussian
     ushort4 *rect_r;           // [N] rect of each depth-ordered Gaussian
+    unsigned long long *tmask_r;   // [N] its tile mask (GS_FLAG_TIGHT)
     // per key (max_keys)
     uint32_t *kt[2];           // [K] tile ids, ping-pong; kt[0] final
     uint32_t *kv[2];           // [K] Gaussian indices, ping-pong; kv[0] final
@@ -204,9 +206,9 @@ constexpr float ALPHA_MAX = 0.99f; // alpha cap (R-4)
 namespace gs {
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H);
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
-                   uint32_t &epoch);
+                   uint32_t &epoch, bool tight);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,

@@ -90,12 +90,13 @@ void enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const 
                    const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
     mark(c, st, o, 0);
     cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
+    const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                          o.scale_modifier, cam, W, H);
+                          o.scale_modifier, cam, W, H, tight);
     c->launches += N > 0 ? 1 : 0;
     mark(c, st, o, 1);
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
-    c->launches += gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch);
+    c->launches += gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch, tight);
     mark(c, st, o, 2);
 }
 
@@ -227,7 +228,7 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
     A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
-    A(w.radius, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
+    A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
     A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
     A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 256); A(w.row_total, 256);
     A(w.counters, 1);
@@ -246,7 +247,7 @@ int gs_ctx_destroy(gs_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     gs::Workspace &w = c->ws;
-    void *ptrs[] = {w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+    void *ptrs[] = {w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
                     w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
                     w.ranges, w.sums, w.cmat, w.row_total, w.counters, w.stage, c->frame_rgb, c->frame_T};
     for (void *p : ptrs)
@@ -376,7 +377,7 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     gs::launch_preprocess(c->ws, st, N, means3D, scales, rots, opacity, shs, o->sh_degree, o->sh_stride,
-                          o->scale_modifier, *cam, W, H);
+                          o->scale_modifier, *cam, W, H, (o->flags & GS_FLAG_TIGHT) != 0);
     if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
     return finish(c, st, *o, N);
 }

@@ -21,17 +21,65 @@ __device__ __forceinline__ int rect_bound(float v, int g) {
 
 constexpr int PRE_THREADS = 256;
 
-// Two dependent memory round trips per Gaussian: (means, rotation, scales,
-// opacity) together, then -- only for projected Gaussians -- the SH row.
-// Every output is written for every Gaussian (zeros when culled) so that
-// all stores are full sectors.
+// Tile-exact intersection (GS_FLAG_TIGHT). A pixel p can keep the Gaussian only if
+// ln(o) - q/2 >= ln(1/255) - margin (Eq. 3 power, q = d^T Q d, d = p - mu up to sign),
+// i.e. p - mu lies in the ellipse E = {d : d^T Q d <= lim}, lim = 2 (ln(255 o) + margin),
+// margin 5e-3 in ln(alpha) (25x the documented exponent error delta_a). With
+// Sigma = Q^-1 = (a, b; b, c) the dilated 2-D covariance:
+//   - E's bounding box is |dx| <= sqrt(lim a), |dy| <= sqrt(lim c): the rect shrinks to it;
+//   - E cut by a band of pixel rows v in [v0, v1] spans dx in [L, R] with
+//     R = max_v (-B v + sqrt(A lim - det_Q v^2)) / A, a concave function whose
+//     maximiser is v* = b sqrt(lim / a); L is its mirror image (v -> -v).
+// Each row of tiles therefore keeps a contiguous run of columns; for boxes of <= 64
+// tiles bit (ty-y0)*w + (tx-x0) of the mask marks the kept tiles. The column test
+// uses the half-open [16 tx, 16 tx + 16) so it is a superset of the exact pixel set.
+// Not part of the bit-exact set: explicit FMAs / approximate reciprocals are fine.
+__device__ __forceinline__ bool tight_rect(float mx, float my, float A, float B, float a, float b, float c, float op,
+                                           int gx, int gy, int &xmin, int &ymin, int &xmax, int &ymax,
+                                           unsigned long long &mask, uint32_t &count) {
+    const float lim = 2.0f * (__logf(255.0f * op) + 5e-3f);
+    if (!(lim > 0.f)) return false;
+    const float ex = __fsqrt_rn(lim * a), ey = __fsqrt_rn(lim * c);
+    xmin = max(xmin, (int)fminf((float)gx, fmaxf(0.0f, floorf((mx - ex) * 0.0625f))));
+    xmax = min(xmax, (int)fminf((float)gx, fmaxf(0.0f, floorf((mx + ex) * 0.0625f) + 1.0f)));
+    ymin = max(ymin, (int)fminf((float)gy, fmaxf(0.0f, floorf((my - ey) * 0.0625f))));
+    ymax = min(ymax, (int)fminf((float)gy, fmaxf(0.0f, floorf((my + ey) * 0.0625f) + 1.0f)));
+    const int w = xmax - xmin, h = ymax - ymin;
+    if (w <= 0 || h <= 0) return false;
+    if (w == 1 || h == 1 || w * h > 64) {   // a 1-wide box is covered by convexity; > 64 keeps all
+        mask = w * h >= 64 ? ~0ull : (1ull << (w * h)) - 1ull;
+        count = (uint32_t)(w * h);
+        return true;
+    }
+    const float iA = __frcp_rn(A), detQ = __frcp_rn(a * c - b * b);
+    const float vstar = b * __fsqrt_rn(lim * __frcp_rn(a));
+    unsigned long long m = 0ull;
+    uint32_t n = 0;
+    for (int r = 0; r < h; r++) {
+        const float by0 = (float)(GS_TILE * (ymin + r));
+        const float v0 = fmaxf(by0 - my, -ey), v1 = fminf(by0 + 15.0f - my, ey);
+        if (v0 > v1) continue;
+        const float vr = fminf(fmaxf(vstar, v0), v1), vl = fminf(fmaxf(-vstar, v0), v1);
+        const float R = (-B * vr + __fsqrt_rn(fmaxf(A * lim - detQ * vr * vr, 0.f))) * iA;
+        const float L = (-B * vl - __fsqrt_rn(fmaxf(A * lim - detQ * vl * vl, 0.f))) * iA;
+        const int c0 = max(xmin, (int)floorf((mx + L) * 0.0625f)) - xmin;
+        const int c1 = min(xmax - 1, (int)floorf((mx + R) * 0.0625f)) - xmin;
+        if (c0 > c1) continue;
+        m |= (((1ull << (c1 - c0 + 1)) - 1ull) << c0) << (r * w);
+        n += (uint32_t)(c1 - c0 + 1);
+    }
+    mask = m;
+    count = n;
+    return n != 0;
+}
+
 __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
                                                                const float4 *__restrict__ rots,
                                                                const float *__restrict__ opacity,
                                                                const float *__restrict__ shs, int sh_degree,
                                                                int sh_stride, float scale_mod, int W, int H,
-                                                               const gs_camera cam, Workspace ws) {
+                                                               const gs_camera cam, Workspace ws, bool tight) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const float *R = cam.R;
@@ -43,7 +91,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const floa
     const float op = __ldcs(opacity + i);
 
     bool vis = false;
-    float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f;
+    float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f;
     int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
     // 1. view-space point
     const float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam.t[0];
@@ -107,6 +155,7 @@ __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const floa
         const float det = a * c - b * b;
         if (det > 0.0f) {
             cA = c / det; cB = -(b / det); cC = a / det;
+            sxx = a; sxy = b; syy = c;
             // 8. radius
             const float mid = 0.5f * (a + c);
             const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
@@ -122,6 +171,12 @@ __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const floa
             ymax = rect_bound(((my + rf) + 15.0f) / 16.0f, gy);
             vis = (xmax - xmin) * (ymax - ymin) != 0;
         }
+    }
+    uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
+    if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
+        unsigned long long m = 0ull;
+        vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, m, n_tiles);
+        ws.tmask[i] = m;
     }
     if (!vis) {
         ws.depth_bits[i] = 0u;
@@ -199,17 +254,17 @@ __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const floa
     ws.rgb[i] = make_float4(col0, col1, col2, 0.f);
     ws.rect[i] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
                               (unsigned short)ymax);
-    ws.touched[i] = (uint32_t)((xmax - xmin) * (ymax - ymin));
+    ws.touched[i] = n_tiles;
     ws.radius[i] = r;
 }
 
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H) {
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight) {
     if (N <= 0) return;
     k_preprocess<<<ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st>>>(
         N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
-        H, cam, ws);
+        H, cam, ws, tight);
 }
 
 }  // namespace gs

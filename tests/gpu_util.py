@@ -30,7 +30,7 @@ def gpu_preprocess(ctx, scene, cam, st=None):
     return out
 
 
-def gpu_binning(ctx, scene, cam, capacity=None, st=None):
+def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0):
     import torch
     st = st or scene_to_device(scene)
     cap = capacity or (1 << 22)
@@ -38,21 +38,21 @@ def gpu_binning(ctx, scene, cam, capacity=None, st=None):
     vals = torch.empty(cap, dtype=torch.int32, device="cuda")
     ntiles = ((cam.W + 15) // 16) * ((cam.H + 15) // 16)
     ranges = torch.empty((ntiles, 2), dtype=torch.int32, device="cuda")
-    code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree), keys, vals,
-                                   ranges)
+    code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree, flags=flags), keys,
+                                   vals, ranges)
     if code != 0:
         return code, K, None
     return code, K, dict(keys=keys[:K].cpu().numpy().view(np.uint64), vals=vals[:K].cpu().numpy().view(np.uint32),
                          ranges=ranges.cpu().numpy().view(np.uint32))
 
 
-def gpu_render(ctx, scene, cam, bg, blend=0, st=None):
+def gpu_render(ctx, scene, cam, bg, blend=0, st=None, flags=0):
     import torch
     st = st or scene_to_device(scene)
     out_rgb = torch.full((3, cam.H, cam.W), float("nan"), device="cuda")
     out_T = torch.full((cam.H, cam.W), float("nan"), device="cuda")
-    ctx.gs_render(st, camera(cam), cam.W, cam.H, opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=1),
-                  out_rgb, out_T)
+    ctx.gs_render(st, camera(cam), cam.W, cam.H,
+                  opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=1 | flags), out_rgb, out_T)
     torch.cuda.synchronize()
     return out_rgb.cpu().numpy().astype(np.float64), out_T.cpu().numpy().astype(np.float64)
 

@@ -260,3 +260,52 @@ def test_full_size_c5_view_sampled_parity():
     assert err[:, ok].max() <= MAX_ABS
     mse = float((err ** 2).mean())
     assert 10 * np.log10(1 / max(mse, 1e-30)) >= MIN_PSNR
+
+
+# ---------------------------------------------------------------------------
+# N3: tile-exact intersection (GS_FLAG_TIGHT)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("case", list(CASES))
+def test_tight_intersection_renders_bit_identical(case):
+    """Dropped pairs are alpha-skipped anyway and every exponent is independent of
+    the batch it lands in, so the frame is bit-identical to the vanilla-rect one."""
+    from paper_2604_02120_b200 import GS_FLAG_TIGHT
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    a, ta = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC)
+    b, tb = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=GS_FLAG_TIGHT)
+    assert np.array_equal(a, b) and np.array_equal(ta, tb)
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "adversarial"])
+def test_tight_binning_is_an_alpha_exact_subset(case):
+    """Tight lists = the vanilla lists minus pairs whose alpha < 1/255 on every
+    pixel of the tile (checked by brute force in float64 against the oracle's
+    splats); the per-tile order is the vanilla order."""
+    from paper_2604_02120_b200 import GS_FLAG_TIGHT
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    code, K, tb = gpu_binning(ctx, scene, cam, flags=GS_FLAG_TIGHT)
+    assert code == 0
+    pre = oracle.preprocess(scene, cam)
+    ref = oracle.binning(pre, cam.W, cam.H)
+    assert 0 < K < ref["K"]
+    gx = (cam.W + 15) // 16
+    rng = np.random.default_rng(0)
+    tiles = np.nonzero(ref["ranges"][:, 1] > ref["ranges"][:, 0])[0]
+    for t in rng.choice(tiles, min(60, len(tiles)), replace=False):
+        v_all = ref["vals"][ref["ranges"][t, 0]:ref["ranges"][t, 1]]
+        v_t = tb["vals"][tb["ranges"][t, 0]:tb["ranges"][t, 1]] if tb["ranges"][t, 1] > tb["ranges"][t, 0] else []
+        kept = set(int(v) for v in v_t)
+        assert [int(v) for v in v_all if int(v) in kept] == [int(v) for v in v_t]    # order preserved
+        tx, ty = t % gx, t // gx
+        yy, xx = np.mgrid[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16]
+        inside = (xx < cam.W) & (yy < cam.H)
+        for i in v_all:
+            if int(i) in kept:
+                continue
+            dx = float(pre["xy"][i, 0]) - xx[inside]
+            dy = float(pre["xy"][i, 1]) - yy[inside]
+            A, B, C = (float(c) for c in pre["conic"][i])
+            a = float(pre["opacity"][i]) * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
+            assert a.max() < 1.0 / 255.0, (t, i, a.max())
