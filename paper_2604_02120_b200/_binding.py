@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsrender.so")
+# GS_RENDER_LIB: an alternative build of this same library (tuning sweeps, tools/sweep_blend.py)
+LIB_PATH = os.environ.get("GS_RENDER_LIB") or os.path.join(_HERE, "libgsrender.so")
 
 GS_OK = 0
 GS_ERR_INVALID_ARG = -1

@@ -41,17 +41,26 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // each warp owns a contiguous range, so warp-local ranking in round order is stable.
 __device__ __forceinline__ int elem_of(int w, int r, int lane) { return w * (SORT_ITEMS * 32) + r * 32 + lane; }
 
-// Warp multisplit on an 8-bit digit: mask of the lanes holding the same digit.
-// 8 ballots: 0.46 ns/element/SM on sm_100a with distinct digits, vs 1.0 for
-// match.any (tools/microbench_rank.cu); counting alone uses shared atomics
-// (0.04 ns/element/SM).
+// Warp multisplit on a DBITS-bit digit: mask of the lanes holding the same digit.
+// Ballots: 0.46 ns/element/SM on sm_100a for 8 bits with distinct digits, vs 1.0
+// for match.any (tools/microbench_rank.cu); counting alone uses shared atomics
+// (0.04 ns/element/SM). Each bit is 4 SASS instructions (LOP3->P, VOTE, predicated
+// NOT, AND); the plain C++ form compiled to 7. Only the digit's significant bits
+// are voted on, so the last, narrow pass of a sort costs proportionally less.
+template <int DBITS>
 __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
     if (!valid) peers = ~peers;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
-        const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? m : ~m;
+    for (int b = 0; b < DBITS; b++) {
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %1, %2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+            "@!p not.b32 t, t;\n\t"
+            "and.b32 %0, %0, t;\n\t}"
+            : "+r"(peers)
+            : "r"(d), "r"(1u << b));
     }
     return peers;
 }
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int w
 
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
 // earlier chunks) + (rank among this chunk's elements of the digit)
-template <class Loader>
+template <class Loader, int DBITS>
 __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint32_t *__restrict__ kout,
                                                              uint32_t *__restrict__ vout, const Counters *cnt,
                                                              int which, uint64_t max_keys, int shift,
@@ -480,7 +489,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
             const int e = elem_of(warp, r, lane);
             const bool valid = (uint32_t)e < cvalid;
             const uint32_t d = valid ? ((s_k[e] >> shift) & 255u) : 0u;
-            const uint32_t peers = peers_of(d, valid);
+            const uint32_t peers = peers_of<DBITS>(d, valid);
             uint32_t before = 0;
             if (valid) before = s_whist[warp][d];
             __syncwarp();
@@ -552,20 +561,38 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ til
 }
 
 // ---------------------------------------------------------------------------
-template <class Loader>
-static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout, uint32_t *vout,
-                      int which, uint64_t mk, int shift) {
+template <class Loader, int DBITS>
+static void launch_scatter(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout,
+                           uint32_t *vout, int which, uint64_t mk, int shift) {
     const size_t ldm = ws.max_chunks;
     const size_t sc_smem = (4 * SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t);
     static bool attrs = false;
     if (!attrs) {
-        cudaFuncSetAttribute(k_rs_scatter<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
+        cudaFuncSetAttribute(k_rs_scatter<Loader, DBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
         attrs = true;
     }
+    k_rs_scatter<Loader, DBITS><<<grid, SORT_THREADS, sc_smem, st>>>(ld, kout, vout, ws.counters, which, mk, shift,
+                                                                     ws.cmat, (uint32_t)ldm, ws.row_total);
+}
+
+// One stable LSD pass on bits [shift, shift + dbits) (dbits <= 8; higher key bits
+// must already be zero above shift + dbits or belong to later passes).
+template <class Loader>
+static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout, uint32_t *vout,
+                      int which, uint64_t mk, int shift, int dbits = 8) {
+    const size_t ldm = ws.max_chunks;
     k_rs_count<Loader><<<grid, SORT_THREADS, 0, st>>>(ld, ws.counters, which, mk, shift, ws.cmat, (uint32_t)ldm);
     k_rs_scanrows<<<256, 1024, 0, st>>>(ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
-    k_rs_scatter<Loader><<<grid, SORT_THREADS, sc_smem, st>>>(ld, kout, vout, ws.counters, which, mk, shift,
-                                                              ws.cmat, (uint32_t)ldm, ws.row_total);
+    switch (dbits) {
+    case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 2: launch_scatter<Loader, 2>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 3: launch_scatter<Loader, 3>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 4: launch_scatter<Loader, 4>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 5: launch_scatter<Loader, 5>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 6: launch_scatter<Loader, 6>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 7: launch_scatter<Loader, 7>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    default: launch_scatter<Loader, 8>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    }
     return 3;
 }
 
@@ -602,7 +629,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     // 4. tile sort with the expansion fused into the first pass; final order in kt[0]/kv[0]
     int tbits = 0;
     while ((1 << tbits) < ntiles) tbits++;
-    const int tpasses = tbits <= 8 ? 1 : 2;
+    const int tpasses = std::max(1, (tbits + 7) / 8);
     {
         const size_t xs = Expander::SCRATCH_WORDS * sizeof(uint32_t);
         static bool xattr = false;
@@ -618,7 +645,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         for (int p = 0; p < tpasses; p++) {
             const int src = (e + p) & 1;
             launches += radix_pass(ws, st, grid_k, PlainLoader{ws.kt[src], ws.kv[src]}, ws.kt[src ^ 1],
-                                   ws.kv[src ^ 1], CNT_KEYS, mk, 8 * p);
+                                   ws.kv[src ^ 1], CNT_KEYS, mk, 8 * p, std::min(8, std::max(1, tbits - 8 * p)));
         }
     }
     // 5. tile ranges

@@ -27,17 +27,34 @@
 
 namespace gs {
 
-constexpr int NB = 32;        // Gaussians per batch (MMA N)
-constexpr int STAGES = 4;     // M_g / TMEM ring depth
-constexpr int NCW = 8;        // compositor warps: 256 pixels
-constexpr int NBLD = 2;       // builder warps (alternate batches)
-constexpr int RAW = 4;        // raw-record ring (producer -> builders): gathers in flight
-constexpr int PF = 4;         // index lookahead of the producer (batches)
+// Pipeline shape; overridable with -D for tuning sweeps (tools/sweep_blend.py).
+#ifndef GS_BLEND_STAGES
+#define GS_BLEND_STAGES 2
+#endif
+#ifndef GS_BLEND_NBLD
+#define GS_BLEND_NBLD 2
+#endif
+#ifndef GS_BLEND_RAW
+#define GS_BLEND_RAW 4
+#endif
+#ifndef GS_BLEND_PF
+#define GS_BLEND_PF 4
+#endif
+#ifndef GS_BLEND_MINB
+#define GS_BLEND_MINB 3      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
+#endif
+constexpr int NB = 32;                  // Gaussians per batch (MMA N)
+constexpr int STAGES = GS_BLEND_STAGES; // M_g / TMEM ring depth
+constexpr int NCW = 8;                  // compositor warps: 256 pixels
+constexpr int NBLD = GS_BLEND_NBLD;     // builder warps (alternate batches)
+constexpr int RAW = GS_BLEND_RAW;       // raw-record ring (producer -> builders): gathers in flight
+constexpr int PF = GS_BLEND_PF;         // index lookahead of the producer (batches)
 constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
 constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_MMA = NCW + 1 + NBLD;
 constexpr int TC_THREADS = (NCW + 2 + NBLD) * 32;
 constexpr int TMEM_COLS = STAGES * 2 * NB;   // 256
-static_assert(TMEM_COLS == 256, "TMEM allocation must be a power of two");
+static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0 && GS_BLEND_MINB * TMEM_COLS <= 512,
+              "TMEM allocation must be a power of two >= 32 and fit MINB CTAs per SM");
 // Batch b of a CTA's stream (data batch, end-of-tile marker or terminal)
 //   raw slot b % RAW  (producer -> builder b % NBLD),
 //   M_g/TMEM stage b % STAGES (builder -> MMA warp -> compositors),
@@ -163,7 +180,7 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
     } while (0)
 
 template <bool DUMP, bool STATS, bool TRACE>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+__global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W,
                int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
@@ -478,7 +495,7 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
         cudaFuncSetAttribute(k_blend_tc<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    const int grid = std::max(1, std::min(2 * num_sms, ntiles));
+    const int grid = std::max(1, std::min(GS_BLEND_MINB * num_sms, ntiles));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
 #define ARGS xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk

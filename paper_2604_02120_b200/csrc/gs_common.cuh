@@ -92,14 +92,27 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t cnt) {
 // Waits for the phase with the given parity. The suspend-time hint lets a
 // waiting warp sleep in hardware until the phase completes instead of
 // spinning (spinning warps took a third of the blend's issue slots).
+#ifndef GS_MBAR_SUSPEND_NS
+#define GS_MBAR_SUSPEND_NS 0x100000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if GS_MBAR_SUSPEND_NS > 0
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x100000u)
+        "r"(parity), "r"((uint32_t)GS_MBAR_SUSPEND_NS)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 // tcgen05 / TMEM
