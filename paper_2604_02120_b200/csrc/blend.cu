@@ -2,23 +2,29 @@
 // exponent of GEMM-GS (Eq. 6-8; Alg. 2), and
 // the CUDA-core direct form (Alg. 1) as an A/B baseline.
 //
-// k_blend_tc: persistent, warp-specialised tcgen05 kernel, 2 CTAs per SM.
-//   warp 8 (producer + MMA issuer): per batch of NB = 32 Gaussians of a tile's
-//     sorted list, lane j gathers Gaussian j (mean, conic, opacity, colour),
-//     builds v_g (Eq. 6) scaled by log2(e) with log2(o) folded into
-//     the constant term (reading R-10), splits it into TF32 hi + lo (reading
-//     R-11) and writes the row [hi(6) | lo(6) | 0(4)] of M_g into shared memory;
-//     one lane then issues 4 x tcgen05.mma.kind::tf32 (M=128 pixels, N=32,
-//     K=8; 2 pixel halves x 2 K-steps) that multiply the constant pixel matrix
-//     M_p (rows [v_p | v_p | 0], precomputed once per CTA, the
-//     "offline" M_p of P:302) by M_g^T into TMEM, and commits to an mbarrier.
-//   warps 0-7 (compositors, one pixel per thread): tcgen05.ld 32x32b.x32 gives
-//     each thread its own pixel's 32 exponents m = log2(alpha); then alpha =
-//     min(0.99, 2^m), alpha-skip below 1/255, T' = T(1-alpha), stop when
+// k_blend_tc: persistent, warp-specialised tcgen05 kernel, 4 CTAs per SM
+// (10 warps, <= 51 registers, 128 TMEM columns each: 4 x 128 = the SM's 512).
+//   warp 8 (producer): per batch of NB = 32 Gaussians of a tile's sorted list,
+//     lane j gathers Gaussian j (mean, conic+opacity, colour) with cp.async into
+//     a raw-record ring RAW batches deep; tiles come from an atomic work queue.
+//   warp 9 (builder + MMA issuer): builds v_g (Eq. 6) scaled by
+//     log2(e) with log2(o) folded into the constant term (reading R-10), splits
+//     it into TF32 hi + lo (reading R-11), writes the row [hi(6) | lo(6) | 0(4)]
+//     of M_g into shared memory, then one lane issues 4 x tcgen05.mma.kind::tf32
+//     (M=128 pixels, N=32, K=8; 2 pixel halves x 2 K-steps) that multiply the
+//     constant pixel matrix M_p (rows [v_p | v_p | 0], built once per
+//     CTA: the "offline" M_p of P:302) by M_g^T into TMEM, committing to an
+//     mbarrier. The TMEM ring is STAGES = 2 batches deep.
+//   warps 0-7 (compositors, one pixel per thread): tcgen05.ld 32x32b.x16 gives
+//     each thread its own pixel's exponents m = log2(alpha), 16 at a time; then
+//     alpha = min(0.99, 2^m), alpha-skip below 1/255, T' = T(1-alpha), stop when
 //     T' < 1e-4 (not composited), C += alpha T c (Eq. 1; readings R-1..R-4).
 //     A warp skips a Gaussian with one vote when none of its 32 pixels keeps it.
-//   A tile ends when its list is exhausted or all 256 pixels have terminated;
-//   tiles come from an atomic work queue.
+//   The compositor loop is a serial dependency chain per pixel, so the kernel is
+//   latency-bound: occupancy (CTAs per SM) is what sets its speed, and the pipe-
+//   line shape (one helper warp each for gathers and rows+MMA, 2 TMEM stages,
+//   16-column loads) is the one that fits 4 CTAs per SM (blend).
+//   A tile ends when its list is exhausted or all 256 pixels have terminated.
 // Reference pixel p_c = tile centre (16 t_x + 7.5, 16 t_y + 7.5) (reading R-6),
 // x_bar = x_c - x_p (Eq. 4; reading R-7).
 #include <algorithm>
@@ -32,7 +38,7 @@ namespace gs {
 #define GS_BLEND_STAGES 2
 #endif
 #ifndef GS_BLEND_NBLD
-#define GS_BLEND_NBLD 2
+#define GS_BLEND_NBLD 1
 #endif
 #ifndef GS_BLEND_RAW
 #define GS_BLEND_RAW 4
@@ -41,17 +47,24 @@ namespace gs {
 #define GS_BLEND_PF 4
 #endif
 #ifndef GS_BLEND_MINB
-#define GS_BLEND_MINB 3      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
+#define GS_BLEND_MINB 4      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
+#endif
+#ifndef GS_BLEND_CH
+#define GS_BLEND_CH 16
 #endif
 constexpr int NB = 32;                  // Gaussians per batch (MMA N)
+constexpr int CH = GS_BLEND_CH;         // TMEM columns per compositor load (16 or 32)
 constexpr int STAGES = GS_BLEND_STAGES; // M_g / TMEM ring depth
 constexpr int NCW = 8;                  // compositor warps: 256 pixels
 constexpr int NBLD = GS_BLEND_NBLD;     // builder warps (alternate batches)
 constexpr int RAW = GS_BLEND_RAW;       // raw-record ring (producer -> builders): gathers in flight
 constexpr int PF = GS_BLEND_PF;         // index lookahead of the producer (batches)
 constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
-constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_MMA = NCW + 1 + NBLD;
-constexpr int TC_THREADS = (NCW + 2 + NBLD) * 32;
+// warp roles: 0..NCW-1 compositors, NCW producer, NCW+1.. builders (each also issues
+// the MMAs of the batches it built, and builder 0 owns the TMEM allocation)
+constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_TMEM = NCW + 1;
+constexpr int TC_THREADS = (NCW + 1 + NBLD) * 32;
+static_assert(STAGES % NBLD == 0, "all batches of a TMEM stage must come from one builder");
 constexpr int TMEM_COLS = STAGES * 2 * NB;   // 256
 static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0 && GS_BLEND_MINB * TMEM_COLS <= 512,
               "TMEM allocation must be a power of two >= 32 and fit MINB CTAs per SM");
@@ -80,7 +93,6 @@ struct __align__(1024) SmemTC {
     int4 raw_hdr[RAW];
     uint64_t full[STAGES];        // MMA done (commit), or marker -> compositors
     uint64_t empty[STAGES];       // compositors released the TMEM stage -> MMA warp
-    uint64_t rows_ready[STAGES];  // M_g rows built -> MMA warp
     uint64_t slot_ready[RING];    // colours/header written -> compositors
     uint64_t raw_full[RAW];       // producer -> builder
     uint64_t raw_empty[RAW];      // builder -> producer
@@ -111,6 +123,9 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
+
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[32]) { tmem_ld32(taddr, v); }
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[16]) { tmem_ld16(taddr, v); }
 
 struct Rec {
     float2 m;     // projected mean
@@ -195,7 +210,6 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], NCW);
-            mbar_init(&sm.rows_ready[s], 1);
         }
         for (int r = 0; r < RING; r++) mbar_init(&sm.slot_ready[r], 1);
         for (int r = 0; r < RAW; r++) {
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         for (int c = 0; c < 4; c++) st_shared_v4(base + op_off(r, c), u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
         if (lane == 0) sm.warp_done_seq[warp] = 0;
         fence_proxy_async_smem();
-    } else if (warp == WARP_MMA) {
+    } else if (warp == WARP_TMEM) {
         tmem_alloc(&sm.tmem_base, TMEM_COLS);
         tmem_relinquish();
     }
@@ -331,7 +345,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             TRACE_EV(2, kb);
             int4 hd = sm.raw_hdr[r];
             // stage s / slot are reusable once batch kb-STAGES went through the MMA warp
-            // (for every batch kind: this also keeps the rows_ready / slot_ready phases in step)
+            // (for every batch kind: this also keeps the slot_ready phases in step)
             if (kb >= STAGES) mbar_wait(&sm.full[s], ((kb / STAGES) - 1) & 1u);
             TRACE_EV(3, kb);
             if (hd.z > 0) {
@@ -346,48 +360,32 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             if (lane == 0) {
                 mbar_arrive(&sm.raw_empty[r]);
                 mbar_arrive(&sm.slot_ready[slot]);
-                mbar_arrive(&sm.rows_ready[s]);
             }
             TRACE_EV(4, kb);
+            {
+                const uint32_t ph = (kb / STAGES) & 1u;
+                mbar_wait(&sm.empty[s], ph ^ 1u);   // batch kb - STAGES no longer read from TMEM
+                if (hd.z > 0) {
+                    tc_fence_after();
+                    if (lane == 0) {
+                        constexpr uint32_t IDESC = idesc_tf32(128, NB);
+                        const uint32_t a_base = smem_u32(&sm.A[0][0]);
+                        const uint32_t b_base = smem_u32(&sm.B[s][0]);
+#pragma unroll
+                        for (int kk = 0; kk < 2; kk++)
+#pragma unroll
+                            for (int h = 0; h < 2; h++)
+                                mma_tf32(tmem + s * (2 * NB) + h * NB,
+                                         umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512),
+                                         umma_desc(b_base + kk * 256, 128, 512), IDESC, kk);
+                        mma_commit(&sm.full[s]);
+                    }
+                } else if (lane == 0) {
+                    mbar_arrive(&sm.full[s]);   // marker / skipped batch: no MMA
+                }
+                __syncwarp();
+            }
             if (hd.x < 0) break;
-        }
-    } else if (warp == WARP_MMA) {
-        // =================== MMA issuer ===================
-        constexpr uint32_t IDESC = idesc_tf32(128, NB);
-        const uint32_t a_base = smem_u32(&sm.A[0][0]);
-        const uint32_t b_base = smem_u32(&sm.B[0][0]);
-        uint64_t adesc[2][2];   // [K-step][pixel half]; B descriptors differ only by the stage offset
-#pragma unroll
-        for (int kk = 0; kk < 2; kk++)
-#pragma unroll
-            for (int h = 0; h < 2; h++) adesc[kk][h] = umma_desc(a_base + h * (128 * 64) + kk * 256, 128, 512);
-        const uint64_t bdesc0 = umma_desc(b_base, 128, 512), bdesc1 = umma_desc(b_base + 256, 128, 512);
-        for (uint32_t k = 0;; k++) {
-            const int s = k % STAGES;
-            const uint32_t ph = (k / STAGES) & 1u;
-            mbar_wait(&sm.rows_ready[s], ph);
-            TRACE_EV(5, k);
-            const int4 hd = sm.hdr[k % RING];
-            if (hd.z <= 0) {                    // marker or skipped batch: no MMA
-                mbar_wait(&sm.empty[s], ph ^ 1u);
-                if (lane == 0) mbar_arrive(&sm.full[s]);
-                if (hd.x < 0) break;
-                continue;
-            }
-            mbar_wait(&sm.empty[s], ph ^ 1u);   // batch k-STAGES no longer read from TMEM
-            TRACE_EV(6, k);
-            tc_fence_after();
-            if (lane == 0) {
-                const uint64_t soff = (uint64_t)((s * (NB * 64)) >> 4);   // start-address field, 16 B units
-#pragma unroll
-                for (int kk = 0; kk < 2; kk++)
-#pragma unroll
-                    for (int h = 0; h < 2; h++)
-                        mma_tf32(tmem + s * (2 * NB) + h * NB, adesc[kk][h], (kk ? bdesc1 : bdesc0) + soff, IDESC,
-                                 kk);
-                mma_commit(&sm.full[s]);
-            }
-            __syncwarp();
         }
     } else {
         // =================== compositors ===================
@@ -432,33 +430,41 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 }
                 T = 1.0f; C0 = C1 = C2 = 0.f; thr = LOG2_ALPHA_MIN; wdone = false;
             } else if (hd.z > 0 && !wdone) {
-                float m[NB];
-                tmem_ld32(tmem + t_lane + s * (2 * NB) + t_half, m);
-                tmem_wait_ld();
                 const int cnt = hd.z;
-                if (DUMP) {
-                    for (int j = 0; j < cnt; j++) dump_m[((size_t)hd.w + j) * GS_TILE_PIX + p] = m[j];
-                } else {
-                    // columns j >= cnt hold the padding exponent -1e30: no count checks needed
-                    const uint32_t crow = smem_u32(&sm.rgb[c_slot][0]);
+                const uint32_t crow = smem_u32(&sm.rgb[c_slot][0]);
+                // exponents come out of TMEM CH columns at a time (CH = 16 keeps the
+                // register count low enough for 4 CTAs per SM)
 #pragma unroll
-                    for (int j = 0; j < NB; j++) {
-                        const float mj = m[j];
-                        const bool live = mj >= thr;                    // alpha >= 1/255 (R-1), pixel running
-                        if (__any_sync(0xffffffffu, live)) {            // warp-uniform skip
-                            const float4 c = ld_shared_f4(crow + 16 * j);
-                            const float a = fminf(ALPHA_MAX, ex2_approx(mj));   // alpha = 2^m capped (R-4)
-                            const float tT = fmaf(-a, T, T);                    // T (1 - alpha)
-                            const float w = a * T;
-                            const bool acc = live && tT >= T_MIN;               // composite (Eq. 1, R-3)
-                            if (STATS) n_kept += live ? 1u : 0u;
-                            C0 = acc ? fmaf(w, c.x, C0) : C0;
-                            C1 = acc ? fmaf(w, c.y, C1) : C1;
-                            C2 = acc ? fmaf(w, c.z, C2) : C2;
-                            T = acc ? tT : T;
-                            thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;   // stop (R-2)
+                for (int h0 = 0; h0 < NB; h0 += CH) {
+                    float m[CH];
+                    tmem_ld_cols(tmem + t_lane + s * (2 * NB) + t_half + h0, m);
+                    tmem_wait_ld();
+                    if (DUMP) {
+                        for (int j = 0; j < CH && h0 + j < cnt; j++)
+                            dump_m[((size_t)hd.w + h0 + j) * GS_TILE_PIX + p] = m[j];
+                    } else {
+                        // columns j >= cnt hold the padding exponent -1e30: no count checks needed
+#pragma unroll
+                        for (int j = 0; j < CH; j++) {
+                            const float mj = m[j];
+                            const bool live = mj >= thr;                    // alpha >= 1/255 (R-1), pixel running
+                            if (__any_sync(0xffffffffu, live)) {            // warp-uniform skip
+                                const float4 c = ld_shared_f4(crow + 16 * (h0 + j));
+                                const float a = fminf(ALPHA_MAX, ex2_approx(mj));   // alpha = 2^m capped (R-4)
+                                const float tT = fmaf(-a, T, T);                    // T (1 - alpha)
+                                const float w = a * T;
+                                const bool acc = live && tT >= T_MIN;               // composite (Eq. 1, R-3)
+                                if (STATS) n_kept += live ? 1u : 0u;
+                                C0 = acc ? fmaf(w, c.x, C0) : C0;
+                                C1 = acc ? fmaf(w, c.y, C1) : C1;
+                                C2 = acc ? fmaf(w, c.z, C2) : C2;
+                                T = acc ? tT : T;
+                                thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;   // stop (R-2)
+                            }
                         }
                     }
+                }
+                if (!DUMP) {
                     if (__all_sync(0xffffffffu, thr > 0.f)) {
                         wdone = true;
                         if (lane == 0) *((volatile uint32_t *)&sm.warp_done_seq[warp]) = (uint32_t)hd.y;
@@ -474,7 +480,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == WARP_MMA) {
+    if (warp == WARP_TMEM) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
