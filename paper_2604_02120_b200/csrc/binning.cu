@@ -68,10 +68,11 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
 // ---------------------------------------------------------------------------
 // element counts (device-resident)
 // ---------------------------------------------------------------------------
-enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2 };
+enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2, CNT_RENT = 3 };
 __device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint32_t n_points, uint64_t max_keys) {
     if (which == CNT_POINTS) return n_points;
     if (which == CNT_VISIBLE) return c->n_visible;
+    if (which == CNT_RENT) return c->err ? 0u : c->n_rent;   // > max_keys sets err
     const uint64_t k = c->n_keys;
     return c->err ? 0u : (uint32_t)(k < max_keys ? k : max_keys);
 }
@@ -239,11 +240,24 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // ---------------------------------------------------------------------------
 // loaders: a chunk's keys (and values) into shared memory
 // ---------------------------------------------------------------------------
-struct PlainLoader {
+// Chunking of a radix pass: linear 4096-element chunks over n elements; the digit
+// bases come from the digit totals (s_dbase). Loaders derive from this unless they
+// define their own chunks (ColLoader).
+struct LinearChunks {
+    static constexpr bool EXPANDS = false;   // keys via key(i) from global memory
+    __device__ uint32_t nchunks(uint32_t n) const { return (n + SORT_CHUNK - 1) / SORT_CHUNK; }
+    __device__ void chunk(uint32_t c, uint32_t n, uint32_t &cbase, uint32_t &cvalid) const {
+        cbase = c * SORT_CHUNK;
+        cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+    }
+    __device__ uint32_t digit_base(uint32_t, uint32_t d, const uint32_t *s_dbase) const { return s_dbase[d]; }
+};
+
+struct PlainLoader : LinearChunks {
     const uint32_t *keys, *vals;
     static constexpr int SCRATCH_WORDS = 0;
     __device__ uint32_t key(uint32_t i) const { return __ldcs(keys + i); }
-    __device__ void load(uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
+    __device__ void load(uint32_t, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
         uint32_t k[SORT_ITEMS], v[SORT_ITEMS];   // all loads in flight before the first use
 #pragma unroll
         for (int q = 0; q < SORT_ITEMS; q++) {
@@ -377,20 +391,32 @@ template <class Loader>
 __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Counters *cnt, int which,
                                                            uint64_t max_keys, int shift, uint32_t *cmat,
                                                            uint32_t ldm) {
+    extern __shared__ uint32_t dyn[];   // expanding loaders: the chunk's keys + loader scratch
     constexpr int NH = 4;   // privatised histograms (warp % NH)
     __shared__ uint32_t s_h[NH][256];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
-    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const uint32_t nchunks = ld.nchunks(n);
     const int warp = threadIdx.x >> 5;
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint32_t cbase = c * SORT_CHUNK, cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+        uint32_t cbase, cvalid;
+        ld.chunk(c, n, cbase, cvalid);
 #pragma unroll
         for (int h = 0; h < NH; h++) s_h[h][threadIdx.x] = 0;
         uint32_t k[SORT_ITEMS];
+        if constexpr (Loader::EXPANDS) {
+            ld.load(c, cbase, cvalid, dyn, nullptr, dyn + SORT_CHUNK);
+            __syncthreads();
 #pragma unroll
-        for (int q = 0; q < SORT_ITEMS; q++) {
-            const uint32_t e = threadIdx.x + q * SORT_THREADS;
-            k[q] = e < cvalid ? ld.key(cbase + e) : 0u;
+            for (int q = 0; q < SORT_ITEMS; q++) {
+                const uint32_t e = threadIdx.x + q * SORT_THREADS;
+                k[q] = e < cvalid ? dyn[e] : 0u;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < SORT_ITEMS; q++) {
+                const uint32_t e = threadIdx.x + q * SORT_THREADS;
+                k[q] = e < cvalid ? ld.key(cbase + e) : 0u;
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -453,11 +479,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
     extern __shared__ uint32_t dyn[];
     uint32_t *s_k = dyn, *s_v = dyn + SORT_CHUNK;                                   // loaded chunk
     uint32_t *s_ok = dyn + 2 * SORT_CHUNK, *s_ov = dyn + 3 * SORT_CHUNK;            // digit-ordered chunk
-    uint32_t *s_scr = dyn + 4 * SORT_CHUNK;                                         // loader scratch
+    // loader scratch: expanding loaders are done with it before s_ok is written
+    uint32_t *s_scr = Loader::EXPANDS ? s_ok : dyn + 4 * SORT_CHUNK;
     __shared__ uint16_t s_whist[NWARP][256];
     __shared__ uint32_t s_dbase[256], s_blk[256], s_base[256], s_tot[NWARP];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
-    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
+    const uint32_t nchunks = ld.nchunks(n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int d_own = threadIdx.x;
     auto block_excl_scan = [&](uint32_t v) -> uint32_t {   // over the 256 threads (one value each)
@@ -476,11 +503,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
     };
     s_dbase[d_own] = block_excl_scan(row_total[d_own]);
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint32_t cbase = c * SORT_CHUNK, cvalid = min((uint32_t)SORT_CHUNK, n - cbase);
+        uint32_t cbase, cvalid;
+        ld.chunk(c, n, cbase, cvalid);
 #pragma unroll
         for (int w = 0; w < NWARP; w++) s_whist[w][d_own] = 0;
-        s_base[d_own] = s_dbase[d_own] + cmat[(size_t)d_own * ldm + c];
-        ld.load(cbase, cvalid, s_k, s_v, s_scr);
+        s_base[d_own] = ld.digit_base(c, d_own, s_dbase) + cmat[(size_t)d_own * ldm + c];
+        ld.load(c, cbase, cvalid, s_k, s_v, s_scr);
         __syncthreads();
         // warp-local stable ranks
         uint32_t rank[SORT_ITEMS];
@@ -525,7 +553,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
             const uint32_t k = s_ok[p];
             const uint32_t d = (k >> shift) & 255u;
             const uint32_t g = s_base[d] + (p - s_blk[d]);
-            kout[g] = k;
+            if (kout) kout[g] = k;
             vout[g] = s_ov[p];
         }
         __syncthreads();
@@ -561,11 +589,399 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ til
 }
 
 // ---------------------------------------------------------------------------
+// Two-level binning (tile grids up to 256 x 256): the stable sort by tile of the
+// depth-ordered pairs is done MSD-style without materialising the K tile keys.
+//   rows:    each depth-ordered Gaussian r contributes one entry per tile row it
+//            keeps; one stable 8-bit pass on the row ty puts the entries in
+//            (ty, depth) order (values r, keys ty).
+//   columns: an entry of row ty holds a contiguous run of tile columns (the rect's
+//            columns, or the kept run of a GS_FLAG_TIGHT row). Its pairs are
+//            enumerated run by run, in row-aligned 4096-pair chunks, and one stable
+//            pass on the column tx, segmented by row, writes each Gaussian index
+//            straight to its final slot. Tile ranges follow from the column counts.
+// The result is the same (tile, depth, index) order as a full stable sort.
+// ---------------------------------------------------------------------------
+
+// kept tile rows of a rect (bit ry of the result; rows without a kept tile are
+// skipped); the full-rect case is all h rows
+__device__ __forceinline__ uint32_t kept_rows(const ushort4 &rc, unsigned long long m) {
+    const uint32_t w = rc.z - rc.x, h = rc.w - rc.y;
+    if (m == ~0ull || w * h > 64u || h > 32u) return h >= 32u ? 0xFFFFFFFFu : ((1u << h) - 1u);
+    const unsigned long long wmask = (w >= 64u) ? ~0ull : ((1ull << w) - 1ull);
+    uint32_t rows = 0;
+    for (uint32_t ry = 0; ry < h; ry++)
+        if ((m >> (ry * w)) & wmask) rows |= 1u << ry;
+    return rows;
+}
+
+struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry offsets (+ rects/masks in depth order)
+    const uint32_t *sorted_idx;
+    const ushort4 *rect;
+    const unsigned long long *tmask;   // GS_FLAG_TIGHT (nullptr: whole rects)
+    uint32_t *roff, *rowmask_r;
+    ushort4 *rect_r;
+    unsigned long long *tmask_r;
+    uint32_t *chunk_first;
+    Counters *cnt;
+    uint64_t max_keys;
+    static constexpr int WHICH = CNT_VISIBLE;
+    struct Aux {
+        ushort4 rc;
+        unsigned long long m;
+        uint32_t rows;
+    };
+    __device__ uint32_t nrows(const ushort4 &rc, unsigned long long m, uint32_t &rows) const {
+        if (!tmask) {
+            rows = 0xFFFFFFFFu;
+            return (uint32_t)(rc.w - rc.y);
+        }
+        rows = kept_rows(rc, m);
+        return (uint32_t)(rc.w - rc.y) > 32u ? (uint32_t)(rc.w - rc.y) : (uint32_t)__popc(rows);
+    }
+    __device__ uint32_t load(uint32_t r) const {
+        const uint32_t i = sorted_idx[r];
+        uint32_t rows;
+        return nrows(rect[i], tmask ? tmask[i] : ~0ull, rows);
+    }
+    __device__ uint32_t load(uint32_t r, Aux &a) const {
+        const uint32_t i = sorted_idx[r];
+        a.rc = rect[i];
+        a.m = tmask ? tmask[i] : ~0ull;
+        return nrows(a.rc, a.m, a.rows);
+    }
+    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &a) const {
+        roff[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
+        rect_r[r] = a.rc;
+        if (tmask) {
+            tmask_r[r] = a.m;
+            rowmask_r[r] = a.rows;
+        }
+        for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
+            if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
+    }
+    __device__ void finish(uint64_t total) const {
+        cnt->n_rent = (uint32_t)(total < 0xFFFFFFFFull ? total : 0xFFFFFFFFull);
+        if (total > max_keys) atomicOr(&cnt->err, 1u);
+    }
+};
+
+// Warp-cooperative run expansion. Lane L holds a run of len_L >= 1 consecutive
+// output slots (lanes with len 0 only after the last run); the runs are laid out
+// back to back from slot 0. Each round maps 32 slots to their runs with one OR-
+// reduction of the run heads, so the work is balanced whatever the run lengths.
+// emit(valid, owner, j, t): slot t is element j of the run of lane `owner`
+// (every lane calls it, so it may shuffle the owner's data).
+template <class F>
+__device__ __forceinline__ void warp_expand(uint32_t len, F &&emit) {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t pre = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= (uint32_t)o) pre += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+    pre -= len;   // exclusive
+    int carry = -1;   // run of the slot before this round
+    for (uint32_t g = 0; g < total; g += 32) {
+        const uint32_t head = (len && pre >= g && pre < g + 32u) ? (1u << (pre - g)) : 0u;
+        const uint32_t heads = __reduce_or_sync(0xffffffffu, head);
+        const int owner = min(31, carry + __popc(heads & (0xFFFFFFFFu >> (31u - lane))));
+        carry += __popc(heads);
+        const uint32_t t = g + lane;
+        const uint32_t opre = __shfl_sync(0xffffffffu, pre, owner);
+        emit(t < total, owner, t - opre, t);
+    }
+}
+
+// Row entries cbase .. cbase+cvalid-1: entry e belongs to the depth-ordered Gaussian r
+// with roff[r] <= e < roff[r+1] and is r's (e - roff[r])-th kept tile row ty. Its key
+// packs the row and the row's run of kept tile columns: ty | x0 << 8 | width << 16
+// (a GS_FLAG_TIGHT row keeps one contiguous run of columns); value = Gaussian index.
+struct RowLoader : LinearChunks {
+    const uint32_t *roff, *chunk_first, *rowmask_r, *sorted_idx;   // rowmask_r: GS_FLAG_TIGHT only
+    const ushort4 *rect_r;
+    const unsigned long long *tmask_r;                              // GS_FLAG_TIGHT only
+    const Counters *cnt;
+    bool tight;
+    static constexpr bool EXPANDS = true;
+    static constexpr int SCRATCH_WORDS = 0;
+    __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
+        const uint32_t nv = cnt->n_visible;
+        const uint32_t nchunks = (cnt->n_rent + SORT_CHUNK - 1) / SORT_CHUNK;
+        const uint32_t r_lo = chunk_first[c];
+        const uint32_t r_hi = c + 1 < nchunks ? min(nv - 1, chunk_first[c + 1]) : nv - 1;
+        const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+        const uint32_t cend = cbase + cvalid;
+        for (uint32_t g0 = r_lo + 32u * warp; g0 <= r_hi; g0 += 32u * NWARP) {
+            const uint32_t r = g0 + lane;
+            uint32_t len = 0, q0 = 0, slot0 = 0, rxy = 0, rzw = 0, rows = 0xFFFFFFFFu, idx = 0;
+            unsigned long long m = ~0ull;
+            if (r <= r_hi) {
+                const uint32_t o = roff[r];
+                const uint32_t o1 = r + 1 < nv ? roff[r + 1] : (uint32_t)cnt->n_rent;
+                const ushort4 rc = rect_r[r];
+                rxy = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
+                rzw = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+                idx = sorted_idx[r];
+                if (tight) {
+                    rows = rowmask_r[r];
+                    m = tmask_r[r];
+                }
+                q0 = o < cbase ? cbase - o : 0u;
+                len = min(o1, cend) - (o + q0);
+                slot0 = o + q0 - cbase;
+            }
+            const uint32_t wslot = __shfl_sync(0xffffffffu, slot0, 0);
+            warp_expand(len, [&](bool valid, int owner, uint32_t j, uint32_t t) {
+                const uint32_t oq0 = __shfl_sync(0xffffffffu, q0, owner);
+                const uint32_t oxy = __shfl_sync(0xffffffffu, rxy, owner);
+                const uint32_t ozw = __shfl_sync(0xffffffffu, rzw, owner);
+                const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
+                uint32_t orows = 0xFFFFFFFFu;
+                unsigned long long om = ~0ull;
+                if (tight) {
+                    orows = __shfl_sync(0xffffffffu, rows, owner);
+                    om = ((unsigned long long)__shfl_sync(0xffffffffu, (uint32_t)(m >> 32), owner) << 32) |
+                         __shfl_sync(0xffffffffu, (uint32_t)m, owner);
+                }
+                if (!valid) return;
+                const uint32_t x0r = oxy & 0xFFFFu, y0 = oxy >> 16, w = (ozw & 0xFFFFu) - x0r, h = (ozw >> 16) - y0;
+                uint32_t q = oq0 + j;                                                   // q-th kept row
+                if (orows != 0xFFFFFFFFu) q = __fns(orows, 0, (int)q + 1);
+                uint32_t x0 = x0r, wr = w;
+                if (om != ~0ull && w * h <= 64u) {   // the kept run of this row
+                    const uint32_t bits = (uint32_t)((om >> (q * w)) & ((1ull << w) - 1ull));
+                    x0 = x0r + (uint32_t)(__ffs(bits) - 1);
+                    wr = (uint32_t)__popc(bits);
+                }
+                sk[wslot + t] = (y0 + q) | (x0 << 8) | (wr << 16);
+                if (sv) sv[wslot + t] = oidx;
+            });
+        }
+    }
+};
+
+struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (run widths from the packed keys)
+    const uint32_t *e_key;
+    uint32_t *poff;
+    Counters *cnt;
+    uint64_t max_keys;
+    static constexpr int WHICH = CNT_RENT;
+    struct Aux {};
+    __device__ uint32_t load(uint32_t e) const { return e_key[e] >> 16; }
+    __device__ uint32_t load(uint32_t e, Aux &) const { return e_key[e] >> 16; }
+    __device__ void emit(uint32_t e, uint64_t o, uint32_t, const Aux &) const {
+        poff[e] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
+    }
+    __device__ void finish(uint64_t total) const {
+        cnt->n_keys = total;
+        if (total > max_keys) atomicOr(&cnt->err, 1u);
+    }
+};
+
+// Pairs of one row-aligned chunk (cdesc): pair p belongs to the entry e with
+// poff[e] <= p < poff[e+1] and is column x0 + (p - poff[e]) of its run. key = tile
+// column tx, value = Gaussian index; digit bases are the tile starts (ranges[.].x).
+struct ColLoader {
+    const uint32_t *poff, *e_key, *e_idx, *cdesc_last;
+    const uint4 *cdesc;
+    const uint2 *ranges;
+    const Counters *cnt;
+    int gx;
+    static constexpr bool EXPANDS = true;
+    static constexpr int SCRATCH_WORDS = 0;
+    __device__ uint32_t nchunks(uint32_t) const { return cnt->err ? 0u : cnt->n_cchunks; }
+    __device__ void chunk(uint32_t c, uint32_t, uint32_t &cbase, uint32_t &cvalid) const {
+        const uint4 d = cdesc[c];
+        cbase = d.y;
+        cvalid = d.z;
+    }
+    __device__ uint32_t digit_base(uint32_t c, uint32_t d, const uint32_t *) const {
+        return d < (uint32_t)gx ? ranges[cdesc[c].x * (uint32_t)gx + d].x : 0u;
+    }
+    __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
+        const uint32_t e_lo = cdesc[c].w, e_hi = cdesc_last[c];
+        const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+        const uint32_t cend = cbase + cvalid;
+        for (uint32_t g0 = e_lo + 32u * warp; g0 <= e_hi; g0 += 32u * NWARP) {
+            const uint32_t e = g0 + lane;
+            uint32_t len = 0, x = 0, idx = 0, slot0 = 0;
+            if (e <= e_hi) {
+                const uint32_t o = poff[e], k = e_key[e];
+                idx = e_idx[e];
+                const uint32_t q0 = o < cbase ? cbase - o : 0u;
+                len = min(o + (k >> 16), cend) - (o + q0);
+                x = ((k >> 8) & 0xFFu) + q0;
+                slot0 = o + q0 - cbase;
+            }
+            const uint32_t wslot = __shfl_sync(0xffffffffu, slot0, 0);
+            warp_expand(len, [&](bool valid, int owner, uint32_t j, uint32_t t) {
+                const uint32_t ox = __shfl_sync(0xffffffffu, x, owner);
+                const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
+                if (!valid) return;
+                sk[wslot + t] = ox + j;
+                if (sv) sv[wslot + t] = oidx;
+            });
+        }
+    }
+};
+
+// Capacity error path: when the row entries alone overflowed max_keys, the pair
+// offsets were not computed; K (= sum of tiles touched) is still reported.
+__global__ void __launch_bounds__(256) k_keys_on_overflow(const uint32_t *__restrict__ sorted_idx,
+                                                          const uint32_t *__restrict__ touched, Counters *cnt) {
+    if (!cnt->err || cnt->n_keys != 0) return;
+    const uint32_t nv = cnt->n_visible;
+    unsigned long long acc = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nv; r += gridDim.x * blockDim.x)
+        acc += touched[sorted_idx[r]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)&cnt->n_keys, acc);
+}
+
+// one block: per tile row, first entry / first pair / first column chunk; chunk count
+__global__ void __launch_bounds__(256) k_row_bounds(const uint32_t *__restrict__ rows_per_ty,
+                                                    const uint32_t *__restrict__ poff, Counters *cnt, int gy,
+                                                    uint64_t max_keys, uint32_t *rowinfo) {
+    __shared__ uint32_t s_w[NWARP];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    auto excl = [&](uint32_t v) -> uint32_t {
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        uint32_t b = 0;
+        for (int w = 0; w < warp; w++) b += s_w[w];
+        __syncthreads();
+        return b + x - v;
+    };
+    const bool ok = cnt->err == 0u;
+    const uint32_t R = ok ? cnt->n_rent : 0u;
+    const uint32_t K = ok ? (uint32_t)cnt->n_keys : 0u;
+    const uint32_t ne = (ok && t < gy) ? rows_per_ty[t] : 0u;
+    const uint32_t rs = excl(ne);
+    const uint32_t P = (t <= gy && rs < R) ? poff[rs] : K;
+    // pairs of row t: next row's first pair - P (rows are contiguous in pair order)
+    __shared__ uint32_t s_P[257];
+    s_P[t] = P;
+    if (t == 0) s_P[256] = K;
+    __syncthreads();
+    const uint32_t np = t < gy ? s_P[t + 1] - P : 0u;
+    const uint32_t nch = (np + SORT_CHUNK - 1) / SORT_CHUNK;
+    const uint32_t cb = excl(nch);
+    if (t < gy) {
+        rowinfo[t] = rs;
+        rowinfo[257 + t] = P;
+        rowinfo[2 * 257 + t] = cb;
+    }
+    if (t == gy - 1) {   // sentinels of row gy
+        rowinfo[gy] = R;
+        rowinfo[257 + gy] = K;
+        rowinfo[2 * 257 + gy] = cb + nch;
+        cnt->n_cchunks = cb + nch;
+    }
+}
+
+// column chunk descriptors: (ty, first pair, pairs, first entry) and last entry
+__global__ void __launch_bounds__(256) k_chunk_desc(const uint32_t *__restrict__ rowinfo,
+                                                    const uint32_t *__restrict__ poff, const Counters *cnt, int gy,
+                                                    uint4 *cdesc, uint32_t *cdesc_last) {
+    const uint32_t nch = cnt->err ? 0u : cnt->n_cchunks;
+    const uint32_t *rs = rowinfo, *P = rowinfo + 257, *cb = rowinfo + 2 * 257;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
+        int lo = 0, hi = gy - 1;   // last row with cb[row] <= c
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cb[mid] <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        const uint32_t ty = (uint32_t)lo;
+        const uint32_t pbase = P[ty] + (c - cb[ty]) * SORT_CHUNK;
+        const uint32_t pcount = min((uint32_t)SORT_CHUNK, P[ty + 1] - pbase);
+        auto entry_of = [&](uint32_t p) {   // last entry of row ty with poff <= p
+            uint32_t a = rs[ty], b = rs[ty + 1] - 1;
+            while (a < b) {
+                const uint32_t m = (a + b + 1) >> 1;
+                if (poff[m] <= p) a = m;
+                else b = m - 1;
+            }
+            return a;
+        };
+        cdesc[c] = make_uint4(ty, pbase, pcount, entry_of(pbase));
+        cdesc_last[c] = entry_of(pbase + pcount - 1);
+    }
+}
+
+// per (tile row, column digit): exclusive scan of the digit's counts over the row's
+// chunks (in place in cmat) and the tile's pair count
+__global__ void __launch_bounds__(32) k_col_scan(const uint32_t *__restrict__ rowinfo, const Counters *cnt,
+                                                 uint32_t *cmat, uint32_t ldm, int gx, uint32_t *tile_cnt) {
+    const uint32_t ty = blockIdx.x, d = blockIdx.y, lane = threadIdx.x;
+    const uint32_t *cb = rowinfo + 2 * 257;
+    const uint32_t c0 = cnt->err ? 0u : cb[ty], c1 = cnt->err ? 0u : cb[ty + 1];
+    uint32_t *row = cmat + (size_t)d * ldm;
+    uint32_t carry = 0;
+    for (uint32_t base = c0; base < c1; base += 32) {
+        const uint32_t c = base + lane;
+        const uint32_t v = c < c1 ? row[c] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (c < c1) row[c] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) tile_cnt[ty * (uint32_t)gx + d] = carry;
+}
+
+// per tile row: tile starts = row's first pair + exclusive scan of the tile counts
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ rowinfo,
+                                                     const uint32_t *__restrict__ tile_cnt, int gx, uint2 *ranges) {
+    __shared__ uint32_t s_w[NWARP];
+    const uint32_t ty = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t n = t < (uint32_t)gx ? tile_cnt[ty * gx + t] : 0u;
+    uint32_t x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t b = 0;
+    for (uint32_t w = 0; w < warp; w++) b += s_w[w];
+    const uint32_t start = rowinfo[257 + ty] + b + x - n;
+    if (t < (uint32_t)gx) ranges[ty * gx + t] = n ? make_uint2(start, start + n) : make_uint2(0u, 0u);
+}
+
+// ---------------------------------------------------------------------------
+template <class Loader>
+static void launch_count(const Workspace &ws, cudaStream_t st, int grid, Loader ld, int which, uint64_t mk,
+                         int shift) {
+    const size_t smem = Loader::EXPANDS ? (SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t) : 0;
+    static bool attrs = false;
+    if (!attrs && smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_rs_count<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attrs = true;
+    }
+    k_rs_count<Loader><<<grid, SORT_THREADS, smem, st>>>(ld, ws.counters, which, mk, shift, ws.cmat,
+                                                         (uint32_t)ws.max_chunks);
+}
+
 template <class Loader, int DBITS>
 static void launch_scatter(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout,
                            uint32_t *vout, int which, uint64_t mk, int shift) {
     const size_t ldm = ws.max_chunks;
-    const size_t sc_smem = (4 * SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t);
+    static_assert(!Loader::EXPANDS || Loader::SCRATCH_WORDS <= SORT_CHUNK, "scratch aliases s_ok");
+    const size_t sc_smem = (4 * SORT_CHUNK + (Loader::EXPANDS ? 0 : Loader::SCRATCH_WORDS)) * sizeof(uint32_t);
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(k_rs_scatter<Loader, DBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
@@ -581,7 +997,7 @@ template <class Loader>
 static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout, uint32_t *vout,
                       int which, uint64_t mk, int shift, int dbits = 8) {
     const size_t ldm = ws.max_chunks;
-    k_rs_count<Loader><<<grid, SORT_THREADS, 0, st>>>(ld, ws.counters, which, mk, shift, ws.cmat, (uint32_t)ldm);
+    launch_count(ws, st, grid, ld, which, mk, shift);
     k_rs_scanrows<<<256, 1024, 0, st>>>(ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
     switch (dbits) {
     case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
@@ -613,14 +1029,53 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     const int grid_n = std::max(1, std::min(nsm * 8, ceil_div_i(N, SORT_CHUNK)));
     const int grid_k = std::max(1, std::min(nsm * 8, ceil_div_i(max_keys, SORT_CHUNK)));
     const uint64_t mk = (uint64_t)max_keys;
+    const int gy = ntiles / gx;
     cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
     int launches = 0;
     // 1. compaction of the visible Gaussians (index order)
     launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[0], ws.sv[0], cnt}, (uint32_t)N);
     // 2. depth sort: 4 stable passes of 8 bits; the result is back in sk[0]/sv[0]
     for (int p = 0; p < 4; p++)
-        launches += radix_pass(ws, st, grid_n, PlainLoader{ws.sk[p & 1], ws.sv[p & 1]}, ws.sk[(p + 1) & 1],
+        launches += radix_pass(ws, st, grid_n, PlainLoader{{}, ws.sk[p & 1], ws.sv[p & 1]}, ws.sk[(p + 1) & 1],
                                ws.sv[(p + 1) & 1], CNT_VISIBLE, mk, 8 * p);
+    int tbx = 0, tby = 0;
+    while ((1 << tbx) < gx) tbx++;
+    while ((1 << tby) < gy) tby++;
+    if (gx <= 256 && gy <= 256) {
+        // 3. row entries of the depth-ordered Gaussians
+        uint32_t *roff = ws.off, *rowmask_r = ws.sk[1];
+        launches += scan_pass(ws, st, grid_n,
+                              RowOffsetsOp{ws.sv[0], ws.rect, tight ? ws.tmask : nullptr, roff, rowmask_r, ws.rect_r,
+                                           ws.tmask_r, ws.chunk_first, cnt, mk},
+                              (uint32_t)N);
+        // 4. rows: one stable pass on ty -> entries (ty | x0 << 8 | width << 16, index) in kt[1] / kv[1]
+        launches += radix_pass(ws, st, grid_k,
+                               RowLoader{{}, roff, ws.chunk_first, rowmask_r, ws.sv[0], ws.rect_r, ws.tmask_r, cnt,
+                                         tight},
+                               ws.kt[1], ws.kv[1], CNT_RENT, mk, 0, std::max(1, tby));
+        // 5. pair offsets of the entries (kt[0])
+        launches += scan_pass(ws, st, grid_k, PairOffsetsOp{ws.kt[1], ws.kt[0], cnt, mk}, (uint32_t)N);
+        k_keys_on_overflow<<<nsm, 256, 0, st>>>(ws.sv[0], ws.touched, cnt);
+        // 6. row bounds and row-aligned column chunks
+        k_row_bounds<<<1, 256, 0, st>>>(ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
+        k_chunk_desc<<<nsm * 2, 256, 0, st>>>(ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
+        // 7. columns: counts, per-(row, column) scans, tile ranges, stable scatter of the indices
+        const ColLoader col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
+        launch_count(ws, st, grid_k, col, CNT_KEYS, mk, 0);
+        k_col_scan<<<dim3(gy, gx), 32, 0, st>>>(ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx, ws.tile_cnt);
+        k_tile_ranges<<<gy, 256, 0, st>>>(ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
+        switch (std::max(1, tbx)) {
+        case 1: launch_scatter<ColLoader, 1>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 2: launch_scatter<ColLoader, 2>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 3: launch_scatter<ColLoader, 3>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 4: launch_scatter<ColLoader, 4>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 5: launch_scatter<ColLoader, 5>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 6: launch_scatter<ColLoader, 6>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        case 7: launch_scatter<ColLoader, 7>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        default: launch_scatter<ColLoader, 8>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        }
+        return launches + 8;
+    }
     // 3. pair offsets in depth order
     launches += scan_pass(ws, st, grid_n,
                           OffsetsOp{ws.sv[0], ws.touched, ws.rect, tight ? ws.tmask : nullptr, ws.off, ws.rect_r,
@@ -644,7 +1099,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         launches++;
         for (int p = 0; p < tpasses; p++) {
             const int src = (e + p) & 1;
-            launches += radix_pass(ws, st, grid_k, PlainLoader{ws.kt[src], ws.kv[src]}, ws.kt[src ^ 1],
+            launches += radix_pass(ws, st, grid_k, PlainLoader{{}, ws.kt[src], ws.kv[src]}, ws.kt[src ^ 1],
                                    ws.kv[src ^ 1], CNT_KEYS, mk, 8 * p, std::min(8, std::max(1, tbits - 8 * p)));
         }
     }

@@ -18,7 +18,9 @@ struct Counters {
     uint32_t err;              // device-side error bits (1 = key capacity)
     uint64_t n_keys;           // K (64-bit: the capacity check is exact)
     uint32_t tile_queue;       // blend persistent work queue
-    uint32_t pad[3];
+    uint32_t n_rent;           // row entries (two-level binning): kept tile rows summed over Gaussians
+    uint32_t n_cchunks;        // column-pass chunks (row-aligned, <= 4096 pairs each)
+    uint32_t pad;
     unsigned long long pairs_eval;   // GS_FLAG_STATS: exponents computed by the blend
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
@@ -47,6 +49,11 @@ struct Workspace {
     uint32_t *chunk_first;     // [K/4096+1] Gaussian holding the first pair of each chunk
     // per tile
     uint2 *ranges;             // [tiles] [start, end) into kv[0]
+    // two-level binning (tile rows, then columns)
+    uint4 *cdesc;              // [max_chunks] column chunk: (tile row, first pair, pairs, first entry)
+    uint32_t *cdesc_last;      // [max_chunks] last row entry of the chunk
+    uint32_t *tile_cnt;        // [tiles] pairs per tile
+    uint32_t *rowinfo;         // [3][257] per tile row: first entry, first pair, first column chunk
     // reduce-then-scan scratch (4096-element chunks)
     uint32_t *sums;            // [max_chunks] chunk sums of the order-preserving scans
     uint32_t *cmat;            // [256][max_chunks] per-chunk digit counts -> offsets
