@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // bases come from the digit totals (s_dbase). Loaders derive from this unless they
 // define their own chunks (ColLoader).
 struct LinearChunks {
-    static constexpr bool EXPANDS = false;   // keys via key(i) from global memory
+    static constexpr bool EXPANDS = false;      // keys via key(i) from global memory
+    static constexpr bool RUN_COUNTS = false;   // digit counts from runs (count_runs)
     __device__ uint32_t nchunks(uint32_t n) const { return (n + SORT_CHUNK - 1) / SORT_CHUNK; }
     __device__ void chunk(uint32_t c, uint32_t n, uint32_t &cbase, uint32_t &cvalid) const {
         cbase = c * SORT_CHUNK;
@@ -400,6 +401,29 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         uint32_t cbase, cvalid;
         ld.chunk(c, n, cbase, cvalid);
+        if constexpr (Loader::RUN_COUNTS) {
+            int *s_diff = reinterpret_cast<int *>(&s_h[0][0]);   // 257 entries
+            s_diff[threadIdx.x] = 0;
+            if (threadIdx.x == 0) s_diff[256] = 0;
+            __syncthreads();
+            ld.count_runs(c, cbase, cvalid, s_diff);
+            __syncthreads();
+            // inclusive scan of the difference array = the digit counts
+            __shared__ uint32_t s_w[NWARP];
+            const int lane = threadIdx.x & 31;
+            uint32_t x = (uint32_t)s_diff[threadIdx.x];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_w[warp] = x;
+            __syncthreads();
+            for (int w = 0; w < warp; w++) x += s_w[w];
+            cmat[(size_t)threadIdx.x * ldm + c] = x;
+            __syncthreads();
+            continue;
+        }
 #pragma unroll
         for (int h = 0; h < NH; h++) s_h[h][threadIdx.x] = 0;
         uint32_t k[SORT_ITEMS];
@@ -625,11 +649,7 @@ struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry off
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
-    struct Aux {
-        ushort4 rc;
-        unsigned long long m;
-        uint32_t rows;
-    };
+    struct Aux {};   // emit re-gathers (L1-hot): nothing is held across the scan, for occupancy
     __device__ uint32_t nrows(const ushort4 &rc, unsigned long long m, uint32_t &rows) const {
         if (!tmask) {
             rows = 0xFFFFFFFFu;
@@ -643,18 +663,18 @@ struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry off
         uint32_t rows;
         return nrows(rect[i], tmask ? tmask[i] : ~0ull, rows);
     }
-    __device__ uint32_t load(uint32_t r, Aux &a) const {
+    __device__ uint32_t load(uint32_t r, Aux &) const { return load(r); }
+    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &) const {
         const uint32_t i = sorted_idx[r];
-        a.rc = rect[i];
-        a.m = tmask ? tmask[i] : ~0ull;
-        return nrows(a.rc, a.m, a.rows);
-    }
-    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &a) const {
+        const ushort4 rc = rect[i];
         roff[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
-        rect_r[r] = a.rc;
+        rect_r[r] = rc;
         if (tmask) {
-            tmask_r[r] = a.m;
-            rowmask_r[r] = a.rows;
+            const unsigned long long m = tmask[i];
+            uint32_t rows;
+            nrows(rc, m, rows);
+            tmask_r[r] = m;
+            rowmask_r[r] = rows;
         }
         for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
             if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
@@ -705,7 +725,9 @@ struct RowLoader : LinearChunks {
     const Counters *cnt;
     bool tight;
     static constexpr bool EXPANDS = true;
+    static constexpr bool RUN_COUNTS = true;   // k_rs_count uses count_runs (no expansion)
     static constexpr int SCRATCH_WORDS = 0;
+    __device__ void count_runs(uint32_t c, uint32_t cbase, uint32_t cvalid, int *s_diff) const;
     __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
         const uint32_t nv = cnt->n_visible;
         const uint32_t nchunks = (cnt->n_rent + SORT_CHUNK - 1) / SORT_CHUNK;
@@ -713,21 +735,35 @@ struct RowLoader : LinearChunks {
         const uint32_t r_hi = c + 1 < nchunks ? min(nv - 1, chunk_first[c + 1]) : nv - 1;
         const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
         const uint32_t cend = cbase + cvalid;
+        const uint32_t n_rent = cnt->n_rent;
+        // the next group's Gaussians are fetched while this group expands (latency hiding)
+        uint32_t n_o = 0, n_o1 = 0, n_idx = 0, n_rows = 0xFFFFFFFFu;
+        ushort4 n_rc = make_ushort4(0, 0, 0, 0);
+        unsigned long long n_m = ~0ull;
+        auto fetch = [&](uint32_t g) {
+            const uint32_t r = g + lane;
+            if (r <= r_hi) {
+                n_o = roff[r];
+                n_o1 = r + 1 < nv ? roff[r + 1] : n_rent;
+                n_rc = rect_r[r];
+                n_idx = sorted_idx[r];
+                if (tight) {
+                    n_rows = rowmask_r[r];
+                    n_m = tmask_r[r];
+                }
+            }
+        };
+        fetch(r_lo + 32u * warp);
         for (uint32_t g0 = r_lo + 32u * warp; g0 <= r_hi; g0 += 32u * NWARP) {
             const uint32_t r = g0 + lane;
-            uint32_t len = 0, q0 = 0, slot0 = 0, rxy = 0, rzw = 0, rows = 0xFFFFFFFFu, idx = 0;
-            unsigned long long m = ~0ull;
+            const uint32_t o = n_o, o1 = n_o1, idx = n_idx, rows = n_rows;
+            const ushort4 rc = n_rc;
+            const unsigned long long m = n_m;
+            if (g0 + 32u * NWARP <= r_hi) fetch(g0 + 32u * NWARP);
+            uint32_t len = 0, q0 = 0, slot0 = 0, rxy = 0, rzw = 0;
             if (r <= r_hi) {
-                const uint32_t o = roff[r];
-                const uint32_t o1 = r + 1 < nv ? roff[r + 1] : (uint32_t)cnt->n_rent;
-                const ushort4 rc = rect_r[r];
                 rxy = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
                 rzw = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
-                idx = sorted_idx[r];
-                if (tight) {
-                    rows = rowmask_r[r];
-                    m = tmask_r[r];
-                }
                 q0 = o < cbase ? cbase - o : 0u;
                 len = min(o1, cend) - (o + q0);
                 slot0 = o + q0 - cbase;
@@ -761,6 +797,40 @@ struct RowLoader : LinearChunks {
         }
     }
 };
+
+// Digit counts of a chunk without expanding it: each Gaussian's rows in the chunk
+// window are a run of consecutive digits (kept rows of a GS_FLAG_TIGHT box are
+// counted one by one), added to the difference array s_diff[257].
+__device__ __forceinline__ void row_count_runs(const RowLoader &ld, uint32_t c, uint32_t cbase, uint32_t cvalid,
+                                               int *s_diff) {
+    const uint32_t nv = ld.cnt->n_visible, n_rent = ld.cnt->n_rent;
+    const uint32_t nchunks = (n_rent + SORT_CHUNK - 1) / SORT_CHUNK;
+    const uint32_t r_lo = ld.chunk_first[c];
+    const uint32_t r_hi = c + 1 < nchunks ? min(nv - 1, ld.chunk_first[c + 1]) : nv - 1;
+    const uint32_t cend = cbase + cvalid;
+    for (uint32_t r = r_lo + threadIdx.x; r <= r_hi; r += SORT_THREADS) {
+        const uint32_t o = ld.roff[r], o1 = r + 1 < nv ? ld.roff[r + 1] : n_rent;
+        const uint32_t q0 = o < cbase ? cbase - o : 0u;
+        const uint32_t len = min(o1, cend) - (o + q0);
+        if (len == 0) continue;
+        const uint32_t y0 = ld.rect_r[r].y;
+        const uint32_t rows = ld.tight ? ld.rowmask_r[r] : 0xFFFFFFFFu;
+        if (rows == 0xFFFFFFFFu) {
+            atomicAdd(&s_diff[y0 + q0], 1);
+            atomicAdd(&s_diff[y0 + q0 + len], -1);
+        } else {
+            for (uint32_t q = q0; q < q0 + len; q++) {
+                const uint32_t ty = y0 + (uint32_t)__fns(rows, 0, (int)q + 1);
+                atomicAdd(&s_diff[ty], 1);
+                atomicAdd(&s_diff[ty + 1], -1);
+            }
+        }
+    }
+}
+
+__device__ void RowLoader::count_runs(uint32_t c, uint32_t cbase, uint32_t cvalid, int *s_diff) const {
+    row_count_runs(*this, c, cbase, cvalid, s_diff);
+}
 
 struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (run widths from the packed keys)
     const uint32_t *e_key;
@@ -800,16 +870,39 @@ struct ColLoader {
     __device__ uint32_t digit_base(uint32_t c, uint32_t d, const uint32_t *) const {
         return d < (uint32_t)gx ? ranges[cdesc[c].x * (uint32_t)gx + d].x : 0u;
     }
+    static constexpr bool RUN_COUNTS = true;
+    __device__ void count_runs(uint32_t c, uint32_t cbase, uint32_t cvalid, int *s_diff) const {
+        const uint32_t e_lo = cdesc[c].w, e_hi = cdesc_last[c], cend = cbase + cvalid;
+        for (uint32_t e = e_lo + threadIdx.x; e <= e_hi; e += SORT_THREADS) {
+            const uint32_t o = poff[e], k = e_key[e];
+            const uint32_t q0 = o < cbase ? cbase - o : 0u;
+            const uint32_t len = min(o + (k >> 16), cend) - (o + q0);
+            const uint32_t x = ((k >> 8) & 0xFFu) + q0;
+            atomicAdd(&s_diff[x], 1);
+            atomicAdd(&s_diff[x + len], -1);
+        }
+    }
     __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
         const uint32_t e_lo = cdesc[c].w, e_hi = cdesc_last[c];
         const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
         const uint32_t cend = cbase + cvalid;
+        // the next group's entries are fetched while this group expands (latency hiding)
+        uint32_t n_o = 0, n_k = 0, n_i = 0;
+        auto fetch = [&](uint32_t g) {
+            const uint32_t e = g + lane;
+            if (e <= e_hi) {
+                n_o = poff[e];
+                n_k = e_key[e];
+                n_i = e_idx[e];
+            }
+        };
+        fetch(e_lo + 32u * warp);
         for (uint32_t g0 = e_lo + 32u * warp; g0 <= e_hi; g0 += 32u * NWARP) {
             const uint32_t e = g0 + lane;
-            uint32_t len = 0, x = 0, idx = 0, slot0 = 0;
+            const uint32_t o = n_o, k = n_k, idx = n_i;
+            if (g0 + 32u * NWARP <= e_hi) fetch(g0 + 32u * NWARP);
+            uint32_t len = 0, x = 0, slot0 = 0;
             if (e <= e_hi) {
-                const uint32_t o = poff[e], k = e_key[e];
-                idx = e_idx[e];
                 const uint32_t q0 = o < cbase ? cbase - o : 0u;
                 len = min(o + (k >> 16), cend) - (o + q0);
                 x = ((k >> 8) & 0xFFu) + q0;
@@ -966,7 +1059,8 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict_
 template <class Loader>
 static void launch_count(const Workspace &ws, cudaStream_t st, int grid, Loader ld, int which, uint64_t mk,
                          int shift) {
-    const size_t smem = Loader::EXPANDS ? (SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t) : 0;
+    const size_t smem =
+        (Loader::EXPANDS && !Loader::RUN_COUNTS) ? (SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t) : 0;
     static bool attrs = false;
     if (!attrs && smem > 48 * 1024) {
         cudaFuncSetAttribute(k_rs_count<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
