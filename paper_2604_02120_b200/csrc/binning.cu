@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // bases come from the digit totals (s_dbase). Loaders derive from this unless they
 // define their own chunks (ColLoader).
 struct LinearChunks {
+    static constexpr bool PACKED = false;       // key = digit | value << 8, no separate values
     static constexpr bool EXPANDS = false;      // keys via key(i) from global memory
     static constexpr bool RUN_COUNTS = false;   // digit counts from runs (count_runs)
     __device__ uint32_t nchunks(uint32_t n) const { return (n + SORT_CHUNK - 1) / SORT_CHUNK; }
@@ -495,14 +496,17 @@ __global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int w
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
 // earlier chunks) + (rank among this chunk's elements of the digit)
 template <class Loader, int DBITS>
-__global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint32_t *__restrict__ kout,
+__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_scatter(Loader ld, uint32_t *__restrict__ kout,
                                                              uint32_t *__restrict__ vout, const Counters *cnt,
                                                              int which, uint64_t max_keys, int shift,
                                                              const uint32_t *__restrict__ cmat, uint32_t ldm,
                                                              const uint32_t *__restrict__ row_total) {
     extern __shared__ uint32_t dyn[];
-    uint32_t *s_k = dyn, *s_v = dyn + SORT_CHUNK;                                   // loaded chunk
-    uint32_t *s_ok = dyn + 2 * SORT_CHUNK, *s_ov = dyn + 3 * SORT_CHUNK;            // digit-ordered chunk
+    // PACKED loaders carry the value in the key's upper bits (key = digit | value << 8):
+    // one word per element, half the shared memory, more resident blocks
+    constexpr bool PK = Loader::PACKED;
+    uint32_t *s_k = dyn, *s_v = PK ? nullptr : dyn + SORT_CHUNK;                    // loaded chunk
+    uint32_t *s_ok = dyn + (PK ? 1 : 2) * SORT_CHUNK, *s_ov = PK ? nullptr : dyn + 3 * SORT_CHUNK;   // digit order
     // loader scratch: expanding loaders are done with it before s_ok is written
     uint32_t *s_scr = Loader::EXPANDS ? s_ok : dyn + 4 * SORT_CHUNK;
     __shared__ uint16_t s_whist[NWARP][256];
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
                 const uint32_t d = (k >> shift) & 255u;
                 const uint32_t pos = s_blk[d] + s_whist[warp][d] + rank[r];
                 s_ok[pos] = k;
-                s_ov[pos] = s_v[e];
+                if (!PK) s_ov[pos] = s_v[e];
             }
         }
         __syncthreads();
@@ -577,8 +581,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3) k_rs_scatter(Loader ld, uint3
             const uint32_t k = s_ok[p];
             const uint32_t d = (k >> shift) & 255u;
             const uint32_t g = s_base[d] + (p - s_blk[d]);
-            if (kout) kout[g] = k;
-            vout[g] = s_ov[p];
+            if (PK) {
+                vout[g] = k >> 8;
+            } else {
+                if (kout) kout[g] = k;
+                vout[g] = s_ov[p];
+            }
         }
         __syncthreads();
     }
@@ -853,7 +861,9 @@ struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (ru
 // Pairs of one row-aligned chunk (cdesc): pair p belongs to the entry e with
 // poff[e] <= p < poff[e+1] and is column x0 + (p - poff[e]) of its run. key = tile
 // column tx, value = Gaussian index; digit bases are the tile starts (ranges[.].x).
+template <bool PK>
 struct ColLoader {
+    static constexpr bool PACKED = PK;   // Gaussian indices < 2^24: key = tx | index << 8
     const uint32_t *poff, *e_key, *e_idx, *cdesc_last;
     const uint4 *cdesc;
     const uint2 *ranges;
@@ -913,8 +923,12 @@ struct ColLoader {
                 const uint32_t ox = __shfl_sync(0xffffffffu, x, owner);
                 const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
                 if (!valid) return;
-                sk[wslot + t] = ox + j;
-                if (sv) sv[wslot + t] = oidx;
+                if (PK) {
+                    sk[wslot + t] = (ox + j) | (oidx << 8);
+                } else {
+                    sk[wslot + t] = ox + j;
+                    if (sv) sv[wslot + t] = oidx;
+                }
             });
         }
     }
@@ -1075,7 +1089,8 @@ static void launch_scatter(const Workspace &ws, cudaStream_t st, int grid, Loade
                            uint32_t *vout, int which, uint64_t mk, int shift) {
     const size_t ldm = ws.max_chunks;
     static_assert(!Loader::EXPANDS || Loader::SCRATCH_WORDS <= SORT_CHUNK, "scratch aliases s_ok");
-    const size_t sc_smem = (4 * SORT_CHUNK + (Loader::EXPANDS ? 0 : Loader::SCRATCH_WORDS)) * sizeof(uint32_t);
+    const size_t sc_smem =
+        ((Loader::PACKED ? 2 : 4) * SORT_CHUNK + (Loader::EXPANDS ? 0 : Loader::SCRATCH_WORDS)) * sizeof(uint32_t);
     static bool attrs = false;
     if (!attrs) {
         cudaFuncSetAttribute(k_rs_scatter<Loader, DBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
@@ -1112,6 +1127,20 @@ static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint
     k_scan_sums<Op><<<1, 1024, 0, st>>>(op, n_points, ws.sums);
     k_scan_apply<Op><<<grid, SORT_THREADS, 0, st>>>(op, n_points, ws.sums);
     return 3;
+}
+
+template <class L>
+static void col_scatter(const Workspace &ws, cudaStream_t st, int grid, const L &col, int tbx, uint64_t mk) {
+    switch (std::max(1, tbx)) {
+    case 1: launch_scatter<L, 1>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 2: launch_scatter<L, 2>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 3: launch_scatter<L, 3>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 4: launch_scatter<L, 4>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 5: launch_scatter<L, 5>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 6: launch_scatter<L, 6>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 7: launch_scatter<L, 7>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    default: launch_scatter<L, 8>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    }
 }
 
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &,
@@ -1154,19 +1183,15 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         k_row_bounds<<<1, 256, 0, st>>>(ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
         k_chunk_desc<<<nsm * 2, 256, 0, st>>>(ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
         // 7. columns: counts, per-(row, column) scans, tile ranges, stable scatter of the indices
-        const ColLoader col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
+        const ColLoader<false> col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
         launch_count(ws, st, grid_k, col, CNT_KEYS, mk, 0);
         k_col_scan<<<dim3(gy, gx), 32, 0, st>>>(ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx, ws.tile_cnt);
         k_tile_ranges<<<gy, 256, 0, st>>>(ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
-        switch (std::max(1, tbx)) {
-        case 1: launch_scatter<ColLoader, 1>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 2: launch_scatter<ColLoader, 2>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 3: launch_scatter<ColLoader, 3>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 4: launch_scatter<ColLoader, 4>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 5: launch_scatter<ColLoader, 5>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 6: launch_scatter<ColLoader, 6>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        case 7: launch_scatter<ColLoader, 7>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
-        default: launch_scatter<ColLoader, 8>(ws, st, grid_k, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+        if (N < (1 << 24)) {
+            const ColLoader<true> colp{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
+            col_scatter(ws, st, grid_k, colp, tbx, mk);
+        } else {
+            col_scatter(ws, st, grid_k, col, tbx, mk);
         }
         return launches + 8;
     }
