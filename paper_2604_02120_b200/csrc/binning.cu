@@ -140,6 +140,7 @@ struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ gathered
 
 template <class Op>
 __global__ void __launch_bounds__(SORT_THREADS) k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums) {
+    pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_reduce(Op op, uint32_t n_
 // one block: exclusive scan of the chunk sums in place; op.finish(total)
 template <class Op>
 __global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, uint32_t *sums) {
+    pdl_wait();
     __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long s_carry;
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, ui
 
 template <class Op>
 __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
+    pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
@@ -376,6 +379,7 @@ struct Expander {
 // writes the K (tile, index) pairs in depth order: one 4096-pair chunk per iteration
 __global__ void __launch_bounds__(SORT_THREADS) k_expand(Expander ex, uint64_t max_keys, uint32_t *kout,
                                                          uint32_t *vout) {
+    pdl_wait();
     extern __shared__ uint32_t dyn[];
     const uint32_t n = count_of(ex.cnt, CNT_KEYS, 0, max_keys);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
@@ -393,6 +397,7 @@ template <class Loader>
 __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Counters *cnt, int which,
                                                            uint64_t max_keys, int shift, uint32_t *cmat,
                                                            uint32_t ldm) {
+    pdl_wait();
     extern __shared__ uint32_t dyn[];   // expanding loaders: the chunk's keys + loader scratch
     constexpr int NH = 4;   // privatised histograms (warp % NH)
     __shared__ uint32_t s_h[NH][256];
@@ -461,6 +466,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
 // step 2: one block per digit: exclusive scan of its row over the chunks; row totals
 __global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int which, uint64_t max_keys,
                                                       uint32_t *cmat, uint32_t ldm, uint32_t *row_total) {
+    pdl_wait();
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_carry;
     const uint32_t n = count_of(cnt, which, 0, max_keys);
@@ -501,6 +507,7 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
                                                              int which, uint64_t max_keys, int shift,
                                                              const uint32_t *__restrict__ cmat, uint32_t ldm,
                                                              const uint32_t *__restrict__ row_total) {
+    pdl_wait();
     extern __shared__ uint32_t dyn[];
     // PACKED loaders carry the value in the key's upper bits (key = digit | value << 8):
     // one word per element, half the shared memory, more resident blocks
@@ -597,6 +604,7 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tiles, const Counters *cnt,
                                                 uint64_t max_keys, uint2 *ranges) {
+    pdl_wait();
     const uint32_t n = count_of(cnt, CNT_KEYS, 0, max_keys);
     const uint32_t stride = gridDim.x * blockDim.x * 4;
     for (uint32_t k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; k0 < n; k0 += stride) {
@@ -938,6 +946,7 @@ struct ColLoader {
 // offsets were not computed; K (= sum of tiles touched) is still reported.
 __global__ void __launch_bounds__(256) k_keys_on_overflow(const uint32_t *__restrict__ sorted_idx,
                                                           const uint32_t *__restrict__ touched, Counters *cnt) {
+    pdl_wait();
     if (!cnt->err || cnt->n_keys != 0) return;
     const uint32_t nv = cnt->n_visible;
     unsigned long long acc = 0;
@@ -952,6 +961,7 @@ __global__ void __launch_bounds__(256) k_keys_on_overflow(const uint32_t *__rest
 __global__ void __launch_bounds__(256) k_row_bounds(const uint32_t *__restrict__ rows_per_ty,
                                                     const uint32_t *__restrict__ poff, Counters *cnt, int gy,
                                                     uint64_t max_keys, uint32_t *rowinfo) {
+    pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     auto excl = [&](uint32_t v) -> uint32_t {
@@ -999,6 +1009,7 @@ __global__ void __launch_bounds__(256) k_row_bounds(const uint32_t *__restrict__
 __global__ void __launch_bounds__(256) k_chunk_desc(const uint32_t *__restrict__ rowinfo,
                                                     const uint32_t *__restrict__ poff, const Counters *cnt, int gy,
                                                     uint4 *cdesc, uint32_t *cdesc_last) {
+    pdl_wait();
     const uint32_t nch = cnt->err ? 0u : cnt->n_cchunks;
     const uint32_t *rs = rowinfo, *P = rowinfo + 257, *cb = rowinfo + 2 * 257;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
@@ -1029,6 +1040,7 @@ __global__ void __launch_bounds__(256) k_chunk_desc(const uint32_t *__restrict__
 // chunks (in place in cmat) and the tile's pair count
 __global__ void __launch_bounds__(32) k_col_scan(const uint32_t *__restrict__ rowinfo, const Counters *cnt,
                                                  uint32_t *cmat, uint32_t ldm, int gx, uint32_t *tile_cnt) {
+    pdl_wait();
     const uint32_t ty = blockIdx.x, d = blockIdx.y, lane = threadIdx.x;
     const uint32_t *cb = rowinfo + 2 * 257;
     const uint32_t c0 = cnt->err ? 0u : cb[ty], c1 = cnt->err ? 0u : cb[ty + 1];
@@ -1052,6 +1064,7 @@ __global__ void __launch_bounds__(32) k_col_scan(const uint32_t *__restrict__ ro
 // per tile row: tile starts = row's first pair + exclusive scan of the tile counts
 __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ rowinfo,
                                                      const uint32_t *__restrict__ tile_cnt, int gx, uint2 *ranges) {
+    pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     const uint32_t ty = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t n = t < (uint32_t)gx ? tile_cnt[ty * gx + t] : 0u;
@@ -1080,7 +1093,7 @@ static void launch_count(const Workspace &ws, cudaStream_t st, int grid, Loader 
         cudaFuncSetAttribute(k_rs_count<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attrs = true;
     }
-    k_rs_count<Loader><<<grid, SORT_THREADS, smem, st>>>(ld, ws.counters, which, mk, shift, ws.cmat,
+    launch_pdl(k_rs_count<Loader>, grid, SORT_THREADS, smem, st, ld, ws.counters, which, mk, shift, ws.cmat,
                                                          (uint32_t)ws.max_chunks);
 }
 
@@ -1096,7 +1109,7 @@ static void launch_scatter(const Workspace &ws, cudaStream_t st, int grid, Loade
         cudaFuncSetAttribute(k_rs_scatter<Loader, DBITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc_smem);
         attrs = true;
     }
-    k_rs_scatter<Loader, DBITS><<<grid, SORT_THREADS, sc_smem, st>>>(ld, kout, vout, ws.counters, which, mk, shift,
+    launch_pdl(k_rs_scatter<Loader, DBITS>, grid, SORT_THREADS, sc_smem, st, ld, kout, vout, ws.counters, which, mk, shift,
                                                                      ws.cmat, (uint32_t)ldm, ws.row_total);
 }
 
@@ -1107,7 +1120,7 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
                       int which, uint64_t mk, int shift, int dbits = 8) {
     const size_t ldm = ws.max_chunks;
     launch_count(ws, st, grid, ld, which, mk, shift);
-    k_rs_scanrows<<<256, 1024, 0, st>>>(ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
+    launch_pdl(k_rs_scanrows, 256, 1024, 0, st, ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
     switch (dbits) {
     case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 2: launch_scatter<Loader, 2>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
@@ -1123,9 +1136,9 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
 
 template <class Op>
 static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint32_t n_points) {
-    k_scan_reduce<Op><<<grid, SORT_THREADS, 0, st>>>(op, n_points, ws.sums);
-    k_scan_sums<Op><<<1, 1024, 0, st>>>(op, n_points, ws.sums);
-    k_scan_apply<Op><<<grid, SORT_THREADS, 0, st>>>(op, n_points, ws.sums);
+    launch_pdl(k_scan_reduce<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
+    launch_pdl(k_scan_sums<Op>, 1, 1024, 0, st, op, n_points, ws.sums);
+    launch_pdl(k_scan_apply<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
     return 3;
 }
 
@@ -1153,8 +1166,8 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     const int grid_k = std::max(1, std::min(nsm * 8, ceil_div_i(max_keys, SORT_CHUNK)));
     const uint64_t mk = (uint64_t)max_keys;
     const int gy = ntiles / gx;
-    cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
-    int launches = 0;
+    if (!(gx <= 256 && gy <= 256)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
+    int launches = 0;   // (the two-level path writes every tile range: no memset node)
     // 1. compaction of the visible Gaussians (index order)
     launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[0], ws.sv[0], cnt}, (uint32_t)N);
     // 2. depth sort: 4 stable passes of 8 bits; the result is back in sk[0]/sv[0]
@@ -1178,15 +1191,15 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
                                ws.kt[1], ws.kv[1], CNT_RENT, mk, 0, std::max(1, tby));
         // 5. pair offsets of the entries (kt[0])
         launches += scan_pass(ws, st, grid_k, PairOffsetsOp{ws.kt[1], ws.kt[0], cnt, mk}, (uint32_t)N);
-        k_keys_on_overflow<<<nsm, 256, 0, st>>>(ws.sv[0], ws.touched, cnt);
+        launch_pdl(k_keys_on_overflow, nsm, 256, 0, st, ws.sv[0], ws.touched, cnt);
         // 6. row bounds and row-aligned column chunks
-        k_row_bounds<<<1, 256, 0, st>>>(ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
-        k_chunk_desc<<<nsm * 2, 256, 0, st>>>(ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
+        launch_pdl(k_row_bounds, 1, 256, 0, st, ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
+        launch_pdl(k_chunk_desc, nsm * 2, 256, 0, st, ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
         // 7. columns: counts, per-(row, column) scans, tile ranges, stable scatter of the indices
         const ColLoader<false> col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
         launch_count(ws, st, grid_k, col, CNT_KEYS, mk, 0);
-        k_col_scan<<<dim3(gy, gx), 32, 0, st>>>(ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx, ws.tile_cnt);
-        k_tile_ranges<<<gy, 256, 0, st>>>(ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
+        launch_pdl(k_col_scan, dim3(gy, gx), 32, 0, st, ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx, ws.tile_cnt);
+        launch_pdl(k_tile_ranges, gy, 256, 0, st, ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
         if (N < (1 << 24)) {
             const ColLoader<true> colp{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
             col_scatter(ws, st, grid_k, colp, tbx, mk);
@@ -1212,7 +1225,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
             xattr = true;
         }
         const int e = tpasses & 1;   // the passes alternate buffers and end in kt[0]/kv[0]
-        k_expand<<<grid_k, SORT_THREADS, xs, st>>>(
+        launch_pdl(k_expand, grid_k, SORT_THREADS, xs, st, 
             Expander{ws.off, ws.sv[0], ws.chunk_first, ws.rect_r, tight ? ws.tmask_r : nullptr, cnt, gx}, mk,
             ws.kt[e], ws.kv[e]);
         launches++;
@@ -1223,7 +1236,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         }
     }
     // 5. tile ranges
-    k_ranges<<<nsm * 4, 256, 0, st>>>(ws.kt[0], cnt, mk, ws.ranges);
+    launch_pdl(k_ranges, nsm * 4, 256, 0, st, ws.kt[0], cnt, mk, ws.ranges);
     return launches + 1;
 }
 

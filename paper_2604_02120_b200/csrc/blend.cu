@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
+    pdl_wait();   // the setup above overlapped the binning's tail
 
     if (warp == WARP_PRODUCER) {
         // =================== producer: asynchronous gathers ===================
@@ -506,13 +507,13 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
 #define ARGS xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
-        k_blend_tc<true, false, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
+        launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
     else if (stats)
-        k_blend_tc<false, true, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
+        launch_pdl(k_blend_tc<false, true, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
     else if (g_blend_trace)
-        k_blend_tc<false, false, true><<<grid, TC_THREADS, smem, st>>>(ARGS, g_blend_trace);
+        launch_pdl(k_blend_tc<false, false, true>, grid, TC_THREADS, smem, st, ARGS, g_blend_trace);
     else
-        k_blend_tc<false, false, false><<<grid, TC_THREADS, smem, st>>>(ARGS, nullptr);
+        launch_pdl(k_blend_tc<false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
 #undef ARGS
 }
 
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__
                                                       const uint2 *__restrict__ ranges, int gx, int W, int H,
                                                       float bg0, float bg1, float bg2, float *__restrict__ out_rgb,
                                                       float *__restrict__ out_T) {
+    pdl_wait();
     __shared__ float4 s_g[256];     // (x, y, A, B)
     __shared__ float2 s_g2[256];    // (C, log2 o)
     __shared__ float4 s_c[256];
@@ -578,7 +580,7 @@ void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_
                          const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *) {
     if (ntiles <= 0) return;
-    k_blend_direct<<<ntiles, 256, 0, st>>>(xy, conic_o, rgb, vals, ranges, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
+    launch_pdl(k_blend_direct, ntiles, 256, 0, st, xy, conic_o, rgb, vals, ranges, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
                                            out_T);
 }
 

@@ -3,6 +3,7 @@
 // Product code only: nothing here is shared with oracle/.
 #pragma once
 #include <cuda_runtime.h>
+#include <utility>
 #include <stdint.h>
 
 #include "../../include/gs_render.h"
@@ -71,6 +72,29 @@ constexpr int SORT_ITEMS = 16;
 constexpr int SORT_CHUNK = SORT_THREADS * SORT_ITEMS;   // 4096 keys per chunk
 
 __host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- programmatic dependent launch ------------------------------------------
+// Every kernel of the frame path is launched with programmatic stream
+// serialisation and calls pdl_wait() before it touches its predecessor's results,
+// so its launch (and any setup before the wait) overlaps the predecessor's tail.
+// Without the launch attribute griddepcontrol.wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- small PTX helpers ------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

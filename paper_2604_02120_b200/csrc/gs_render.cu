@@ -89,7 +89,7 @@ void mark(gs_ctx *c, cudaStream_t st, const gs_opts &o, int k) {
 void enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
                    const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
     mark(c, st, o, 0);
-    cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
+    if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
     const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
                           o.scale_modifier, cam, W, H, tight);

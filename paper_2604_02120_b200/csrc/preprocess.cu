@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const floa
                                                                const float *__restrict__ shs, int sh_degree,
                                                                int sh_stride, float scale_mod, int W, int H,
                                                                const gs_camera cam, Workspace ws, bool tight) {
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *ws.counters = Counters{};   // the frame's device counters (no memset node: keeps PDL chained)
     if (i >= N) return;
     const float *R = cam.R;
     const int gx = (W + GS_TILE - 1) / GS_TILE, gy = (H + GS_TILE - 1) / GS_TILE;
@@ -262,7 +264,7 @@ void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float 
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
                        int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight) {
     if (N <= 0) return;
-    k_preprocess<<<ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st>>>(
+    launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
         N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
         H, cam, ws, tight);
 }
