@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -236,7 +237,8 @@ def run_ours(args):
         "preprocess": {"ms": pre_ms, "bound": "hbm", "achieved": pre_bytes / (pre_ms * 1e-3) / 1e9,
                        "peak": hbm, "unit": "GB/s"},
         "binning": {"ms": bin_ms, "bound": "hbm", "achieved": bin_bytes / (bin_ms * 1e-3) / 1e9, "peak": hbm,
-                    "unit": "GB/s", "kernels": "compaction, 4 depth passes, duplication, tile sort, ranges"},
+                    "unit": "GB/s", "kernels": "compaction, 4 depth passes, row entries + row pass, pair offsets, "
+                    "column pass with tile ranges (two-level binning)"},
         "blend": {"ms": blend_ms, "bound": "alu", "achieved": blend_flop / (blend_ms * 1e-3) / 1e12,
                   "peak": fp32_peak, "unit": "TFLOP/s", "pairs_evaluated": n_eval, "pairs_kept": n_kept},
     }
@@ -295,6 +297,41 @@ def run_ours(args):
                  "n_keys_view0": ts.n_keys, "pairs_evaluated_view0": ts.pairs_evaluated,
                  "note": "GS_FLAG_TIGHT: frames bit-identical to the vanilla-rect ones (tested)"}
 
+    # --- N2: resolution sensitivity (1x / 2x / 3x of 1080p, same scene, orbit views) ---
+    res_sweep = None
+    if not args.no_sweep and ws == 1:
+        res_sweep = {}
+        o_r = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=base_flags)
+        for sc in (1, 2, 3):
+            Ws, Hs = W * sc, H * sc
+            cams_s = [camera(c) for c in synth.orbit_cameras(args.views, Ws, Hs, math.radians(60.0))]
+            cams_s = cams_s[:: max(1, args.views // args.sweep_views)][:args.sweep_views]
+            ctx_s = ctx if sc == 1 else Context(local, max_points=scene.n, max_keys=args.max_keys * sc * sc,
+                                                   max_w=Ws, max_h=Hs)
+            rgb_s = torch.empty((len(cams_s), 3, Hs, Ws), device="cuda")
+            T_s = torch.empty((len(cams_s), Hs, Ws), device="cuda")
+            ctx_s.gs_render_views(st, cams_s, Ws, Hs, o_r, rgb_s, T_s, stream)   # warm
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(2):
+                ctx_s.gs_render_views(st, cams_s, Ws, Hs, o_r, rgb_s, T_s, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / (2 * len(cams_s))
+            ctx_s.gs_render(st, cams_s[0], Ws, Hs, opts(bg, sh_degree=scene.sh_degree, flags=GS_FLAG_STATS | base_flags),
+                            rgb_s[0], T_s[0], stream)
+            s0 = ctx_s.gs_last_stats()
+            gx, gy = -(-Ws // 16), -(-Hs // 16)
+            res_sweep[f"{sc}x"] = {"W": Ws, "H": Hs, "fps": 1e3 / ms, "ms_per_frame": ms, "views": len(cams_s),
+                                   "n_keys_view0": s0.n_keys, "pairs_evaluated_view0": s0.pairs_evaluated,
+                                   "binning": "two-level" if gx <= 256 and gy <= 256 else "one-level"}
+            del rgb_s, T_s
+            if ctx_s is not ctx:
+                ctx_s.close()
+        torch.cuda.empty_cache()
+
     # --- end to end through the host-pointer C-ABI entry point ---------------
     e2e = None
     if not args.no_e2e:
@@ -335,6 +372,7 @@ def run_ours(args):
                     k: v["ms"] for k, v in stages.items()},
                 "roofline": roof, "stages": stages, "clocks": clk,
                 "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_direct_blend": ab, "tight_intersection": tight,
+                "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
                                    "pairs_kept": n_kept}}
         print(json.dumps(line), flush=True)
@@ -357,6 +395,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ab", action="store_true")
     ap.add_argument("--tight", action="store_true", help="time the GS_FLAG_TIGHT path as the headline")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the N2 resolution sweep")
+    ap.add_argument("--sweep-views", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

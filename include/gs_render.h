@@ -105,6 +105,8 @@ typedef struct gs_ctx gs_ctx;
 
 /* Creates a context owning device workspace for up to max_points Gaussians,
  * max_keys duplicated keys and max_w x max_h images on `device`.
+ * Limits: max_keys < 2^32, max_points < 2^31, at most 2^20 16x16 tiles
+ * (e.g. 16384 x 16384 px); otherwise GS_ERR_INVALID_ARG.
  * Fails with GS_ERR_UNSUPPORTED_ARCH unless the device is sm_100. */
 int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys,
                   int max_w, int max_h);

@@ -26,7 +26,7 @@ struct Counters {
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
 
-constexpr int MAX_TILES = 65536;   // tile ids sorted in two 8-bit passes
+constexpr int MAX_TILES = 1 << 20;   // 16384 x 16384 px; one-level binning sorts ceil(tile bits / 8) passes
 
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
