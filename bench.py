@@ -326,7 +326,7 @@ def run_ours(args):
             gx, gy = -(-Ws // 16), -(-Hs // 16)
             res_sweep[f"{sc}x"] = {"W": Ws, "H": Hs, "fps": 1e3 / ms, "ms_per_frame": ms, "views": len(cams_s),
                                    "n_keys_view0": s0.n_keys, "pairs_evaluated_view0": s0.pairs_evaluated,
-                                   "binning": "two-level" if gx <= 256 and gy <= 256 else "one-level"}
+                                   "binning": "two-level" if gx <= 512 and gy <= 512 else "one-level"}
             del rgb_s, T_s
             if ctx_s is not ctx:
                 ctx_s.close()

@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // bases come from the digit totals (s_dbase). Loaders derive from this unless they
 // define their own chunks (ColLoader).
 struct LinearChunks {
-    static constexpr bool PACKED = false;       // key = digit | value << 8, no separate values
+    static constexpr bool PACKED = false;       // key = digit | value << PACK_SHIFT, no separate values
+    static constexpr int PACK_SHIFT = 0;
     static constexpr bool EXPANDS = false;      // keys via key(i) from global memory
     static constexpr bool RUN_COUNTS = false;   // digit counts from runs (count_runs)
     __device__ uint32_t nchunks(uint32_t n) const { return (n + SORT_CHUNK - 1) / SORT_CHUNK; }
@@ -393,45 +394,52 @@ __global__ void __launch_bounds__(SORT_THREADS) k_expand(Expander ex, uint64_t m
 // ---------------------------------------------------------------------------
 // radix pass, step 1: per-chunk digit counts -> cmat[digit][chunk]
 // ---------------------------------------------------------------------------
-template <class Loader>
+template <class Loader, int NDIG>
 __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Counters *cnt, int which,
                                                            uint64_t max_keys, int shift, uint32_t *cmat,
                                                            uint32_t ldm) {
     pdl_wait();
-    extern __shared__ uint32_t dyn[];   // expanding loaders: the chunk's keys + loader scratch
-    constexpr int NH = 4;   // privatised histograms (warp % NH)
-    __shared__ uint32_t s_h[NH][256];
+    static_assert(NDIG == 256 || NDIG == 512, "8- or 9-bit digits");
+    constexpr int DPT = NDIG / SORT_THREADS;   // digits per thread
+    extern __shared__ uint32_t dyn[];          // expanding loaders: the chunk's keys + loader scratch
+    constexpr int NH = 4;                      // privatised histograms (warp % NH)
+    __shared__ uint32_t s_h[NH][NDIG];
+    __shared__ uint32_t s_w[NWARP];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
     const uint32_t nchunks = ld.nchunks(n);
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         uint32_t cbase, cvalid;
         ld.chunk(c, n, cbase, cvalid);
         if constexpr (Loader::RUN_COUNTS) {
-            int *s_diff = reinterpret_cast<int *>(&s_h[0][0]);   // 257 entries
-            s_diff[threadIdx.x] = 0;
-            if (threadIdx.x == 0) s_diff[256] = 0;
+            int *s_diff = reinterpret_cast<int *>(&s_h[0][0]);   // NDIG + 1 entries
+            for (int i = threadIdx.x; i <= NDIG; i += SORT_THREADS) s_diff[i] = 0;
             __syncthreads();
             ld.count_runs(c, cbase, cvalid, s_diff);
             __syncthreads();
-            // inclusive scan of the difference array = the digit counts
-            __shared__ uint32_t s_w[NWARP];
-            const int lane = threadIdx.x & 31;
-            uint32_t x = (uint32_t)s_diff[threadIdx.x];
+            // inclusive scan of the difference array = the digit counts (DPT digits per thread)
+            uint32_t loc[DPT], x = 0;
+#pragma unroll
+            for (int i = 0; i < DPT; i++) {
+                x += (uint32_t)s_diff[threadIdx.x * DPT + i];
+                loc[i] = x;
+            }
+            uint32_t sc = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, sc, o);
+                if (lane >= o) sc += y;
             }
-            if (lane == 31) s_w[warp] = x;
+            if (lane == 31) s_w[warp] = sc;
             __syncthreads();
-            for (int w = 0; w < warp; w++) x += s_w[w];
-            cmat[(size_t)threadIdx.x * ldm + c] = x;
+            uint32_t base = sc - x;
+            for (int w = 0; w < warp; w++) base += s_w[w];
+#pragma unroll
+            for (int i = 0; i < DPT; i++) cmat[(size_t)(threadIdx.x * DPT + i) * ldm + c] = base + loc[i];
             __syncthreads();
             continue;
         }
-#pragma unroll
-        for (int h = 0; h < NH; h++) s_h[h][threadIdx.x] = 0;
+        for (int i = threadIdx.x; i < NH * NDIG; i += SORT_THREADS) (&s_h[0][0])[i] = 0;
         uint32_t k[SORT_ITEMS];
         if constexpr (Loader::EXPANDS) {
             ld.load(c, cbase, cvalid, dyn, nullptr, dyn + SORT_CHUNK);
@@ -452,13 +460,17 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
 #pragma unroll
         for (int q = 0; q < SORT_ITEMS; q++) {
             const uint32_t e = threadIdx.x + q * SORT_THREADS;
-            if (e < cvalid) atomicAdd(&s_h[warp % NH][(k[q] >> shift) & 255u], 1u);
+            if (e < cvalid) atomicAdd(&s_h[warp % NH][(k[q] >> shift) & (NDIG - 1)], 1u);
         }
         __syncthreads();
-        uint32_t t = 0;
 #pragma unroll
-        for (int h = 0; h < NH; h++) t += s_h[h][threadIdx.x];
-        cmat[(size_t)threadIdx.x * ldm + c] = t;
+        for (int i = 0; i < DPT; i++) {
+            const int d = threadIdx.x * DPT + i;
+            uint32_t t = 0;
+#pragma unroll
+            for (int h = 0; h < NH; h++) t += s_h[h][d];
+            cmat[(size_t)d * ldm + c] = t;
+        }
         __syncthreads();
     }
 }
@@ -502,28 +514,33 @@ __global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int w
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
 // earlier chunks) + (rank among this chunk's elements of the digit)
 template <class Loader, int DBITS>
-__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_scatter(Loader ld, uint32_t *__restrict__ kout,
-                                                             uint32_t *__restrict__ vout, const Counters *cnt,
-                                                             int which, uint64_t max_keys, int shift,
-                                                             const uint32_t *__restrict__ cmat, uint32_t ldm,
-                                                             const uint32_t *__restrict__ row_total) {
+__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3)
+    k_rs_scatter(Loader ld, uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, const Counters *cnt,
+                 int which, uint64_t max_keys, int shift, const uint32_t *__restrict__ cmat, uint32_t ldm,
+                 const uint32_t *__restrict__ row_total) {
     pdl_wait();
+    constexpr int NDIG = DBITS > 8 ? 512 : 256;
+    constexpr int DPT = NDIG / SORT_THREADS;   // digits owned per thread (consecutive)
     extern __shared__ uint32_t dyn[];
-    // PACKED loaders carry the value in the key's upper bits (key = digit | value << 8):
+    // PACKED loaders carry the value in the key's upper bits (key = digit | value << PACK_SHIFT):
     // one word per element, half the shared memory, more resident blocks
     constexpr bool PK = Loader::PACKED;
     uint32_t *s_k = dyn, *s_v = PK ? nullptr : dyn + SORT_CHUNK;                    // loaded chunk
     uint32_t *s_ok = dyn + (PK ? 1 : 2) * SORT_CHUNK, *s_ov = PK ? nullptr : dyn + 3 * SORT_CHUNK;   // digit order
     // loader scratch: expanding loaders are done with it before s_ok is written
     uint32_t *s_scr = Loader::EXPANDS ? s_ok : dyn + 4 * SORT_CHUNK;
-    __shared__ uint16_t s_whist[NWARP][256];
-    __shared__ uint32_t s_dbase[256], s_blk[256], s_base[256], s_tot[NWARP];
+    __shared__ uint16_t s_whist[NWARP][NDIG];
+    __shared__ uint32_t s_dbase[NDIG], s_blk[NDIG], s_base[NDIG], s_tot[NWARP];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
     const uint32_t nchunks = ld.nchunks(n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int d_own = threadIdx.x;
-    auto block_excl_scan = [&](uint32_t v) -> uint32_t {   // over the 256 threads (one value each)
-        uint32_t x = v;
+    const int d0 = threadIdx.x * DPT;
+    // exclusive scan over all NDIG digits; v[i] belongs to digit d0 + i
+    auto block_excl_scan = [&](const uint32_t (&v)[DPT], uint32_t (&out)[DPT]) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int i = 0; i < DPT; i++) t += v[i];
+        uint32_t x = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -531,18 +548,33 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
         }
         if (lane == 31) s_tot[warp] = x;
         __syncthreads();
-        uint32_t wb = 0;
+        uint32_t wb = x - t;
         for (int w = 0; w < warp; w++) wb += s_tot[w];
         __syncthreads();
-        return wb + x - v;
+#pragma unroll
+        for (int i = 0; i < DPT; i++) {
+            out[i] = wb;
+            wb += v[i];
+        }
     };
-    s_dbase[d_own] = block_excl_scan(row_total[d_own]);
+    {
+        uint32_t v[DPT], o[DPT];
+#pragma unroll
+        for (int i = 0; i < DPT; i++) v[i] = row_total[d0 + i];
+        block_excl_scan(v, o);
+#pragma unroll
+        for (int i = 0; i < DPT; i++) s_dbase[d0 + i] = o[i];
+    }
+    __syncthreads();
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         uint32_t cbase, cvalid;
         ld.chunk(c, n, cbase, cvalid);
 #pragma unroll
-        for (int w = 0; w < NWARP; w++) s_whist[w][d_own] = 0;
-        s_base[d_own] = ld.digit_base(c, d_own, s_dbase) + cmat[(size_t)d_own * ldm + c];
+        for (int i = 0; i < DPT; i++) {
+#pragma unroll
+            for (int w = 0; w < NWARP; w++) s_whist[w][d0 + i] = 0;
+            s_base[d0 + i] = ld.digit_base(c, d0 + i, s_dbase) + cmat[(size_t)(d0 + i) * ldm + c];
+        }
         ld.load(c, cbase, cvalid, s_k, s_v, s_scr);
         __syncthreads();
         // warp-local stable ranks
@@ -551,7 +583,7 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
         for (int r = 0; r < SORT_ITEMS; r++) {
             const int e = elem_of(warp, r, lane);
             const bool valid = (uint32_t)e < cvalid;
-            const uint32_t d = valid ? ((s_k[e] >> shift) & 255u) : 0u;
+            const uint32_t d = valid ? ((s_k[e] >> shift) & (NDIG - 1)) : 0u;
             const uint32_t peers = peers_of<DBITS>(d, valid);
             uint32_t before = 0;
             if (valid) before = s_whist[warp][d];
@@ -561,21 +593,30 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
             rank[r] = before + __popc(peers & lanemask_lt());
         }
         __syncthreads();
-        uint32_t total = 0;
+        {
+            uint32_t tot[DPT], o[DPT];
 #pragma unroll
-        for (int w = 0; w < NWARP; w++) {
-            const uint32_t t = s_whist[w][d_own];
-            s_whist[w][d_own] = (uint16_t)total;
-            total += t;
+            for (int i = 0; i < DPT; i++) {
+                uint32_t total = 0;
+#pragma unroll
+                for (int w = 0; w < NWARP; w++) {
+                    const uint32_t t = s_whist[w][d0 + i];
+                    s_whist[w][d0 + i] = (uint16_t)total;
+                    total += t;
+                }
+                tot[i] = total;
+            }
+            block_excl_scan(tot, o);
+#pragma unroll
+            for (int i = 0; i < DPT; i++) s_blk[d0 + i] = o[i];
         }
-        s_blk[d_own] = block_excl_scan(total);
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < SORT_ITEMS; r++) {
             const int e = elem_of(warp, r, lane);
             if ((uint32_t)e < cvalid) {
                 const uint32_t k = s_k[e];
-                const uint32_t d = (k >> shift) & 255u;
+                const uint32_t d = (k >> shift) & (NDIG - 1);
                 const uint32_t pos = s_blk[d] + s_whist[warp][d] + rank[r];
                 s_ok[pos] = k;
                 if (!PK) s_ov[pos] = s_v[e];
@@ -586,10 +627,10 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3) k_rs_sca
 #pragma unroll 4
         for (uint32_t p = threadIdx.x; p < cvalid; p += SORT_THREADS) {
             const uint32_t k = s_ok[p];
-            const uint32_t d = (k >> shift) & 255u;
+            const uint32_t d = (k >> shift) & (NDIG - 1);
             const uint32_t g = s_base[d] + (p - s_blk[d]);
-            if (PK) {
-                vout[g] = k >> 8;
+            if constexpr (PK) {
+                vout[g] = k >> Loader::PACK_SHIFT;
             } else {
                 if (kout) kout[g] = k;
                 vout[g] = s_ov[p];
@@ -629,7 +670,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ til
 }
 
 // ---------------------------------------------------------------------------
-// Two-level binning (tile grids up to 256 x 256): the stable sort by tile of the
+// Two-level binning (tile grids up to 512 x 512): the stable sort by tile of the
 // depth-ordered pairs is done MSD-style without materialising the K tile keys.
 //   rows:    each depth-ordered Gaussian r contributes one entry per tile row it
 //            keeps; one stable 8-bit pass on the row ty puts the entries in
@@ -732,7 +773,7 @@ __device__ __forceinline__ void warp_expand(uint32_t len, F &&emit) {
 
 // Row entries cbase .. cbase+cvalid-1: entry e belongs to the depth-ordered Gaussian r
 // with roff[r] <= e < roff[r+1] and is r's (e - roff[r])-th kept tile row ty. Its key
-// packs the row and the row's run of kept tile columns: ty | x0 << 8 | width << 16
+// packs the row and the row's run of kept tile columns: ty | x0 << 9 | width << 18
 // (a GS_FLAG_TIGHT row keeps one contiguous run of columns); value = Gaussian index.
 struct RowLoader : LinearChunks {
     const uint32_t *roff, *chunk_first, *rowmask_r, *sorted_idx;   // rowmask_r: GS_FLAG_TIGHT only
@@ -807,7 +848,7 @@ struct RowLoader : LinearChunks {
                     x0 = x0r + (uint32_t)(__ffs(bits) - 1);
                     wr = (uint32_t)__popc(bits);
                 }
-                sk[wslot + t] = (y0 + q) | (x0 << 8) | (wr << 16);
+                sk[wslot + t] = (y0 + q) | (x0 << 9) | (wr << 18);
                 if (sv) sv[wslot + t] = oidx;
             });
         }
@@ -855,8 +896,8 @@ struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (ru
     uint64_t max_keys;
     static constexpr int WHICH = CNT_RENT;
     struct Aux {};
-    __device__ uint32_t load(uint32_t e) const { return e_key[e] >> 16; }
-    __device__ uint32_t load(uint32_t e, Aux &) const { return e_key[e] >> 16; }
+    __device__ uint32_t load(uint32_t e) const { return e_key[e] >> 18; }
+    __device__ uint32_t load(uint32_t e, Aux &) const { return e_key[e] >> 18; }
     __device__ void emit(uint32_t e, uint64_t o, uint32_t, const Aux &) const {
         poff[e] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
     }
@@ -869,9 +910,10 @@ struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (ru
 // Pairs of one row-aligned chunk (cdesc): pair p belongs to the entry e with
 // poff[e] <= p < poff[e+1] and is column x0 + (p - poff[e]) of its run. key = tile
 // column tx, value = Gaussian index; digit bases are the tile starts (ranges[.].x).
-template <bool PK>
+template <bool PK, int RB>
 struct ColLoader {
-    static constexpr bool PACKED = PK;   // Gaussian indices < 2^24: key = tx | index << 8
+    static constexpr bool PACKED = PK;    // Gaussian indices < 2^(32 - RB): key = tx | index << RB
+    static constexpr int PACK_SHIFT = RB;
     const uint32_t *poff, *e_key, *e_idx, *cdesc_last;
     const uint4 *cdesc;
     const uint2 *ranges;
@@ -894,8 +936,8 @@ struct ColLoader {
         for (uint32_t e = e_lo + threadIdx.x; e <= e_hi; e += SORT_THREADS) {
             const uint32_t o = poff[e], k = e_key[e];
             const uint32_t q0 = o < cbase ? cbase - o : 0u;
-            const uint32_t len = min(o + (k >> 16), cend) - (o + q0);
-            const uint32_t x = ((k >> 8) & 0xFFu) + q0;
+            const uint32_t len = min(o + (k >> 18), cend) - (o + q0);
+            const uint32_t x = ((k >> 9) & 0x1FFu) + q0;
             atomicAdd(&s_diff[x], 1);
             atomicAdd(&s_diff[x + len], -1);
         }
@@ -922,8 +964,8 @@ struct ColLoader {
             uint32_t len = 0, x = 0, slot0 = 0;
             if (e <= e_hi) {
                 const uint32_t q0 = o < cbase ? cbase - o : 0u;
-                len = min(o + (k >> 16), cend) - (o + q0);
-                x = ((k >> 8) & 0xFFu) + q0;
+                len = min(o + (k >> 18), cend) - (o + q0);
+                x = ((k >> 9) & 0x1FFu) + q0;
                 slot0 = o + q0 - cbase;
             }
             const uint32_t wslot = __shfl_sync(0xffffffffu, slot0, 0);
@@ -932,7 +974,7 @@ struct ColLoader {
                 const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
                 if (!valid) return;
                 if (PK) {
-                    sk[wslot + t] = (ox + j) | (oidx << 8);
+                    sk[wslot + t] = (ox + j) | (oidx << RB);
                 } else {
                     sk[wslot + t] = ox + j;
                     if (sv) sv[wslot + t] = oidx;
@@ -958,11 +1000,11 @@ __global__ void __launch_bounds__(256) k_keys_on_overflow(const uint32_t *__rest
 }
 
 // one block: per tile row, first entry / first pair / first column chunk; chunk count
-__global__ void __launch_bounds__(256) k_row_bounds(const uint32_t *__restrict__ rows_per_ty,
+__global__ void __launch_bounds__(512) k_row_bounds(const uint32_t *__restrict__ rows_per_ty,
                                                     const uint32_t *__restrict__ poff, Counters *cnt, int gy,
                                                     uint64_t max_keys, uint32_t *rowinfo) {
     pdl_wait();
-    __shared__ uint32_t s_w[NWARP];
+    __shared__ uint32_t s_w[16];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     auto excl = [&](uint32_t v) -> uint32_t {
         uint32_t x = v;
@@ -985,22 +1027,22 @@ __global__ void __launch_bounds__(256) k_row_bounds(const uint32_t *__restrict__
     const uint32_t rs = excl(ne);
     const uint32_t P = (t <= gy && rs < R) ? poff[rs] : K;
     // pairs of row t: next row's first pair - P (rows are contiguous in pair order)
-    __shared__ uint32_t s_P[257];
+    __shared__ uint32_t s_P[513];
     s_P[t] = P;
-    if (t == 0) s_P[256] = K;
+    if (t == 0) s_P[512] = K;
     __syncthreads();
     const uint32_t np = t < gy ? s_P[t + 1] - P : 0u;
     const uint32_t nch = (np + SORT_CHUNK - 1) / SORT_CHUNK;
     const uint32_t cb = excl(nch);
     if (t < gy) {
         rowinfo[t] = rs;
-        rowinfo[257 + t] = P;
-        rowinfo[2 * 257 + t] = cb;
+        rowinfo[513 + t] = P;
+        rowinfo[2 * 513 + t] = cb;
     }
     if (t == gy - 1) {   // sentinels of row gy
         rowinfo[gy] = R;
-        rowinfo[257 + gy] = K;
-        rowinfo[2 * 257 + gy] = cb + nch;
+        rowinfo[513 + gy] = K;
+        rowinfo[2 * 513 + gy] = cb + nch;
         cnt->n_cchunks = cb + nch;
     }
 }
@@ -1011,7 +1053,7 @@ __global__ void __launch_bounds__(256) k_chunk_desc(const uint32_t *__restrict__
                                                     uint4 *cdesc, uint32_t *cdesc_last) {
     pdl_wait();
     const uint32_t nch = cnt->err ? 0u : cnt->n_cchunks;
-    const uint32_t *rs = rowinfo, *P = rowinfo + 257, *cb = rowinfo + 2 * 257;
+    const uint32_t *rs = rowinfo, *P = rowinfo + 513, *cb = rowinfo + 2 * 513;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += gridDim.x * blockDim.x) {
         int lo = 0, hi = gy - 1;   // last row with cb[row] <= c
         while (lo < hi) {
@@ -1042,7 +1084,7 @@ __global__ void __launch_bounds__(32) k_col_scan(const uint32_t *__restrict__ ro
                                                  uint32_t *cmat, uint32_t ldm, int gx, uint32_t *tile_cnt) {
     pdl_wait();
     const uint32_t ty = blockIdx.x, d = blockIdx.y, lane = threadIdx.x;
-    const uint32_t *cb = rowinfo + 2 * 257;
+    const uint32_t *cb = rowinfo + 2 * 513;
     const uint32_t c0 = cnt->err ? 0u : cb[ty], c1 = cnt->err ? 0u : cb[ty + 1];
     uint32_t *row = cmat + (size_t)d * ldm;
     uint32_t carry = 0;
@@ -1062,10 +1104,10 @@ __global__ void __launch_bounds__(32) k_col_scan(const uint32_t *__restrict__ ro
 }
 
 // per tile row: tile starts = row's first pair + exclusive scan of the tile counts
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ rowinfo,
+__global__ void __launch_bounds__(512) k_tile_ranges(const uint32_t *__restrict__ rowinfo,
                                                      const uint32_t *__restrict__ tile_cnt, int gx, uint2 *ranges) {
     pdl_wait();
-    __shared__ uint32_t s_w[NWARP];
+    __shared__ uint32_t s_w[16];
     const uint32_t ty = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint32_t n = t < (uint32_t)gx ? tile_cnt[ty * gx + t] : 0u;
     uint32_t x = n;
@@ -1078,22 +1120,22 @@ __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict_
     __syncthreads();
     uint32_t b = 0;
     for (uint32_t w = 0; w < warp; w++) b += s_w[w];
-    const uint32_t start = rowinfo[257 + ty] + b + x - n;
+    const uint32_t start = rowinfo[513 + ty] + b + x - n;
     if (t < (uint32_t)gx) ranges[ty * gx + t] = n ? make_uint2(start, start + n) : make_uint2(0u, 0u);
 }
 
 // ---------------------------------------------------------------------------
-template <class Loader>
+template <class Loader, int NDIG = 256>
 static void launch_count(const Workspace &ws, cudaStream_t st, int grid, Loader ld, int which, uint64_t mk,
                          int shift) {
     const size_t smem =
         (Loader::EXPANDS && !Loader::RUN_COUNTS) ? (SORT_CHUNK + Loader::SCRATCH_WORDS) * sizeof(uint32_t) : 0;
     static bool attrs = false;
     if (!attrs && smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_rs_count<Loader>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_rs_count<Loader, NDIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attrs = true;
     }
-    launch_pdl(k_rs_count<Loader>, grid, SORT_THREADS, smem, st, ld, ws.counters, which, mk, shift, ws.cmat,
+    launch_pdl(k_rs_count<Loader, NDIG>, grid, SORT_THREADS, smem, st, ld, ws.counters, which, mk, shift, ws.cmat,
                                                          (uint32_t)ws.max_chunks);
 }
 
@@ -1113,14 +1155,16 @@ static void launch_scatter(const Workspace &ws, cudaStream_t st, int grid, Loade
                                                                      ws.cmat, (uint32_t)ldm, ws.row_total);
 }
 
-// One stable LSD pass on bits [shift, shift + dbits) (dbits <= 8; higher key bits
+// One stable LSD pass on bits [shift, shift + dbits) (dbits <= 9; higher key bits
 // must already be zero above shift + dbits or belong to later passes).
 template <class Loader>
 static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld, uint32_t *kout, uint32_t *vout,
                       int which, uint64_t mk, int shift, int dbits = 8) {
     const size_t ldm = ws.max_chunks;
-    launch_count(ws, st, grid, ld, which, mk, shift);
-    launch_pdl(k_rs_scanrows, 256, 1024, 0, st, ws.counters, which, mk, ws.cmat, (uint32_t)ldm, ws.row_total);
+    if (dbits > 8) launch_count<Loader, 512>(ws, st, grid, ld, which, mk, shift);
+    else launch_count<Loader, 256>(ws, st, grid, ld, which, mk, shift);
+    launch_pdl(k_rs_scanrows, dbits > 8 ? 512 : 256, 1024, 0, st, ws.counters, which, mk, ws.cmat, (uint32_t)ldm,
+               ws.row_total);
     switch (dbits) {
     case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 2: launch_scatter<Loader, 2>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
@@ -1129,6 +1173,7 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
     case 5: launch_scatter<Loader, 5>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 6: launch_scatter<Loader, 6>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 7: launch_scatter<Loader, 7>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
+    case 9: launch_scatter<Loader, 9>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     default: launch_scatter<Loader, 8>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     }
     return 3;
@@ -1152,7 +1197,26 @@ static void col_scatter(const Workspace &ws, cudaStream_t st, int grid, const L 
     case 5: launch_scatter<L, 5>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
     case 6: launch_scatter<L, 6>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
     case 7: launch_scatter<L, 7>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    case 9: launch_scatter<L, 9>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
     default: launch_scatter<L, 8>(ws, st, grid, col, nullptr, ws.kv[0], CNT_KEYS, mk, 0); break;
+    }
+}
+
+// column pass of the two-level binning with RB-bit column digits
+template <int RB>
+static void column_pass(const Workspace &ws, cudaStream_t st, int grid, int N, int gx, int gy, int tbx,
+                        uint64_t mk) {
+    Counters *cnt = ws.counters;
+    const ColLoader<false, RB> col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
+    launch_count<ColLoader<false, RB>, (1 << RB)>(ws, st, grid, col, CNT_KEYS, mk, 0);
+    launch_pdl(k_col_scan, dim3(gy, gx), 32, 0, st, ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx,
+               ws.tile_cnt);
+    launch_pdl(k_tile_ranges, gy, 512, 0, st, ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
+    if ((int64_t)N < ((int64_t)1 << (32 - RB))) {   // key = tx | index << RB fits one word
+        const ColLoader<true, RB> colp{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
+        col_scatter(ws, st, grid, colp, tbx, mk);
+    } else {
+        col_scatter(ws, st, grid, col, tbx, mk);
     }
 }
 
@@ -1166,7 +1230,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     const int grid_k = std::max(1, std::min(nsm * 8, ceil_div_i(max_keys, SORT_CHUNK)));
     const uint64_t mk = (uint64_t)max_keys;
     const int gy = ntiles / gx;
-    if (!(gx <= 256 && gy <= 256)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
+    if (!(gx <= 512 && gy <= 512)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
     int launches = 0;   // (the two-level path writes every tile range: no memset node)
     // 1. compaction of the visible Gaussians (index order)
     launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[0], ws.sv[0], cnt}, (uint32_t)N);
@@ -1177,7 +1241,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     int tbx = 0, tby = 0;
     while ((1 << tbx) < gx) tbx++;
     while ((1 << tby) < gy) tby++;
-    if (gx <= 256 && gy <= 256) {
+    if (gx <= 512 && gy <= 512) {
         // 3. row entries of the depth-ordered Gaussians
         uint32_t *roff = ws.off, *rowmask_r = ws.sk[1];
         launches += scan_pass(ws, st, grid_n,
@@ -1193,19 +1257,11 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         launches += scan_pass(ws, st, grid_k, PairOffsetsOp{ws.kt[1], ws.kt[0], cnt, mk}, (uint32_t)N);
         launch_pdl(k_keys_on_overflow, nsm, 256, 0, st, ws.sv[0], ws.touched, cnt);
         // 6. row bounds and row-aligned column chunks
-        launch_pdl(k_row_bounds, 1, 256, 0, st, ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
+        launch_pdl(k_row_bounds, 1, 512, 0, st, ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
         launch_pdl(k_chunk_desc, nsm * 2, 256, 0, st, ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
         // 7. columns: counts, per-(row, column) scans, tile ranges, stable scatter of the indices
-        const ColLoader<false> col{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
-        launch_count(ws, st, grid_k, col, CNT_KEYS, mk, 0);
-        launch_pdl(k_col_scan, dim3(gy, gx), 32, 0, st, ws.rowinfo, cnt, ws.cmat, (uint32_t)ws.max_chunks, gx, ws.tile_cnt);
-        launch_pdl(k_tile_ranges, gy, 256, 0, st, ws.rowinfo, ws.tile_cnt, gx, ws.ranges);
-        if (N < (1 << 24)) {
-            const ColLoader<true> colp{ws.kt[0], ws.kt[1], ws.kv[1], ws.cdesc_last, ws.cdesc, ws.ranges, cnt, gx};
-            col_scatter(ws, st, grid_k, colp, tbx, mk);
-        } else {
-            col_scatter(ws, st, grid_k, col, tbx, mk);
-        }
+        if (tbx > 8) column_pass<9>(ws, st, grid_k, N, gx, gy, tbx, mk);
+        else column_pass<8>(ws, st, grid_k, N, gx, gy, tbx, mk);
         return launches + 8;
     }
     // 3. pair offsets in depth order

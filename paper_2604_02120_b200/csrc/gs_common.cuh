@@ -54,11 +54,11 @@ struct Workspace {
     uint4 *cdesc;              // [max_chunks] column chunk: (tile row, first pair, pairs, first entry)
     uint32_t *cdesc_last;      // [max_chunks] last row entry of the chunk
     uint32_t *tile_cnt;        // [tiles] pairs per tile
-    uint32_t *rowinfo;         // [3][257] per tile row: first entry, first pair, first column chunk
+    uint32_t *rowinfo;         // [3][513] per tile row: first entry, first pair, first column chunk
     // reduce-then-scan scratch (4096-element chunks)
     uint32_t *sums;            // [max_chunks] chunk sums of the order-preserving scans
-    uint32_t *cmat;            // [256][max_chunks] per-chunk digit counts -> offsets
-    uint32_t *row_total;       // [256] digit totals
+    uint32_t *cmat;            // [512][max_chunks] per-chunk digit counts -> offsets
+    uint32_t *row_total;       // [512] digit totals
     size_t max_chunks;
     Counters *counters;
     // scene staging for the host-pointer entry point

@@ -223,16 +223,16 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
     const size_t N = (size_t)max_points, K = (size_t)max_keys, T = (size_t)c->max_tiles;
     gs::Workspace &w = c->ws;
-    // + 256: the row-aligned column chunks add at most one partial chunk per tile row
-    w.max_chunks = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1 + 256;
+    // + 512: the row-aligned column chunks add at most one partial chunk per tile row
+    w.max_chunks = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1 + 512;
     cudaError_t e = cudaSuccess;
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
     A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
     A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
     A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
-    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 256); A(w.row_total, 256);
-    A(w.cdesc, w.max_chunks); A(w.cdesc_last, w.max_chunks); A(w.tile_cnt, T); A(w.rowinfo, 3 * 257);
+    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
+    A(w.cdesc, w.max_chunks); A(w.cdesc_last, w.max_chunks); A(w.tile_cnt, T); A(w.rowinfo, 3 * 513);
     A(w.counters, 1);
 #undef A
     if (e == cudaSuccess) e = cudaDeviceSynchronize();

@@ -68,15 +68,16 @@ def _dense():
 
 
 def _wide(W=4200, H=40):
-    """Tile grids beyond 256 columns (or rows): the one-level binning path
-    (all K (tile, index) pairs expanded, ceil(tile bits / 8) stable passes)."""
+    """Wide / tall tile grids: 263 columns take the two-level path with 9-bit
+    column digits; 525 rows (> 512) take the one-level path (all K (tile,
+    index) pairs expanded, ceil(tile bits / 8) stable passes)."""
     scene = synth.object_scene(20000, 107, sh_degree=3)
     cam = synth.look_at((0.0, -0.3, -3.2), (0, 0, 0), W, H, 1.6 if W > H else 0.05)
     return scene, cam, np.array([0.1, 0.2, 0.3], np.float32)
 
 
 CASES = {"C1": lambda: _cfg("C1"), "C2": lambda: _cfg("C2"), "ragged": _ragged, "adversarial": _adversarial,
-         "dense": _dense, "wide": _wide, "tall": lambda: _wide(40, 4200)}
+         "dense": _dense, "wide": _wide, "tall": lambda: _wide(40, 8400)}
 
 
 @pytest.mark.parametrize("case", list(CASES))
