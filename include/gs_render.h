@@ -122,8 +122,12 @@ int gs_render(gs_ctx *ctx, void *stream, int N, const float *means3D, const floa
               float *out_rgb, float *out_T);
 
 /* Renders n_views cameras (host array cams[n_views]) of the same scene into
- * out_rgb [n_views,3,H,W] and out_T [n_views,H,W] (device), back to back on
- * `stream`. Equivalent to n_views gs_render calls. */
+ * out_rgb [n_views,3,H,W] and out_T [n_views,H,W] (device), on `stream`.
+ * Frames are bit-identical to n_views gs_render calls. The views are processed
+ * in groups (gs_set_view_group, default 4): one preprocess launch reads each
+ * Gaussian's record (means, scales, rotation, opacity, SH) from HBM once for
+ * the whole group and writes the group's per-view splats; binning and blending
+ * then run view by view (P:109-117 per view). */
 int gs_render_views(gs_ctx *ctx, void *stream, int N, const float *means3D, const float *scales,
                     const float *rots, const float *opacity, const float *shs_or_colors,
                     const gs_camera *cams, int n_views, int W, int H, const gs_opts *opts,
@@ -132,11 +136,18 @@ int gs_render_views(gs_ctx *ctx, void *stream, int N, const float *means3D, cons
 /* End-to-end variant with HOST buffers (pinned memory recommended): copies the
  * scene host->device, renders n_views, copies the frames device->host and
  * synchronises `stream` before returning. Scene staging uses the context's own
- * device buffers (sized by max_points). */
+ * device buffers (sized by max_points). The frame copies run on a context-owned
+ * second stream, one view group behind the rendering (two staging slots). */
 int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
                          const float *scales, const float *rots, const float *opacity,
                          const float *shs_or_colors, const gs_camera *cams, int n_views,
                          int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
+
+/* Sets the view-group size of gs_render_views / gs_render_views_host (1..4;
+ * 1 = one preprocess launch per view). Output does not depend on it. The first
+ * multi-view call with group g allocates g-1 extra sets of per-Gaussian
+ * preprocess outputs (60 B x max_points each). GS_ERR_INVALID_ARG otherwise. */
+int gs_set_view_group(gs_ctx *ctx, int g);
 
 /* Synchronises the last stream used by ctx and reports counts and the status
  * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */

@@ -35,7 +35,7 @@ GS_FLAG_TIGHT = 8
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
            "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times",
-           "gs_debug_set_trace")
+           "gs_debug_set_trace", "gs_set_view_group")
 
 
 class GsError(RuntimeError):
@@ -91,6 +91,7 @@ def load():
         "gs_debug_exponents": [P, P, I, P, P, P, P, I64, P, I, I, P],
         "gs_stage_times": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
         "gs_debug_set_trace": [P, P],
+        "gs_set_view_group": [P, I],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -198,6 +199,9 @@ class Context:
         _check(self.lib.gs_render_views_host(self.h, _stream(stream), n, _ptr(m), _ptr(s), _ptr(r), _ptr(op),
                                              _ptr(sh), arr, len(cams), W, H, ctypes.byref(o),
                                              _ptr(h_out_rgb), _ptr(h_out_T)), "gs_render_views_host")
+
+    def gs_set_view_group(self, g):
+        _check(self.lib.gs_set_view_group(self.h, int(g)), "gs_set_view_group")
 
     def gs_last_stats(self):
         st = gs_stats()

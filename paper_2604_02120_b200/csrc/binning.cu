@@ -24,6 +24,7 @@
 // block ever waits on another block (a decoupled look-back variant spent
 // most of its time spinning on its predecessors).
 #include <algorithm>
+#include <cstring>
 
 #include "gs_common.cuh"
 
@@ -68,10 +69,11 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
 // ---------------------------------------------------------------------------
 // element counts (device-resident)
 // ---------------------------------------------------------------------------
-enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2, CNT_RENT = 3 };
+enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2, CNT_RENT = 3, CNT_VISIBLE_WIDE = 4 };
 __device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint32_t n_points, uint64_t max_keys) {
     if (which == CNT_POINTS) return n_points;
     if (which == CNT_VISIBLE) return c->n_visible;
+    if (which == CNT_VISIBLE_WIDE) return c->wide_depth ? c->n_visible : 0u;   // 4th depth pass only if needed
     if (which == CNT_RENT) return c->err ? 0u : c->n_rent;   // > max_keys sets err
     const uint64_t k = c->n_keys;
     return c->err ? 0u : (uint32_t)(k < max_keys ? k : max_keys);
@@ -80,54 +82,47 @@ __device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint3
 // ---------------------------------------------------------------------------
 // order-preserving scans (reduce -> scan sums -> apply)
 // ---------------------------------------------------------------------------
-struct CompactOp {   // visible flags -> (depth bits, index) of the visible Gaussians, index order
+// The depth key is stored relative to the near plane: key = bits(z) - bits(znear).
+// Every visible z > znear > 0, so the subtraction keeps the order of the raw bits
+// (R-13), and depths below znear * 2^16 (13107 at znear 0.2) give keys < 2^27:
+// three 9-bit passes sort them; a larger key sets wide_depth and a 4th pass runs.
+struct CompactOp {   // visible flags -> (depth key, index) of the visible Gaussians, index order
     const uint32_t *touched, *depth_bits;
     uint32_t *out_k, *out_v;
     Counters *cnt;
+    uint32_t dbase;   // bits(znear) if znear > 0, else 0 (raw bits, always 4 passes)
     static constexpr int WHICH = CNT_POINTS;
     struct Aux {
         uint32_t depth;
     };
     __device__ uint32_t load(uint32_t i) const { return touched[i] > 0 ? 1u : 0u; }
     __device__ uint32_t load(uint32_t i, Aux &a) const {
-        a.depth = depth_bits[i];
+        a.depth = depth_bits[i];   // unconditional: both loads in flight at once
         return touched[i] > 0 ? 1u : 0u;
     }
     __device__ void emit(uint32_t i, uint64_t pos, uint32_t v, const Aux &a) const {
         if (v) {
-            out_k[pos] = a.depth;
+            const uint32_t k = a.depth - dbase;
+            out_k[pos] = k;
             out_v[pos] = i;
+            if (k >= (1u << 27)) cnt->wide_depth = 1u;
         }
     }
     __device__ void finish(uint64_t total) const { cnt->n_visible = (uint32_t)total; }
 };
 
-struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ gathered rects/masks, chunk heads)
+struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ chunk heads)
     const uint32_t *sorted_idx, *touched;
-    const ushort4 *rect;
-    const unsigned long long *tmask;   // GS_FLAG_TIGHT tile masks (nullptr: whole rects)
     uint32_t *off;
-    ushort4 *rect_r;
-    unsigned long long *tmask_r;
     uint32_t *chunk_first;
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
-    struct Aux {
-        ushort4 rc;
-        unsigned long long m;
-    };
+    struct Aux {};
     __device__ uint32_t load(uint32_t r) const { return touched[sorted_idx[r]]; }
-    __device__ uint32_t load(uint32_t r, Aux &a) const {
-        const uint32_t i = sorted_idx[r];
-        a.rc = rect[i];
-        a.m = tmask ? tmask[i] : ~0ull;
-        return touched[i];
-    }
-    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &a) const {
+    __device__ uint32_t load(uint32_t r, Aux &) const { return touched[sorted_idx[r]]; }
+    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &) const {
         off[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
-        rect_r[r] = a.rc;
-        if (tmask) tmask_r[r] = a.m;
         // every 4096-pair chunk boundary inside [o, o+v) belongs to Gaussian r
         for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
             if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
@@ -247,6 +242,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // bases come from the digit totals (s_dbase). Loaders derive from this unless they
 // define their own chunks (ColLoader).
 struct LinearChunks {
+    __device__ void epilogue(uint32_t, uint32_t) const {}   // per scattered element (g = slot, v = value)
     static constexpr bool PACKED = false;       // key = digit | value << PACK_SHIFT, no separate values
     static constexpr int PACK_SHIFT = 0;
     static constexpr bool EXPANDS = false;      // keys via key(i) from global memory
@@ -261,7 +257,19 @@ struct LinearChunks {
 
 struct PlainLoader : LinearChunks {
     const uint32_t *keys, *vals;
+    // final depth pass: gather each Gaussian's rect (and tile mask) into depth order
+    // as it is scattered, so later passes read them contiguously (nullptr: off)
+    const ushort4 *g_rect = nullptr;
+    ushort4 *g_rect_out = nullptr;
+    const unsigned long long *g_tmask = nullptr;
+    unsigned long long *g_tmask_out = nullptr;
     static constexpr int SCRATCH_WORDS = 0;
+    __device__ void epilogue(uint32_t g, uint32_t v) const {
+        if (g_rect_out) {
+            g_rect_out[g] = g_rect[v];
+            if (g_tmask_out) g_tmask_out[g] = g_tmask[v];
+        }
+    }
     __device__ uint32_t key(uint32_t i) const { return __ldcs(keys + i); }
     __device__ void load(uint32_t, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
         uint32_t k[SORT_ITEMS], v[SORT_ITEMS];   // all loads in flight before the first use
@@ -633,7 +641,9 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3)
                 vout[g] = k >> Loader::PACK_SHIFT;
             } else {
                 if (kout) kout[g] = k;
-                vout[g] = s_ov[p];
+                const uint32_t v = s_ov[p];
+                vout[g] = v;
+                ld.epilogue(g, v);
             }
         }
         __syncthreads();
@@ -695,20 +705,17 @@ __device__ __forceinline__ uint32_t kept_rows(const ushort4 &rc, unsigned long l
     return rows;
 }
 
-struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry offsets (+ rects/masks in depth order)
-    const uint32_t *sorted_idx;
-    const ushort4 *rect;
-    const unsigned long long *tmask;   // GS_FLAG_TIGHT (nullptr: whole rects)
+struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry offsets (+ kept-row masks)
+    const ushort4 *rect_r;                 // rects in depth order (gathered by the last depth pass)
+    const unsigned long long *tmask_r;     // GS_FLAG_TIGHT masks in depth order (nullptr: whole rects)
     uint32_t *roff, *rowmask_r;
-    ushort4 *rect_r;
-    unsigned long long *tmask_r;
     uint32_t *chunk_first;
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
-    struct Aux {};   // emit re-gathers (L1-hot): nothing is held across the scan, for occupancy
+    struct Aux {};   // emit re-reads (L1-hot): nothing is held across the scan, for occupancy
     __device__ uint32_t nrows(const ushort4 &rc, unsigned long long m, uint32_t &rows) const {
-        if (!tmask) {
+        if (!tmask_r) {
             rows = 0xFFFFFFFFu;
             return (uint32_t)(rc.w - rc.y);
         }
@@ -716,21 +723,15 @@ struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry off
         return (uint32_t)(rc.w - rc.y) > 32u ? (uint32_t)(rc.w - rc.y) : (uint32_t)__popc(rows);
     }
     __device__ uint32_t load(uint32_t r) const {
-        const uint32_t i = sorted_idx[r];
         uint32_t rows;
-        return nrows(rect[i], tmask ? tmask[i] : ~0ull, rows);
+        return nrows(rect_r[r], tmask_r ? tmask_r[r] : ~0ull, rows);
     }
     __device__ uint32_t load(uint32_t r, Aux &) const { return load(r); }
     __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &) const {
-        const uint32_t i = sorted_idx[r];
-        const ushort4 rc = rect[i];
         roff[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
-        rect_r[r] = rc;
-        if (tmask) {
-            const unsigned long long m = tmask[i];
+        if (tmask_r) {
             uint32_t rows;
-            nrows(rc, m, rows);
-            tmask_r[r] = m;
+            nrows(rect_r[r], tmask_r[r], rows);
             rowmask_r[r] = rows;
         }
         for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
@@ -921,6 +922,7 @@ struct ColLoader {
     int gx;
     static constexpr bool EXPANDS = true;
     static constexpr int SCRATCH_WORDS = 0;
+    __device__ void epilogue(uint32_t, uint32_t) const {}
     __device__ uint32_t nchunks(uint32_t) const { return cnt->err ? 0u : cnt->n_cchunks; }
     __device__ void chunk(uint32_t c, uint32_t, uint32_t &cbase, uint32_t &cvalid) const {
         const uint4 d = cdesc[c];
@@ -983,6 +985,23 @@ struct ColLoader {
         }
     }
 };
+
+// Wide depth range only (a visible depth key >= 2^27, see CompactOp): the 4th pass
+// left the order in sv[1]; move it back to sv[0] and gather the rects / masks.
+__global__ void __launch_bounds__(256) k_depth_wide_copy(const Counters *cnt, const uint32_t *__restrict__ v_in,
+                                                         uint32_t *__restrict__ v_out, const ushort4 *__restrict__ rect,
+                                                         ushort4 *__restrict__ rect_r,
+                                                         const unsigned long long *__restrict__ tmask,
+                                                         unsigned long long *__restrict__ tmask_r) {
+    pdl_wait();
+    const uint32_t n = count_of(cnt, CNT_VISIBLE_WIDE, 0, 0);
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t v = v_in[r];
+        v_out[r] = v;
+        rect_r[r] = rect[v];
+        if (tmask) tmask_r[r] = tmask[v];
+    }
+}
 
 // Capacity error path: when the row entries alone overflowed max_keys, the pair
 // offsets were not computed; K (= sum of tiles touched) is still reported.
@@ -1221,7 +1240,7 @@ static void column_pass(const Workspace &ws, cudaStream_t st, int grid, int N, i
 }
 
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &,
-                   bool tight) {
+                   bool tight, float znear) {
     Counters *cnt = ws.counters;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -1232,12 +1251,31 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     const int gy = ntiles / gx;
     if (!(gx <= 512 && gy <= 512)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
     int launches = 0;   // (the two-level path writes every tile range: no memset node)
-    // 1. compaction of the visible Gaussians (index order)
-    launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[0], ws.sv[0], cnt}, (uint32_t)N);
-    // 2. depth sort: 4 stable passes of 8 bits; the result is back in sk[0]/sv[0]
-    for (int p = 0; p < 4; p++)
-        launches += radix_pass(ws, st, grid_n, PlainLoader{{}, ws.sk[p & 1], ws.sv[p & 1]}, ws.sk[(p + 1) & 1],
-                               ws.sv[(p + 1) & 1], CNT_VISIBLE, mk, 8 * p);
+    // 1. compaction of the visible Gaussians (index order), keys relative to the near plane
+    uint32_t dbase = 0;
+    if (znear > 0.f) memcpy(&dbase, &znear, 4);
+    launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[1], ws.sv[1], cnt, dbase},
+                          (uint32_t)N);
+    // 2. depth sort: 3 stable passes of 9 bits (sk/sv 1 -> 0 -> 1 -> 0); the last one also
+    //    gathers each Gaussian's rect (and tile mask) into depth order. Keys >= 2^27 (a
+    //    visible depth beyond znear * 2^16) take a 4th pass on bits 27-31 and a copy back;
+    //    both launches are no-ops otherwise (device-side count, no host sync).
+    const unsigned long long *tm = tight ? ws.tmask : nullptr;
+    for (int p = 0; p < 3; p++) {
+        PlainLoader ld{{}, ws.sk[(p + 1) & 1], ws.sv[(p + 1) & 1]};
+        if (p == 2) {
+            ld.g_rect = ws.rect;
+            ld.g_rect_out = ws.rect_r;
+            ld.g_tmask = tm;
+            ld.g_tmask_out = tm ? ws.tmask_r : nullptr;
+        }
+        launches += radix_pass(ws, st, grid_n, ld, ws.sk[p & 1], ws.sv[p & 1], CNT_VISIBLE, mk, 9 * p, 9);
+    }
+    launches += radix_pass(ws, st, grid_n, PlainLoader{{}, ws.sk[0], ws.sv[0]}, ws.sk[1], ws.sv[1], CNT_VISIBLE_WIDE,
+                           mk, 27, 5);
+    launch_pdl(k_depth_wide_copy, nsm * 2, 256, 0, st, (const Counters *)cnt, (const uint32_t *)ws.sv[1], ws.sv[0],
+               (const ushort4 *)ws.rect, ws.rect_r, tm, ws.tmask_r);
+    launches++;
     int tbx = 0, tby = 0;
     while ((1 << tbx) < gx) tbx++;
     while ((1 << tby) < gy) tby++;
@@ -1245,8 +1283,8 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
         // 3. row entries of the depth-ordered Gaussians
         uint32_t *roff = ws.off, *rowmask_r = ws.sk[1];
         launches += scan_pass(ws, st, grid_n,
-                              RowOffsetsOp{ws.sv[0], ws.rect, tight ? ws.tmask : nullptr, roff, rowmask_r, ws.rect_r,
-                                           ws.tmask_r, ws.chunk_first, cnt, mk},
+                              RowOffsetsOp{ws.rect_r, tight ? ws.tmask_r : nullptr, roff, rowmask_r, ws.chunk_first,
+                                           cnt, mk},
                               (uint32_t)N);
         // 4. rows: one stable pass on ty -> entries (ty | x0 << 8 | width << 16, index) in kt[1] / kv[1]
         launches += radix_pass(ws, st, grid_k,
@@ -1266,8 +1304,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     }
     // 3. pair offsets in depth order
     launches += scan_pass(ws, st, grid_n,
-                          OffsetsOp{ws.sv[0], ws.touched, ws.rect, tight ? ws.tmask : nullptr, ws.off, ws.rect_r,
-                                    ws.tmask_r, ws.chunk_first, cnt, mk},
+                          OffsetsOp{ws.sv[0], ws.touched, ws.off, ws.chunk_first, cnt, mk},
                           (uint32_t)N);
     // 4. tile sort with the expansion fused into the first pass; final order in kt[0]/kv[0]
     int tbits = 0;

@@ -21,7 +21,7 @@ struct Counters {
     uint32_t tile_queue;       // blend persistent work queue
     uint32_t n_rent;           // row entries (two-level binning): kept tile rows summed over Gaussians
     uint32_t n_cchunks;        // column-pass chunks (row-aligned, <= 4096 pairs each)
-    uint32_t pad;
+    uint32_t wide_depth;       // some visible depth key >= 2^27 above the near plane: 4th depth pass
     unsigned long long pairs_eval;   // GS_FLAG_STATS: exponents computed by the blend
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
@@ -64,6 +64,25 @@ struct Workspace {
     // scene staging for the host-pointer entry point
     float *stage;
     size_t stage_bytes;
+};
+
+// ---- per-view outputs of the preprocess (a view group shares one scene read) ----
+struct PreOut {
+    uint32_t *depth_bits;
+    float2 *xy;
+    float4 *conic_o;
+    float4 *rgb;
+    ushort4 *rect;
+    uint32_t *touched;
+    unsigned long long *tmask;
+    int32_t *radius;           // nullptr: not written (debug output only)
+    Counters *counters;        // zeroed by the preprocess
+};
+constexpr int MAX_VIEW_GROUP = 4;
+struct PreViews {
+    gs_camera cam[MAX_VIEW_GROUP];
+    PreOut out[MAX_VIEW_GROUP];
+    int n;
 };
 
 // Chunk geometry of the single-pass scans / onesweep radix passes.
@@ -264,9 +283,14 @@ constexpr float ALPHA_MAX = 0.99f; // alpha cap (R-4)
 namespace gs {
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight);
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight,
+                       bool with_radius);
+PreOut pre_out_of(const Workspace &ws, bool with_radius);
+void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const float *means, const float *scales,
+                             const float *rots, const float *opacity, const float *shs, int sh_degree,
+                             int sh_stride, float scale_mod, int W, int H, bool tight);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
-                   uint32_t &epoch, bool tight);
+                   uint32_t &epoch, bool tight, float znear);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,

@@ -23,14 +23,24 @@ struct gs_ctx {
     int last_status = GS_OK;
     float *frame_rgb = nullptr, *frame_T = nullptr;   // staging for the host entry point
     int64_t launches = 0;                             // kernels launched (gs_stats.launches)
-    // GS_FLAG_TIMING: a pool of 4 events per frame, drained by gs_stage_times
+    // GS_FLAG_TIMING: a pool of events and (stage, start, end) spans, drained by gs_stage_times
     std::vector<cudaEvent_t> ev;
     int ev_used = 0;
+    struct Span { int stage, e0, e1; };
+    std::vector<Span> spans;
     double stage_ms[3] = {0, 0, 0};
     int64_t timed_frames = 0;
+    // view groups (gs_render_views): per-view preprocess outputs + counters of views 1..G-1
+    int view_group = gs::MAX_VIEW_GROUP;
+    gs::Workspace vws[gs::MAX_VIEW_GROUP] = {};
+    bool vws_alloc[gs::MAX_VIEW_GROUP] = {};
+    gs::Counters *last_counters = nullptr;   // counters of the last rendered view
+    // gs_render_views_host: device -> host frame copies overlap the next view group
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t group_done[2] = {}, copies_done[2] = {};
 };
 
-static constexpr int kEventFrames = 256;
+static constexpr int kMaxEvents = 4096;
 
 namespace {
 
@@ -61,54 +71,93 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
     return GS_OK;
 }
 
-// preprocess + binning of one view into the workspace (counters zeroed first)
 void drain_events(gs_ctx *c) {
-    for (int f = 0; f < c->ev_used; f++) {
-        cudaEventSynchronize(c->ev[4 * f + 3]);
-        for (int k = 0; k < 3; k++) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, c->ev[4 * f + k], c->ev[4 * f + k + 1]);
-            c->stage_ms[k] += ms;
-        }
+    if (c->ev_used > 0) cudaEventSynchronize(c->ev[c->ev_used - 1]);
+    for (const auto &sp : c->spans) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev[sp.e0], c->ev[sp.e1]);
+        c->stage_ms[sp.stage] += ms;
     }
-    c->timed_frames += c->ev_used;
+    c->spans.clear();
     c->ev_used = 0;
 }
 
-void mark(gs_ctx *c, cudaStream_t st, const gs_opts &o, int k) {
-    if (!(o.flags & GS_FLAG_TIMING)) return;
+// GS_FLAG_TIMING: records an event on st, returns its pool index (-1 when timing is off)
+int mark(gs_ctx *c, cudaStream_t st, const gs_opts &o) {
+    if (!(o.flags & GS_FLAG_TIMING)) return -1;
     if (c->ev.empty()) {
-        c->ev.resize(4 * kEventFrames);
+        c->ev.resize(kMaxEvents);
         for (auto &e : c->ev) cudaEventCreate(&e);
     }
-    if (k == 0 && c->ev_used == kEventFrames) drain_events(c);
-    cudaEventRecord(c->ev[4 * c->ev_used + k], st);
-    if (k == 3) c->ev_used++;
+    if (c->ev_used == kMaxEvents) drain_events(c);   // only between spans (see callers)
+    cudaEventRecord(c->ev[c->ev_used], st);
+    return c->ev_used++;
+}
+void span(gs_ctx *c, int stage, int e0, int e1) {
+    if (e0 >= 0 && e1 > e0) c->spans.push_back({stage, e0, e1});
 }
 
-void enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
-                   const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
-    mark(c, st, o, 0);
-    if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
-    const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
-    gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                          o.scale_modifier, cam, W, H, tight);
-    c->launches += N > 0 ? 1 : 0;
-    mark(c, st, o, 1);
+// the workspace of view slot v of a group: slot 0 is the context's own; slots 1..G-1
+// get their own preprocess outputs and counters and share every binning buffer
+int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
+    if (v == 0) {
+        *out = &c->ws;
+        return GS_OK;
+    }
+    gs::Workspace &w = c->vws[v];
+    if (!c->vws_alloc[v]) {
+        const size_t N = (size_t)c->max_points;
+        w = c->ws;
+        w.depth_bits = nullptr; w.xy = nullptr; w.conic_o = nullptr; w.rgb = nullptr; w.rect = nullptr;
+        w.touched = nullptr; w.tmask = nullptr; w.counters = nullptr;
+        cudaError_t e = cudaSuccess;
+#define A(ptr, n) \
+    if (e == cudaSuccess) e = alloc(ptr, n)
+        A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
+        A(w.tmask, N); A(w.counters, 1);
+#undef A
+        if (e == cudaSuccess) e = cudaMemset(w.counters, 0, sizeof(gs::Counters));
+        c->vws_alloc[v] = true;   // (partially allocated pointers are freed by gs_ctx_destroy)
+        if (int rc = check_cuda(e)) return rc;
+    }
+    *out = &w;
+    return GS_OK;
+}
+
+// binning of one preprocessed view (its workspace) on st
+void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const gs_camera &cam, int W, int H,
+                     const gs_opts &o) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
-    c->launches += gs::launch_binning(c->ws, st, N, c->max_keys, gx * gy, gx, c->epoch, tight);
-    mark(c, st, o, 2);
+    c->launches += gs::launch_binning(w, st, N, c->max_keys, gx * gy, gx, c->epoch, (o.flags & GS_FLAG_TIGHT) != 0,
+                                      cam.znear);
 }
 
-void enqueue_blend(gs_ctx *c, cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                   const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o, float *out_rgb,
-                   float *out_T, float *dump) {
+// preprocess + binning of one view into the context's workspace (counters zeroed first)
+int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
+                  const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
+    const int e0 = mark(c, st, o);
+    if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
+    gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
+                          o.scale_modifier, cam, W, H, (o.flags & GS_FLAG_TIGHT) != 0, false);
+    c->launches += N > 0 ? 1 : 0;
+    const int e1 = mark(c, st, o);
+    enqueue_binning(c, c->ws, st, N, cam, W, H, o);
+    const int e2 = mark(c, st, o);
+    span(c, 0, e0, e1);
+    span(c, 1, e1, e2);
+    c->last_counters = c->ws.counters;
+    return e2;
+}
+
+void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const float2 *xy, const float4 *conic_o,
+                   const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o,
+                   float *out_rgb, float *out_T, float *dump) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     if (o.blend == GS_BLEND_DIRECT && !dump)
         gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
-                                c->ws.counters);
+                                w.counters);
     else
-        gs::launch_blend_tc(c->ws, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_tc(w, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
                             dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
     c->launches += 1;
 }
@@ -255,7 +304,19 @@ int gs_ctx_destroy(gs_ctx *c) {
                     w.counters, w.stage, c->frame_rgb, c->frame_T};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (int v = 1; v < gs::MAX_VIEW_GROUP; v++) {
+        if (!c->vws_alloc[v]) continue;
+        gs::Workspace &x = c->vws[v];
+        void *vp[] = {x.depth_bits, x.xy, x.conic_o, x.rgb, x.rect, x.touched, x.tmask, x.counters};
+        for (void *p : vp)
+            if (p) cudaFree(p);
+    }
     for (auto &e : c->ev) cudaEventDestroy(e);
+    for (int k = 0; k < 2; k++) {
+        if (c->group_done[k]) cudaEventDestroy(c->group_done[k]);
+        if (c->copies_done[k]) cudaEventDestroy(c->copies_done[k]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
     return GS_OK;
 }
@@ -268,26 +329,79 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     if (!out_rgb || !out_T) return GS_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
-    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb, out_T,
-                  nullptr);
-    mark(c, st, *o, 3);
+    const int e2 = enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
+    enqueue_blend(c, c->ws, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb,
+                  out_T, nullptr);
+    const int e3 = mark(c, st, *o);
+    span(c, 2, e2, e3);
+    if (e3 >= 0) c->timed_frames++;
     return finish(c, st, *o, N);
+}
+
+// n views of one scene in groups of view_group: one preprocess launch reads the scene
+// once per group (k_preprocess), then each view is binned and blended in turn (the
+// binning buffers are shared, the per-view preprocess outputs are not).
+static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *means3D, const float *scales,
+                             const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
+                             int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of) {
+    const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
+    const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
+    for (int v0 = 0; v0 < n_views; v0 += G) {
+        const int n = std::min(G, n_views - v0);
+        gs::PreViews pv{};
+        pv.n = n;
+        gs::Workspace *w[gs::MAX_VIEW_GROUP];
+        for (int j = 0; j < n; j++) {
+            if (int rc = view_ws(c, j, &w[j])) return rc;
+            pv.cam[j] = cams[v0 + j];
+            pv.out[j] = gs::pre_out_of(*w[j], false);
+        }
+        const int e0 = mark(c, st, o);
+        if (N == 0)
+            for (int j = 0; j < n; j++) cudaMemsetAsync(w[j]->counters, 0, sizeof(gs::Counters), st);
+        gs::launch_preprocess_views(pv, st, N, means3D, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
+                                    o.scale_modifier, W, H, tight);
+        c->launches += N > 0 ? 1 : 0;
+        int e_prev = mark(c, st, o);
+        span(c, 0, e0, e_prev);
+        for (int j = 0; j < n; j++) {
+            enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
+            const int e1 = mark(c, st, o);
+            enqueue_blend(c, *w[j], st, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H, o,
+                          rgb_of[v0 + j], T_of[v0 + j], nullptr);
+            const int e2 = mark(c, st, o);
+            span(c, 1, e_prev, e1);
+            span(c, 2, e1, e2);
+            e_prev = e2;
+            if (e2 >= 0) c->timed_frames++;
+            c->last_counters = w[j]->counters;
+        }
+    }
+    return GS_OK;
 }
 
 int gs_render_views(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales, const float *rots,
                     const float *opacity, const float *shs, const gs_camera *cams, int n_views, int W, int H,
                     const gs_opts *o, float *out_rgb, float *out_T) {
     if (!cams || n_views < 0) return GS_ERR_INVALID_ARG;
-    const size_t plane = (size_t)W * H;
+    if (n_views == 0) return GS_OK;
     for (int v = 0; v < n_views; v++) {
-        gs_opts ov = *o;
-        ov.flags &= ~GS_FLAG_SYNC;
-        int rc = gs_render(c, stream, N, means3D, scales, rots, opacity, shs, &cams[v], W, H, &ov,
-                           out_rgb + (size_t)v * 3 * plane, out_T + (size_t)v * plane);
+        int rc = validate(c, N, means3D, scales, rots, opacity, shs, &cams[v], W, H, o);
         if (rc) return rc;
     }
-    return finish(c, reinterpret_cast<cudaStream_t>(stream), *o, N);
+    if (!out_rgb || !out_T) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    const size_t plane = (size_t)W * H;
+    std::vector<float *> prgb(n_views), pT(n_views);
+    for (int v = 0; v < n_views; v++) {
+        prgb[v] = out_rgb + (size_t)v * 3 * plane;
+        pT[v] = out_T + (size_t)v * plane;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc = render_views_impl(c, st, N, means3D, scales, rots, opacity, shs, cams, n_views, W, H, *o,
+                                   prgb.data(), pT.data()))
+        return rc;
+    return finish(c, st, *o, N);
 }
 
 int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
@@ -309,35 +423,64 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
         if (check_cuda(cudaMalloc(&c->ws.stage, total * sizeof(float)))) return GS_ERR_CUDA;
         c->ws.stage_bytes = total * sizeof(float);
     }
-    if (!c->frame_rgb) {
-        const size_t plane = (size_t)c->max_w * c->max_h;
-        if (check_cuda(cudaMalloc(&c->frame_rgb, 2 * 3 * plane * sizeof(float)))) return GS_ERR_CUDA;
-        if (check_cuda(cudaMalloc(&c->frame_T, 2 * plane * sizeof(float)))) return GS_ERR_CUDA;
+    if (!c->frame_rgb) {   // 2 staging slots of MAX_VIEW_GROUP frames, a copy stream and its events
+        const size_t fr = 2 * gs::MAX_VIEW_GROUP * (size_t)c->max_w * c->max_h;
+        if (check_cuda(cudaMalloc(&c->frame_rgb, 3 * fr * sizeof(float)))) return GS_ERR_CUDA;
+        if (check_cuda(cudaMalloc(&c->frame_T, fr * sizeof(float)))) return GS_ERR_CUDA;
+        if (check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking))) return GS_ERR_CUDA;
+        for (int k = 0; k < 2; k++) {
+            cudaEventCreateWithFlags(&c->group_done[k], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&c->copies_done[k], cudaEventDisableTiming);
+        }
     }
     float *d = c->ws.stage;
     float *dm = d, *ds = dm + pad4(f_means), *dr = ds + pad4(f_scales), *dop = dr + pad4(f_rots),
           *dsh = dop + pad4(f_op);
+    for (int v = 0; v < n_views; v++)
+        if (int rc = validate(c, N, dm, ds, dr, dop, dsh, &cams[v], W, H, o)) return rc;
+    if (!h_out_rgb || !h_out_T) return GS_ERR_INVALID_ARG;
     cudaMemcpyAsync(dm, means3D, f_means * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(ds, scales, f_scales * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, st);
-    const size_t plane = (size_t)W * H;
+    // Frames come back on a second stream, one view group behind: group g renders into
+    // staging slot g % 2 while the frames of group g - 1 are copied device -> host.
+    const size_t plane = (size_t)W * H, mplane = (size_t)c->max_w * c->max_h;
+    const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     gs_opts ov = *o;
     ov.flags &= ~GS_FLAG_SYNC;
-    for (int v = 0; v < n_views; v++) {
-        float *frgb = c->frame_rgb + (size_t)(v & 1) * 3 * (size_t)c->max_w * c->max_h;
-        float *fT = c->frame_T + (size_t)(v & 1) * (size_t)c->max_w * c->max_h;
-        int rc = gs_render(c, st, N, dm, ds, dr, dop, dsh, &cams[v], W, H, &ov, frgb, fT);
-        if (rc) return rc;
-        cudaMemcpyAsync(h_out_rgb + (size_t)v * 3 * plane, frgb, 3 * plane * 4, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(h_out_T + (size_t)v * plane, fT, plane * 4, cudaMemcpyDeviceToHost, st);
+    for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
+        const int n = std::min(G, n_views - v0), slot = g & 1;
+        if (g >= 2) cudaStreamWaitEvent(st, c->copies_done[slot], 0);   // staging slot free again
+        float *prgb[gs::MAX_VIEW_GROUP], *pT[gs::MAX_VIEW_GROUP];
+        for (int j = 0; j < n; j++) {
+            prgb[j] = c->frame_rgb + (size_t)(slot * gs::MAX_VIEW_GROUP + j) * 3 * mplane;
+            pT[j] = c->frame_T + (size_t)(slot * gs::MAX_VIEW_GROUP + j) * mplane;
+        }
+        if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams + v0, n, W, H, ov, prgb, pT)) return rc;
+        cudaEventRecord(c->group_done[slot], st);
+        cudaStreamWaitEvent(c->copy_stream, c->group_done[slot], 0);
+        for (int j = 0; j < n; j++) {
+            cudaMemcpyAsync(h_out_rgb + (size_t)(v0 + j) * 3 * plane, prgb[j], 3 * plane * 4, cudaMemcpyDeviceToHost,
+                            c->copy_stream);
+            cudaMemcpyAsync(h_out_T + (size_t)(v0 + j) * plane, pT[j], plane * 4, cudaMemcpyDeviceToHost,
+                            c->copy_stream);
+        }
+        cudaEventRecord(c->copies_done[slot], c->copy_stream);
     }
-    int rc = check_cuda(cudaStreamSynchronize(st));
+    int rc = check_cuda(cudaStreamSynchronize(c->copy_stream));
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st));
     if (rc) return rc;
     gs_opts os = *o;
     os.flags |= GS_FLAG_SYNC;
     return finish(c, st, os, N);
+}
+
+int gs_set_view_group(gs_ctx *c, int g) {
+    if (!c || g < 1 || g > gs::MAX_VIEW_GROUP) return GS_ERR_INVALID_ARG;
+    c->view_group = g;
+    return GS_OK;
 }
 
 int gs_last_stats(gs_ctx *c, gs_stats *out) {
@@ -345,7 +488,8 @@ int gs_last_stats(gs_ctx *c, gs_stats *out) {
     cudaSetDevice(c->device);
     if (check_cuda(cudaStreamSynchronize(c->last_stream))) return GS_ERR_CUDA;
     gs::Counters h;
-    if (check_cuda(cudaMemcpy(&h, c->ws.counters, sizeof(h), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
+    const gs::Counters *src = c->last_counters ? c->last_counters : c->ws.counters;
+    if (check_cuda(cudaMemcpy(&h, src, sizeof(h), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
     out->n_points = c->last_n;
     out->n_visible = h.n_visible;
     out->n_keys = (int64_t)h.n_keys;
@@ -380,7 +524,8 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     gs::launch_preprocess(c->ws, st, N, means3D, scales, rots, opacity, shs, o->sh_degree, o->sh_stride,
-                          o->scale_modifier, *cam, W, H, (o->flags & GS_FLAG_TIGHT) != 0);
+                          o->scale_modifier, *cam, W, H, (o->flags & GS_FLAG_TIGHT) != 0, true);
+    c->last_counters = c->ws.counters;
     if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
     return finish(c, st, *o, N);
 }
@@ -423,7 +568,8 @@ static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, c
                                                               c->ws.rgb);
         c->launches++;
     }
-    enqueue_blend(c, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
+    c->last_counters = c->ws.counters;
+    enqueue_blend(c, c->ws, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
                   *o, out_rgb, out_T, dump);
     return finish(c, st, *o, N);
 }

@@ -73,200 +73,247 @@ __device__ __forceinline__ bool tight_rect(float mx, float my, float A, float B,
     return n != 0;
 }
 
-__global__ void __launch_bounds__(PRE_THREADS, 3) k_preprocess(int N, const float *__restrict__ means,
+// Steps 2-4 (view-independent): quaternion normalisation, rotation matrix, 3D covariance.
+__device__ __forceinline__ void cov3d(const float4 &q, float s0, float s1, float s2, float scale_mod, float (&S)[3][3]) {
+    // 2. quaternion normalisation
+    const float n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
+    const float nr = sqrtf(n2);
+    const float w = q.x / nr, x = q.y / nr, y = q.z / nr, z = q.w / nr;
+    // 3. rotation matrix
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+    const float wx = w * x, wy = w * y, wz = w * z;
+    float M[3][3];
+    M[0][0] = 1.0f - 2.0f * (yy + zz); M[0][1] = 2.0f * (xy - wz); M[0][2] = 2.0f * (xz + wy);
+    M[1][0] = 2.0f * (xy + wz); M[1][1] = 1.0f - 2.0f * (xx + zz); M[1][2] = 2.0f * (yz - wx);
+    M[2][0] = 2.0f * (xz - wy); M[2][1] = 2.0f * (yz + wx); M[2][2] = 1.0f - 2.0f * (xx + yy);
+    // 4. 3D covariance
+    float v[3];
+    const float sc[3] = {s0, s1, s2};
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        const float g = scale_mod * sc[k];
+        v[k] = g * g;
+    }
+    float u[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int k = 0; k < 3; k++) u[a][k] = M[a][k] * v[k];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = a; b < 3; b++) {
+            S[a][b] = (u[a][0] * M[b][0] + u[a][1] * M[b][1]) + u[a][2] * M[b][2];
+            S[b][a] = S[a][b];
+        }
+}
+
+// Step 11: SH colour for the view direction normalize(p - campos).
+__device__ __forceinline__ void sh_colour(const float (&k)[48], int sh_degree, float px, float py, float pz,
+                                          const gs_camera &cam, float (&res3)[3]) {
+    const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
+    const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+    const float X = dx / len, Y = dy / len, Z = dz / len;
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+                C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+    const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+                C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+                C36 = -0.5900435899266435f;
+#pragma unroll
+    for (int ch = 0; ch < 3; ch++) {
+#define SHK(j) k[(j) * 3 + ch]
+        float res = C0 * SHK(0);
+        if (sh_degree >= 1) res = ((res - (C1 * Y) * SHK(1)) + (C1 * Z) * SHK(2)) - (C1 * X) * SHK(3);
+        if (sh_degree >= 2) {
+            const float XX = X * X, YY = Y * Y, ZZ = Z * Z, XY = X * Y, YZ = Y * Z, XZ = X * Z;
+            res = res + (C20 * XY) * SHK(4);
+            res = res + (C21 * YZ) * SHK(5);
+            res = res + (C22 * (((2.0f * ZZ) - XX) - YY)) * SHK(6);
+            res = res + (C23 * XZ) * SHK(7);
+            res = res + (C24 * (XX - YY)) * SHK(8);
+            if (sh_degree >= 3) {
+                res = res + ((C30 * Y) * ((3.0f * XX) - YY)) * SHK(9);
+                res = res + ((C31 * XY) * Z) * SHK(10);
+                res = res + ((C32 * Y) * (((4.0f * ZZ) - XX) - YY)) * SHK(11);
+                res = res + ((C33 * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))) * SHK(12);
+                res = res + ((C34 * X) * (((4.0f * ZZ) - XX) - YY)) * SHK(13);
+                res = res + ((C35 * Z) * (XX - YY)) * SHK(14);
+                res = res + ((C36 * X) * (XX - (3.0f * YY))) * SHK(15);
+            }
+        }
+#undef SHK
+        res3[ch] = fmaxf(res + 0.5f, 0.0f);
+    }
+}
+
+// One thread per Gaussian, pv.n views (1..MAX_VIEW_GROUP) of the same scene: the scene
+// record (means, scales, rotation, opacity and the SH coefficients, up to 236 B) is read
+// from HBM once and projected for every view of the group, so an orbit's dominant
+// preprocess traffic is paid once per group instead of once per view. Per view the
+// operation order is the one of docs/preprocess_order.md (outputs bit-identical to a
+// single-view launch: the view-independent steps 2-4 are the same operations).
+__global__ void __launch_bounds__(PRE_THREADS, 2) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
                                                                const float4 *__restrict__ rots,
                                                                const float *__restrict__ opacity,
                                                                const float *__restrict__ shs, int sh_degree,
                                                                int sh_stride, float scale_mod, int W, int H,
-                                                               const gs_camera cam, Workspace ws, bool tight) {
+                                                               const PreViews pv, bool tight) {
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0) *ws.counters = Counters{};   // the frame's device counters (no memset node: keeps PDL chained)
+    if (i == 0)   // the frames' device counters (no memset node: keeps PDL chained)
+        for (int v = 0; v < pv.n; v++) *pv.out[v].counters = Counters{};
     if (i >= N) return;
-    const float *R = cam.R;
     const int gx = (W + GS_TILE - 1) / GS_TILE, gy = (H + GS_TILE - 1) / GS_TILE;
 
     const float px = __ldcs(means + 3 * i), py = __ldcs(means + 3 * i + 1), pz = __ldcs(means + 3 * i + 2);
     const float4 q = __ldcs(rots + i);
     const float s0 = __ldcs(scales + 3 * i), s1 = __ldcs(scales + 3 * i + 1), s2 = __ldcs(scales + 3 * i + 2);
     const float op = __ldcs(opacity + i);
+    float S[3][3];
+    bool have_cov = false, have_sh = false;
+    float k[48];
 
-    bool vis = false;
-    float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f;
-    int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
-    // 1. view-space point
-    const float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam.t[0];
-    const float vy = ((R[3] * px + R[4] * py) + R[5] * pz) + cam.t[1];
-    const float vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam.t[2];
-    if (vz > cam.znear) {
-        // 2. quaternion normalisation
-        const float n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
-        const float nr = sqrtf(n2);
-        const float w = q.x / nr, x = q.y / nr, y = q.z / nr, z = q.w / nr;
-        // 3. rotation matrix
-        const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
-        const float wx = w * x, wy = w * y, wz = w * z;
-        float M[3][3];
-        M[0][0] = 1.0f - 2.0f * (yy + zz); M[0][1] = 2.0f * (xy - wz); M[0][2] = 2.0f * (xz + wy);
-        M[1][0] = 2.0f * (xy + wz); M[1][1] = 1.0f - 2.0f * (xx + zz); M[1][2] = 2.0f * (yz - wx);
-        M[2][0] = 2.0f * (xz - wy); M[2][1] = 2.0f * (yz + wx); M[2][2] = 1.0f - 2.0f * (xx + yy);
-        // 4. 3D covariance
-        float v[3];
-        const float sc[3] = {s0, s1, s2};
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-            const float g = scale_mod * sc[k];
-            v[k] = g * g;
-        }
-        float u[3][3], S[3][3];
-#pragma unroll
-        for (int a = 0; a < 3; a++)
-#pragma unroll
-            for (int k = 0; k < 3; k++) u[a][k] = M[a][k] * v[k];
-#pragma unroll
-        for (int a = 0; a < 3; a++)
-#pragma unroll
-            for (int b = a; b < 3; b++) {
-                S[a][b] = (u[a][0] * M[b][0] + u[a][1] * M[b][1]) + u[a][2] * M[b][2];
-                S[b][a] = S[a][b];
+#pragma unroll 1
+    for (int view = 0; view < pv.n; view++) {
+        const gs_camera &cam = pv.cam[view];
+        const PreOut &out = pv.out[view];
+        const float *R = cam.R;
+        bool vis = false;
+        float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f;
+        int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
+        // 1. view-space point
+        const float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam.t[0];
+        const float vy = ((R[3] * px + R[4] * py) + R[5] * pz) + cam.t[1];
+        const float vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam.t[2];
+        if (vz > cam.znear) {
+            if (!have_cov) {   // 2-4, once per Gaussian
+                cov3d(q, s0, s1, s2, scale_mod, S);
+                have_cov = true;
             }
-        // 5. clamped Jacobian
-        const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
-        const float ux = vx / vz, uy = vy / vz;
-        const float cxz = fminf(lx, fmaxf(-lx, ux));
-        const float cyz = fminf(ly, fmaxf(-ly, uy));
-        const float j00 = cam.fx / vz, j02 = -((cam.fx * cxz) / vz);
-        const float j11 = cam.fy / vz, j12 = -((cam.fy * cyz) / vz);
-        // 6. EWA 2D covariance, T = J R
-        float T[2][3], U[2][3];
+            // 5. clamped Jacobian
+            const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
+            const float ux = vx / vz, uy = vy / vz;
+            const float cxz = fminf(lx, fmaxf(-lx, ux));
+            const float cyz = fminf(ly, fmaxf(-ly, uy));
+            const float j00 = cam.fx / vz, j02 = -((cam.fx * cxz) / vz);
+            const float j11 = cam.fy / vz, j12 = -((cam.fy * cyz) / vz);
+            // 6. EWA 2D covariance, T = J R
+            float T[2][3], U[2][3];
 #pragma unroll
-        for (int k = 0; k < 3; k++) {
-            T[0][k] = j00 * R[0 + k] + j02 * R[6 + k];
-            T[1][k] = j11 * R[3 + k] + j12 * R[6 + k];
-        }
-#pragma unroll
-        for (int a = 0; a < 2; a++)
-#pragma unroll
-            for (int k = 0; k < 3; k++) U[a][k] = (T[a][0] * S[0][k] + T[a][1] * S[1][k]) + T[a][2] * S[2][k];
-        const float c00 = (U[0][0] * T[0][0] + U[0][1] * T[0][1]) + U[0][2] * T[0][2];
-        const float c01 = (U[0][0] * T[1][0] + U[0][1] * T[1][1]) + U[0][2] * T[1][2];
-        const float c11 = (U[1][0] * T[1][0] + U[1][1] * T[1][1]) + U[1][2] * T[1][2];
-        const float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
-        // 7. conic
-        const float det = a * c - b * b;
-        if (det > 0.0f) {
-            cA = c / det; cB = -(b / det); cC = a / det;
-            sxx = a; sxy = b; syy = c;
-            // 8. radius
-            const float mid = 0.5f * (a + c);
-            const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
-            r = (int)ceilf(3.0f * sqrtf(lam));
-            // 9. projected mean
-            mx = cam.fx * ux + cam.cx;
-            my = cam.fy * uy + cam.cy;
-            // 10. tile rectangle
-            const float rf = (float)r;
-            xmin = rect_bound((mx - rf) / 16.0f, gx);
-            xmax = rect_bound(((mx + rf) + 15.0f) / 16.0f, gx);
-            ymin = rect_bound((my - rf) / 16.0f, gy);
-            ymax = rect_bound(((my + rf) + 15.0f) / 16.0f, gy);
-            vis = (xmax - xmin) * (ymax - ymin) != 0;
-        }
-    }
-    uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
-    if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
-        unsigned long long m = 0ull;
-        vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, m, n_tiles);
-        ws.tmask[i] = m;
-    }
-    if (!vis) {
-        ws.depth_bits[i] = 0u;
-        ws.xy[i] = make_float2(0.f, 0.f);
-        ws.conic_o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ws.rgb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        ws.rect[i] = make_ushort4(0, 0, 0, 0);
-        ws.touched[i] = 0u;
-        ws.radius[i] = 0;
-        return;
-    }
-    // 11. colour
-    float col0, col1, col2;
-    if (sh_degree < 0) {
-        col0 = shs[3 * (size_t)i]; col1 = shs[3 * (size_t)i + 1]; col2 = shs[3 * (size_t)i + 2];
-    } else {
-        const int ncoef = (sh_degree + 1) * (sh_degree + 1);
-        const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
-        float k[48];
-        if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
-            const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
-#pragma unroll
-            for (int j = 0; j < 12; j++) {
-                if (4 * j < ncoef * 3) {
-                    const float4 t4 = __ldcs(sh4 + j);
-                    k[4 * j] = t4.x; k[4 * j + 1] = t4.y; k[4 * j + 2] = t4.z; k[4 * j + 3] = t4.w;
-                }
+            for (int kk = 0; kk < 3; kk++) {
+                T[0][kk] = j00 * R[0 + kk] + j02 * R[6 + kk];
+                T[1][kk] = j11 * R[3 + kk] + j12 * R[6 + kk];
             }
+#pragma unroll
+            for (int a = 0; a < 2; a++)
+#pragma unroll
+                for (int kk = 0; kk < 3; kk++)
+                    U[a][kk] = (T[a][0] * S[0][kk] + T[a][1] * S[1][kk]) + T[a][2] * S[2][kk];
+            const float c00 = (U[0][0] * T[0][0] + U[0][1] * T[0][1]) + U[0][2] * T[0][2];
+            const float c01 = (U[0][0] * T[1][0] + U[0][1] * T[1][1]) + U[0][2] * T[1][2];
+            const float c11 = (U[1][0] * T[1][0] + U[1][1] * T[1][1]) + U[1][2] * T[1][2];
+            const float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
+            // 7. conic
+            const float det = a * c - b * b;
+            if (det > 0.0f) {
+                cA = c / det; cB = -(b / det); cC = a / det;
+                sxx = a; sxy = b; syy = c;
+                // 8. radius
+                const float mid = 0.5f * (a + c);
+                const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
+                r = (int)ceilf(3.0f * sqrtf(lam));
+                // 9. projected mean
+                mx = cam.fx * ux + cam.cx;
+                my = cam.fy * uy + cam.cy;
+                // 10. tile rectangle
+                const float rf = (float)r;
+                xmin = rect_bound((mx - rf) / 16.0f, gx);
+                xmax = rect_bound(((mx + rf) + 15.0f) / 16.0f, gx);
+                ymin = rect_bound((my - rf) / 16.0f, gy);
+                ymax = rect_bound(((my + rf) + 15.0f) / 16.0f, gy);
+                vis = (xmax - xmin) * (ymax - ymin) != 0;
+            }
+        }
+        uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
+        if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
+            unsigned long long m = 0ull;
+            vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, m, n_tiles);
+            out.tmask[i] = m;
+        }
+        if (!vis) {   // culled: every array is still written (full sectors: no L2 partial-write fills)
+            out.depth_bits[i] = 0u;
+            out.xy[i] = make_float2(0.f, 0.f);
+            out.conic_o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            out.rgb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            out.rect[i] = make_ushort4(0, 0, 0, 0);
+            out.touched[i] = 0u;
+            if (out.radius) out.radius[i] = 0;
+            continue;
+        }
+        // 11. colour
+        float col[3];
+        if (sh_degree < 0) {
+            col[0] = shs[3 * (size_t)i]; col[1] = shs[3 * (size_t)i + 1]; col[2] = shs[3 * (size_t)i + 2];
         } else {
+            if (!have_sh) {   // the SH record is read once per Gaussian, by its first visible view
+                const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+                const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
+                if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
+                    const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
 #pragma unroll
-            for (int j = 0; j < 48; j++)
-                if (j < ncoef * 3) k[j] = __ldg(sh + j);
-        }
-        const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
-        const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
-        const float X = dx / len, Y = dy / len, Z = dz / len;
-        const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
-        const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
-                    C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
-        const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
-                    C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
-                    C36 = -0.5900435899266435f;
-        float res3[3];
+                    for (int j = 0; j < 12; j++) {
+                        if (4 * j < ncoef * 3) {
+                            const float4 t4 = __ldcs(sh4 + j);
+                            k[4 * j] = t4.x; k[4 * j + 1] = t4.y; k[4 * j + 2] = t4.z; k[4 * j + 3] = t4.w;
+                        }
+                    }
+                } else {
 #pragma unroll
-        for (int ch = 0; ch < 3; ch++) {
-#define SHK(j) k[(j) * 3 + ch]
-            float res = C0 * SHK(0);
-            if (sh_degree >= 1) res = ((res - (C1 * Y) * SHK(1)) + (C1 * Z) * SHK(2)) - (C1 * X) * SHK(3);
-            if (sh_degree >= 2) {
-                const float XX = X * X, YY = Y * Y, ZZ = Z * Z, XY = X * Y, YZ = Y * Z, XZ = X * Z;
-                res = res + (C20 * XY) * SHK(4);
-                res = res + (C21 * YZ) * SHK(5);
-                res = res + (C22 * (((2.0f * ZZ) - XX) - YY)) * SHK(6);
-                res = res + (C23 * XZ) * SHK(7);
-                res = res + (C24 * (XX - YY)) * SHK(8);
-                if (sh_degree >= 3) {
-                    res = res + ((C30 * Y) * ((3.0f * XX) - YY)) * SHK(9);
-                    res = res + ((C31 * XY) * Z) * SHK(10);
-                    res = res + ((C32 * Y) * (((4.0f * ZZ) - XX) - YY)) * SHK(11);
-                    res = res + ((C33 * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))) * SHK(12);
-                    res = res + ((C34 * X) * (((4.0f * ZZ) - XX) - YY)) * SHK(13);
-                    res = res + ((C35 * Z) * (XX - YY)) * SHK(14);
-                    res = res + ((C36 * X) * (XX - (3.0f * YY))) * SHK(15);
+                    for (int j = 0; j < 48; j++)
+                        if (j < ncoef * 3) k[j] = __ldg(sh + j);
                 }
+                have_sh = true;
             }
-#undef SHK
-            res3[ch] = fmaxf(res + 0.5f, 0.0f);
+            sh_colour(k, sh_degree, px, py, pz, cam, col);
         }
-        col0 = res3[0]; col1 = res3[1]; col2 = res3[2];
+        // 12. outputs
+        out.depth_bits[i] = __float_as_uint(vz);
+        out.xy[i] = make_float2(mx, my);
+        out.conic_o[i] = make_float4(cA, cB, cC, op);
+        out.rgb[i] = make_float4(col[0], col[1], col[2], 0.f);
+        out.rect[i] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
+                                   (unsigned short)ymax);
+        out.touched[i] = n_tiles;
+        if (out.radius) out.radius[i] = r;
     }
-    // 12. outputs
-    ws.depth_bits[i] = __float_as_uint(vz);
-    ws.xy[i] = make_float2(mx, my);
-    ws.conic_o[i] = make_float4(cA, cB, cC, op);
-    ws.rgb[i] = make_float4(col0, col1, col2, 0.f);
-    ws.rect[i] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
-                              (unsigned short)ymax);
-    ws.touched[i] = n_tiles;
-    ws.radius[i] = r;
+}
+
+PreOut pre_out_of(const Workspace &ws, bool with_radius) {
+    return PreOut{ws.depth_bits, ws.xy, ws.conic_o, ws.rgb, ws.rect, ws.touched, ws.tmask,
+                  with_radius ? ws.radius : nullptr, ws.counters};
+}
+
+void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const float *means, const float *scales,
+                             const float *rots, const float *opacity, const float *shs, int sh_degree,
+                             int sh_stride, float scale_mod, int W, int H, bool tight) {
+    if (N <= 0) return;
+    launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
+        N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
+        H, pv, tight);
 }
 
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight) {
-    if (N <= 0) return;
-    launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
-        N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
-        H, cam, ws, tight);
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight,
+                       bool with_radius) {
+    PreViews pv{};
+    pv.n = 1;
+    pv.cam[0] = cam;
+    pv.out[0] = pre_out_of(ws, with_radius);
+    launch_preprocess_views(pv, st, N, means, scales, rots, opacity, shs, sh_degree, sh_stride, scale_mod, W, H,
+                            tight);
 }
 
 }  // namespace gs

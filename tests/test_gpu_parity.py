@@ -318,3 +318,41 @@ def test_tight_binning_is_an_alpha_exact_subset(case):
             A, B, C = (float(c) for c in pre["conic"][i])
             a = float(pre["opacity"][i]) * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
             assert a.max() < 1.0 / 255.0, (t, i, a.max())
+
+
+@pytest.mark.parametrize("flags", [0, 8])
+def test_view_groups_are_bit_identical_to_single_views(flags):
+    """gs_render_views reads the scene once per view group (k_preprocess over up to 4
+    views); every frame must equal the single-view gs_render of the same camera, for
+    every group size, with a group count that does not divide the view count, and
+    through the host-buffer entry point (copies overlapped on a second stream)."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device, scene_to_host
+    scene = synth.unbounded_scene(60000, 108, sh_degree=3)
+    cams = synth.orbit_cameras(7, 320, 200, 1.0)
+    bg = np.array([0.1, 0.2, 0.3], np.float32)
+    ctx = Context(0, max_points=scene.n, max_keys=1 << 22, max_w=320, max_h=200)
+    st = scene_to_device(scene)
+    o = opts(bg, sh_degree=scene.sh_degree, flags=flags)
+    ref_rgb, ref_T = [], []
+    for cam in cams:
+        r = torch.empty((3, cam.H, cam.W), device="cuda")
+        t = torch.empty((cam.H, cam.W), device="cuda")
+        ctx.gs_render(st, camera(cam), cam.W, cam.H, o, r, t)
+        ref_rgb.append(r.cpu().numpy())
+        ref_T.append(t.cpu().numpy())
+    ref_rgb, ref_T = np.stack(ref_rgb), np.stack(ref_T)
+    for g in (1, 2, 3, 4):
+        ctx.gs_set_view_group(g)
+        r = torch.full((7, 3, 200, 320), float("nan"), device="cuda")
+        t = torch.full((7, 200, 320), float("nan"), device="cuda")
+        ctx.gs_render_views(st, [camera(c) for c in cams], 320, 200, o, r, t)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), ref_rgb), g
+        assert np.array_equal(t.cpu().numpy(), ref_T), g
+        hr = torch.full((7, 3, 200, 320), float("nan")).pin_memory()
+        ht = torch.full((7, 200, 320), float("nan")).pin_memory()
+        ctx.gs_render_views_host(scene_to_host(scene), [camera(c) for c in cams], 320, 200, o, hr, ht)
+        assert np.array_equal(hr.numpy(), ref_rgb), g
+        assert np.array_equal(ht.numpy(), ref_T), g
+    ctx.close()
