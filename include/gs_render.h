@@ -143,11 +143,15 @@ int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
                          const float *shs_or_colors, const gs_camera *cams, int n_views,
                          int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
 
-/* Sets the view-group size of gs_render_views / gs_render_views_host (1..4;
- * 1 = one preprocess launch per view). Output does not depend on it. The first
- * multi-view call with group g allocates g-1 extra sets of per-Gaussian
- * preprocess outputs (60 B x max_points each). GS_ERR_INVALID_ARG otherwise. */
-int gs_set_view_group(gs_ctx *ctx, int g);
+/* Sets the view-group size of gs_render_views / gs_render_views_host (g = 1..4;
+ * 1 = one preprocess launch per view) and whether the group's per-view binning
+ * chains run concurrently on context-owned streams (concurrent != 0, default) or
+ * back to back on the caller's stream. Output does not depend on either. The
+ * first multi-view call with group g allocates g-1 extra workspaces (as
+ * gs_ctx_create: about 36 B x max_points + 16 B x max_keys each). With
+ * GS_FLAG_TIMING and concurrent chains the per-stage times overlap.
+ * GS_ERR_INVALID_ARG for g outside 1..4. */
+int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
 
 /* Synchronises the last stream used by ctx and reports counts and the status
  * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */

@@ -91,7 +91,7 @@ def load():
         "gs_debug_exponents": [P, P, I, P, P, P, P, I64, P, I, I, P],
         "gs_stage_times": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
         "gs_debug_set_trace": [P, P],
-        "gs_set_view_group": [P, I],
+        "gs_set_view_group": [P, I, I],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -200,8 +200,8 @@ class Context:
                                              _ptr(sh), arr, len(cams), W, H, ctypes.byref(o),
                                              _ptr(h_out_rgb), _ptr(h_out_T)), "gs_render_views_host")
 
-    def gs_set_view_group(self, g):
-        _check(self.lib.gs_set_view_group(self.h, int(g)), "gs_set_view_group")
+    def gs_set_view_group(self, g, concurrent=True):
+        _check(self.lib.gs_set_view_group(self.h, int(g), int(bool(concurrent))), "gs_set_view_group")
 
     def gs_last_stats(self):
         st = gs_stats()

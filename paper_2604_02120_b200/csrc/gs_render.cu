@@ -38,6 +38,12 @@ struct gs_ctx {
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t group_done[2] = {}, copies_done[2] = {};
+    // gs_render_views: binning of slot v on bstream[v] (concurrent chains), joined by ev_binned[v]
+    bool concurrent = true;
+    cudaStream_t bstream[gs::MAX_VIEW_GROUP] = {};
+    cudaEvent_t ev_binned[gs::MAX_VIEW_GROUP] = {}, ev_pre = nullptr;
+    cudaStream_t blend_stream = nullptr;   // high priority
+    cudaEvent_t ev_blended = nullptr;
 };
 
 static constexpr int kMaxEvents = 4096;
@@ -59,6 +65,34 @@ int check_cuda(cudaError_t e) {
     return GS_OK;
 }
 
+// every device buffer of one workspace (preprocess outputs, binning buffers, counters)
+cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
+    // + 512: the row-aligned column chunks add at most one partial chunk per tile row
+    w.max_chunks = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1 + 512;
+    cudaError_t e = cudaSuccess;
+#define A(ptr, n) \
+    if (e == cudaSuccess) e = alloc(ptr, n)
+    A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
+    A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
+    A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
+    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
+    A(w.cdesc, w.max_chunks); A(w.cdesc_last, w.max_chunks); A(w.tile_cnt, T); A(w.rowinfo, 3 * 513);
+    A(w.counters, 1);
+#undef A
+    if (e == cudaSuccess) e = cudaMemset(w.counters, 0, sizeof(gs::Counters));
+    return e;
+}
+
+void free_ws(gs::Workspace &w) {
+    void *ptrs[] = {w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+                    w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
+                    w.ranges, w.sums, w.cmat, w.row_total, w.cdesc, w.cdesc_last, w.tile_cnt, w.rowinfo,
+                    w.counters, w.stage};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    w = gs::Workspace{};
+}
+
 int validate(gs_ctx *c, int N, const void *means, const void *scales, const void *rots, const void *opacity,
              const void *shs, const gs_camera *cam, int W, int H, const gs_opts *o) {
     if (!c || !cam || !o || N < 0 || W <= 0 || H <= 0) return GS_ERR_INVALID_ARG;
@@ -72,7 +106,7 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
 }
 
 void drain_events(gs_ctx *c) {
-    if (c->ev_used > 0) cudaEventSynchronize(c->ev[c->ev_used - 1]);
+    for (const auto &sp : c->spans) cudaEventSynchronize(c->ev[sp.e1]);
     for (const auto &sp : c->spans) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, c->ev[sp.e0], c->ev[sp.e1]);
@@ -98,7 +132,8 @@ void span(gs_ctx *c, int stage, int e0, int e1) {
 }
 
 // the workspace of view slot v of a group: slot 0 is the context's own; slots 1..G-1
-// get their own preprocess outputs and counters and share every binning buffer
+// get a full workspace of their own (~1 GB at C5), so the views' binning chains can run
+// concurrently on their own streams
 int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
     if (v == 0) {
         *out = &c->ws;
@@ -106,19 +141,9 @@ int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
     }
     gs::Workspace &w = c->vws[v];
     if (!c->vws_alloc[v]) {
-        const size_t N = (size_t)c->max_points;
-        w = c->ws;
-        w.depth_bits = nullptr; w.xy = nullptr; w.conic_o = nullptr; w.rgb = nullptr; w.rect = nullptr;
-        w.touched = nullptr; w.tmask = nullptr; w.counters = nullptr;
-        cudaError_t e = cudaSuccess;
-#define A(ptr, n) \
-    if (e == cudaSuccess) e = alloc(ptr, n)
-        A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
-        A(w.tmask, N); A(w.counters, 1);
-#undef A
-        if (e == cudaSuccess) e = cudaMemset(w.counters, 0, sizeof(gs::Counters));
         c->vws_alloc[v] = true;   // (partially allocated pointers are freed by gs_ctx_destroy)
-        if (int rc = check_cuda(e)) return rc;
+        if (int rc = check_cuda(alloc_ws(w, (size_t)c->max_points, (size_t)c->max_keys, (size_t)c->max_tiles)))
+            return rc;
     }
     *out = &w;
     return GS_OK;
@@ -270,20 +295,7 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     c->max_w = max_w;
     c->max_h = max_h;
     c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
-    const size_t N = (size_t)max_points, K = (size_t)max_keys, T = (size_t)c->max_tiles;
-    gs::Workspace &w = c->ws;
-    // + 512: the row-aligned column chunks add at most one partial chunk per tile row
-    w.max_chunks = (size_t)gs::ceil_div_i((int64_t)std::max(N, K) + 1, gs::SORT_CHUNK) + 1 + 512;
-    cudaError_t e = cudaSuccess;
-#define A(ptr, n) \
-    if (e == cudaSuccess) e = alloc(ptr, n)
-    A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
-    A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
-    A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
-    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
-    A(w.cdesc, w.max_chunks); A(w.cdesc_last, w.max_chunks); A(w.tile_cnt, T); A(w.rowinfo, 3 * 513);
-    A(w.counters, 1);
-#undef A
+    cudaError_t e = alloc_ws(c->ws, (size_t)max_points, (size_t)max_keys, (size_t)c->max_tiles);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         gs_ctx_destroy(c);
@@ -297,20 +309,18 @@ int gs_ctx_destroy(gs_ctx *c) {
     if (!c) return GS_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    gs::Workspace &w = c->ws;
-    void *ptrs[] = {w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
-                    w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
-                    w.ranges, w.sums, w.cmat, w.row_total, w.cdesc, w.cdesc_last, w.tile_cnt, w.rowinfo,
-                    w.counters, w.stage, c->frame_rgb, c->frame_T};
-    for (void *p : ptrs)
+    free_ws(c->ws);
+    for (void *p : {(void *)c->frame_rgb, (void *)c->frame_T})
         if (p) cudaFree(p);
-    for (int v = 1; v < gs::MAX_VIEW_GROUP; v++) {
-        if (!c->vws_alloc[v]) continue;
-        gs::Workspace &x = c->vws[v];
-        void *vp[] = {x.depth_bits, x.xy, x.conic_o, x.rgb, x.rect, x.touched, x.tmask, x.counters};
-        for (void *p : vp)
-            if (p) cudaFree(p);
+    for (int v = 1; v < gs::MAX_VIEW_GROUP; v++)
+        if (c->vws_alloc[v]) free_ws(c->vws[v]);
+    for (int v = 0; v < gs::MAX_VIEW_GROUP; v++) {
+        if (c->bstream[v]) cudaStreamDestroy(c->bstream[v]);
+        if (c->ev_binned[v]) cudaEventDestroy(c->ev_binned[v]);
     }
+    if (c->ev_pre) cudaEventDestroy(c->ev_pre);
+    if (c->ev_blended) cudaEventDestroy(c->ev_blended);
+    if (c->blend_stream) cudaStreamDestroy(c->blend_stream);
     for (auto &e : c->ev) cudaEventDestroy(e);
     for (int k = 0; k < 2; k++) {
         if (c->group_done[k]) cudaEventDestroy(c->group_done[k]);
@@ -346,6 +356,20 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                              int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of) {
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
+    if (c->concurrent && G > 1 && !c->ev_pre) {
+        if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming))) return rc;
+        // the blends run on a high-priority stream: a blend gets every SM as soon as its
+        // chain is done; the other chains fill what the blend leaves
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (int rc = check_cuda(cudaStreamCreateWithPriority(&c->blend_stream, cudaStreamNonBlocking, hi))) return rc;
+        if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_blended, cudaEventDisableTiming))) return rc;
+        for (int j = 0; j < gs::MAX_VIEW_GROUP; j++) {
+            if (int rc = check_cuda(cudaStreamCreateWithPriority(&c->bstream[j], cudaStreamNonBlocking, lo)))
+                return rc;
+            if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_binned[j], cudaEventDisableTiming))) return rc;
+        }
+    }
     for (int v0 = 0; v0 < n_views; v0 += G) {
         const int n = std::min(G, n_views - v0);
         gs::PreViews pv{};
@@ -364,6 +388,33 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         c->launches += N > 0 ? 1 : 0;
         int e_prev = mark(c, st, o);
         span(c, 0, e0, e_prev);
+        if (c->concurrent && n > 1) {
+            // the views' binning chains run concurrently, one stream each (they are
+            // latency-bound chains of small kernels); blend j waits for chain j only
+            cudaEventRecord(c->ev_pre, st);
+            for (int j = 0; j < n; j++) {
+                cudaStream_t bs = c->bstream[j];
+                cudaStreamWaitEvent(bs, c->ev_pre, 0);
+                const int b0 = mark(c, bs, o);
+                enqueue_binning(c, *w[j], bs, N, cams[v0 + j], W, H, o);
+                span(c, 1, b0, mark(c, bs, o));
+                cudaEventRecord(c->ev_binned[j], bs);
+            }
+            cudaStream_t bl = c->blend_stream;
+            for (int j = 0; j < n; j++) {
+                cudaStreamWaitEvent(bl, c->ev_binned[j], 0);
+                const int e1 = mark(c, bl, o);
+                enqueue_blend(c, *w[j], bl, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H,
+                              o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
+                const int e2 = mark(c, bl, o);
+                span(c, 2, e1, e2);
+                if (e2 >= 0) c->timed_frames++;
+                c->last_counters = w[j]->counters;
+            }
+            cudaEventRecord(c->ev_blended, bl);
+            cudaStreamWaitEvent(st, c->ev_blended, 0);   // the frames are complete in stream order of st
+            continue;
+        }
         for (int j = 0; j < n; j++) {
             enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
             const int e1 = mark(c, st, o);
@@ -477,9 +528,10 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
     return finish(c, st, os, N);
 }
 
-int gs_set_view_group(gs_ctx *c, int g) {
+int gs_set_view_group(gs_ctx *c, int g, int concurrent) {
     if (!c || g < 1 || g > gs::MAX_VIEW_GROUP) return GS_ERR_INVALID_ARG;
     c->view_group = g;
+    c->concurrent = concurrent != 0;
     return GS_OK;
 }
 

@@ -342,8 +342,8 @@ def test_view_groups_are_bit_identical_to_single_views(flags):
         ref_rgb.append(r.cpu().numpy())
         ref_T.append(t.cpu().numpy())
     ref_rgb, ref_T = np.stack(ref_rgb), np.stack(ref_T)
-    for g in (1, 2, 3, 4):
-        ctx.gs_set_view_group(g)
+    for g, conc in ((1, True), (2, True), (3, False), (3, True), (4, False), (4, True)):
+        ctx.gs_set_view_group(g, conc)
         r = torch.full((7, 3, 200, 320), float("nan"), device="cuda")
         t = torch.full((7, 200, 320), float("nan"), device="cuda")
         ctx.gs_render_views(st, [camera(c) for c in cams], 320, 200, o, r, t)
