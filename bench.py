@@ -145,7 +145,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
+    from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
                                        Context, camera, opts, scene_to_device, scene_to_host, synth)
     from paper_2604_02120_b200.orbit import gather_frames, partition_views
     ws, rank, local = _dist()
@@ -277,21 +277,30 @@ def run_ours(args):
             "tensor_pipe_pct": bl.get("tensor_pipe_pct"), "issue_active_pct": bl.get("issue_active_pct"),
             "ncu_source": bl.get("source")}
 
-    # --- N1: the CUDA-core direct blend (vanilla Alg. 1) on the same frames, A/B ---
+    # --- N1: the CUDA-core direct blend (vanilla Alg. 1) and the warp-level mma.sync
+    # blend (the paper's kernel shape) at batch sizes b = 32..256 (N2), on the same
+    # orbit: blend ms per frame (live events) and orbit fps, A/B against tcgen05 ---
     ab = None
     if not args.no_ab and args.blend == "tc":
-        o_dir = opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_DIRECT, flags=GS_FLAG_TIMING)
-        ctx.gs_stage_times()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        ctx.gs_render_views(st, my_cams, W, H, o_dir, out_rgb, out_T, stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        dms, dfr = ctx.gs_stage_times()
-        ab = {"blend_direct_ms": dms[2] / max(dfr, 1), "blend_tc_ms": blend_ms,
-              "fps_direct": per / (e0.elapsed_time(e1) / 1e3), "speedup_tc_over_direct": (dms[2] / max(dfr, 1)) / blend_ms}
+        def orbit_time(o):
+            ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)   # warm
+            torch.cuda.synchronize()
+            ctx.gs_stage_times()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dms, dfr = ctx.gs_stage_times()
+            return dms[2] / max(dfr, 1), per / (e0.elapsed_time(e1) / 1e3)
+        d_ms, d_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_DIRECT, flags=GS_FLAG_TIMING))
+        ab = {"blend_tc_ms": blend_ms, "blend_direct_ms": d_ms, "fps_direct": d_fps,
+              "speedup_tc_over_direct": d_ms / blend_ms, "mma_sync": {}}
+        for b in (32, 64, 128, 256):
+            m_ms, m_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA, batch=b,
+                                          flags=GS_FLAG_TIMING))
+            ab["mma_sync"][f"b{b}"] = {"blend_ms": m_ms, "fps": m_fps, "speedup_tc_over_mma": m_ms / blend_ms}
 
     # --- N3: tile-exact intersection (bit-identical frames, fewer pairs), one timed orbit ---
     tight = None
@@ -390,7 +399,7 @@ def run_ours(args):
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
                 "roofline": roof, "stages": stages, "clocks": clk,
-                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_direct_blend": ab, "tight_intersection": tight,
+                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "tight_intersection": tight,
                 "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
                                    "pairs_kept": n_kept}}

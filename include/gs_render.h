@@ -68,7 +68,9 @@ typedef struct {
 
 enum {
     GS_BLEND_TC = 0,      /* tcgen05 TF32 hi/lo exponent GEMM (the paper's method, default) */
-    GS_BLEND_DIRECT = 1   /* CUDA-core direct Eq. (3) (vanilla Alg. 1), A/B baseline        */
+    GS_BLEND_DIRECT = 1,  /* CUDA-core direct Eq. (3) (vanilla Alg. 1), A/B baseline        */
+    GS_BLEND_MMA = 2      /* the same GEMM with warp-level mma.sync.m16n8k8 TF32 hi/lo, the
+                           * paper's kernel shape: A/B against tcgen05          */
 };
 
 enum {
@@ -86,8 +88,11 @@ typedef struct {
     int sh_degree;         /* 0..3; -1 => shs_or_colors holds plain colours [N,3]            */
     int sh_stride;         /* SH coefficients per Gaussian in shs (>= (deg+1)^2)             */
     float scale_modifier;  /* multiplies every scale (1.0)                                   */
-    int blend;             /* GS_BLEND_TC | GS_BLEND_DIRECT                                  */
+    int blend;             /* GS_BLEND_TC | GS_BLEND_DIRECT | GS_BLEND_MMA                   */
     unsigned flags;        /* GS_FLAG_*                                                      */
+    int batch;             /* GS_BLEND_MMA: Gaussians per shared-memory batch, 32/64/128/256
+                            * (0 = 256); output bit-identical for every value. The
+                            * tcgen05 blend streams fixed 32-Gaussian batches (ignored). */
 } gs_opts;
 
 typedef struct {

@@ -26,6 +26,7 @@ GS_ERR_UNSUPPORTED_ARCH = -5
 GS_ERR_NO_DEVICE = -6
 GS_BLEND_TC = 0
 GS_BLEND_DIRECT = 1
+GS_BLEND_MMA = 2
 GS_FLAG_SYNC = 1
 GS_FLAG_TIMING = 2
 GS_FLAG_STATS = 4
@@ -53,7 +54,8 @@ class gs_camera(ctypes.Structure):
 
 class gs_opts(ctypes.Structure):
     _fields_ = [("bg", ctypes.c_float * 3), ("sh_degree", ctypes.c_int), ("sh_stride", ctypes.c_int),
-                ("scale_modifier", ctypes.c_float), ("blend", ctypes.c_int), ("flags", ctypes.c_uint)]
+                ("scale_modifier", ctypes.c_float), ("blend", ctypes.c_int), ("flags", ctypes.c_uint),
+                ("batch", ctypes.c_int)]
 
 
 class gs_stats(ctypes.Structure):
@@ -124,7 +126,8 @@ def camera(cam) -> gs_camera:
     return c
 
 
-def opts(bg=(0.0, 0.0, 0.0), sh_degree=3, sh_stride=None, scale_modifier=1.0, blend=GS_BLEND_TC, flags=0):
+def opts(bg=(0.0, 0.0, 0.0), sh_degree=3, sh_stride=None, scale_modifier=1.0, blend=GS_BLEND_TC, flags=0,
+         batch=0):
     o = gs_opts()
     o.bg[:] = [float(v) for v in bg]
     o.sh_degree = int(sh_degree)
@@ -132,6 +135,7 @@ def opts(bg=(0.0, 0.0, 0.0), sh_degree=3, sh_stride=None, scale_modifier=1.0, bl
     o.scale_modifier = float(scale_modifier)
     o.blend = int(blend)
     o.flags = int(flags)
+    o.batch = int(batch)
     return o
 
 

@@ -584,4 +584,244 @@ void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_
                                            out_T);
 }
 
+// ===========================================================================
+// Warp-level tensor-core blend (the paper's own kernel shape, on sm_100a):
+// mma.sync.m16n8k8 TF32 (HMMA.1688) instead of tcgen05. A/B against k_blend_tc for
+// the north star's "mma.sync or tcgen05, whichever ncu shows wins".
+//   One 256-thread CTA per tile at a time (persistent, atomic tile queue), batches of
+//   BATCH Gaussians (256): every thread gathers one Gaussian and writes its row
+//   of M_g (Eq. 6, TF32 hi/lo, K = 16) into shared memory (Stage 2).
+//   Each warp then owns its 32 pixels and, 16 Gaussians at a time, issues 2 (pixel
+//   halves) x 2 (8-Gaussian n-blocks) x 2 (K-steps) mma.m16n8k8 (Stage 3)
+//   with the constant M_p fragments in registers. The accumulator fragment spreads a
+//   pixel's exponents over a lane quad, so they go through a per-warp shared buffer
+//   (conflict-free: MMA row r is stored in buffer row 2r (r < 8) / 2(r-8)+1 of its
+//   half, rows 20 words apart) and each lane reads back its own pixel's 16 values.
+//   Compositing is the same as k_blend_tc's (Eq. 1, R-1..R-4, warp-uniform skip).
+// Output is bit-identical for every BATCH (each exponent is the same MMA sum).
+// ===========================================================================
+constexpr int MMA_THREADS = 256;
+constexpr int MMA_SUB = 16;            // Gaussians per MMA step (two n8 blocks)
+constexpr int MMA_TS = 20;             // transpose-buffer row stride (words)
+
+template <int BATCH>
+struct SmemMMA {
+    uint32_t Mg[BATCH][16];            // rows: word 4q + j holds K index q + 4j
+    float4 rgb[BATCH];
+    float tr[NCW][32 * MMA_TS];        // per-warp transpose buffer
+    int tile;
+};
+
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// K index k of the pixel row [v_p | v_p | 0] (Eq. 7) for the pixel (x, y)
+__device__ __forceinline__ uint32_t mp_word(int x, int y, int k) {
+    const float xb = 7.5f - (float)x, yb = 7.5f - (float)y;
+    const int kk = k < 6 ? k : (k < 12 ? k - 6 : -1);
+    float v = 0.f;
+    switch (kk) {
+        case 0: v = xb * xb; break;
+        case 1: v = yb * yb; break;
+        case 2: v = xb * yb; break;
+        case 3: v = xb; break;
+        case 4: v = yb; break;
+        case 5: v = 1.0f; break;
+        default: v = 0.f;
+    }
+    return __float_as_uint(v);   // exact in TF32
+}
+
+#ifndef GS_MMA_MINB
+#define GS_MMA_MINB 4
+#endif
+template <int BATCH>
+__global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
+    k_blend_mma(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
+                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W, int H,
+                float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
+                uint32_t *tile_queue) {
+    extern __shared__ uint8_t smem_raw[];
+    SmemMMA<BATCH> &sm = *reinterpret_cast<SmemMMA<BATCH> *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r4 = lane >> 2;
+    // compositor pixel of this thread = buffer row `lane` of its warp
+    int x, y;
+    pixel_of(threadIdx.x, x, y);
+    // A fragments (M_p rows): MMA row r of pixel half h is buffer row 16h + (r < 8 ? 2r : 2(r-8)+1)
+    uint32_t afr[2][2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        int px0, py0, px1, py1;
+        pixel_of(warp * 32 + 16 * h + 2 * r4, px0, py0);       // MMA row r4
+        pixel_of(warp * 32 + 16 * h + 2 * r4 + 1, px1, py1);   // MMA row r4 + 8
+#pragma unroll
+        for (int ks = 0; ks < 2; ks++) {
+            afr[h][ks][0] = mp_word(px0, py0, 8 * ks + q);
+            afr[h][ks][1] = mp_word(px1, py1, 8 * ks + q);
+            afr[h][ks][2] = mp_word(px0, py0, 8 * ks + q + 4);
+            afr[h][ks][3] = mp_word(px1, py1, 8 * ks + q + 4);
+        }
+    }
+    float *tr = sm.tr[warp];
+    pdl_wait();
+    for (;;) {
+        if (threadIdx.x == 0) sm.tile = (int)atomicAdd(tile_queue, 1u);
+        __syncthreads();
+        const int tile = sm.tile;
+        if (tile >= ntiles) break;
+        const uint2 rg = ranges[tile];
+        const float xc = (float)(GS_TILE * (tile % gx)) + 7.5f, yc = (float)(GS_TILE * (tile / gx)) + 7.5f;
+        float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
+        bool wdone = false;
+        // the record of Gaussian b + threadIdx.x is fetched one batch ahead, into registers,
+        // so the gathers of batch k+1 overlap the MMAs and compositing of batch k
+        float2 pm = make_float2(0.f, 0.f);
+        float4 pco = make_float4(0.f, 0.f, 0.f, 1.f), pcol = make_float4(0.f, 0.f, 0.f, 0.f);
+        auto fetch = [&](uint32_t b) {
+            if (threadIdx.x < BATCH && b + threadIdx.x < rg.y) {
+                const uint32_t gi = vals[b + threadIdx.x];
+                pm = xy[gi];
+                pco = conic_o[gi];
+                pcol = rgb[gi];
+            }
+        };
+        fetch(rg.x);
+        for (uint32_t b0 = rg.x; b0 < rg.y; b0 += BATCH) {
+            if (__syncthreads_and(wdone)) break;   // every warp terminated (also: batch b0-1 consumed)
+            const int cnt = (int)min((uint32_t)BATCH, rg.y - b0);
+            const int i = threadIdx.x;
+            if (i < ((cnt + MMA_SUB - 1) & ~(MMA_SUB - 1))) {
+                uint32_t u[16];
+                float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < cnt) {   // Eq. (6) row, log2 e and log2 o folded in (R-10), TF32 hi/lo (R-11)
+                    col = pcol;
+                    const float xh = pm.x - xc, yh = pm.y - yc;
+                    const float A = pco.x, B = pco.y, C = pco.z;
+                    float v[6];
+                    v[0] = -0.5f * A * LOG2E;
+                    v[1] = -0.5f * C * LOG2E;
+                    v[2] = -B * LOG2E;
+                    v[3] = -(A * xh + B * yh) * LOG2E;
+                    v[4] = -(C * yh + B * xh) * LOG2E;
+                    v[5] = -(0.5f * A * xh * xh + 0.5f * C * yh * yh + B * xh * yh) * LOG2E + lg2_approx(pco.w);
+#pragma unroll
+                    for (int k = 0; k < 6; k++) {
+                        const uint32_t hi = f32_to_tf32_rna(v[k]);
+                        u[k] = hi;
+                        u[6 + k] = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
+                    }
+                } else {   // padding row: exponent -1e30, never kept
+#pragma unroll
+                    for (int k = 0; k < 12; k++) u[k] = 0u;
+                    u[5] = __float_as_uint(-1e30f);
+                }
+                u[12] = u[13] = u[14] = u[15] = 0u;
+                uint4 *row = reinterpret_cast<uint4 *>(&sm.Mg[i][0]);
+#pragma unroll
+                for (int qq = 0; qq < 4; qq++) row[qq] = make_uint4(u[qq], u[qq + 4], u[qq + 8], u[qq + 12]);
+                sm.rgb[i] = col;
+            }
+            fetch(b0 + BATCH);
+            __syncthreads();
+            if (wdone) continue;
+            for (int g0 = 0; g0 < cnt; g0 += MMA_SUB) {
+                // ---- exponents of 16 Gaussians for the warp's 32 pixels ----
+                float d[2][2][4];
+#pragma unroll
+                for (int nb = 0; nb < 2; nb++) {
+                    const uint4 bw = *reinterpret_cast<const uint4 *>(&sm.Mg[g0 + 8 * nb + r4][4 * q]);
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+#pragma unroll
+                        for (int e = 0; e < 4; e++) d[h][nb][e] = 0.f;
+                        mma_tf32_16x8x8(d[h][nb], afr[h][0], bw.x, bw.y);
+                        mma_tf32_16x8x8(d[h][nb], afr[h][1], bw.z, bw.w);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+#pragma unroll
+                    for (int nb = 0; nb < 2; nb++) {
+                        float *r0 = tr + (16 * h + 2 * r4) * MMA_TS + 8 * nb + 2 * q;
+                        *reinterpret_cast<float2 *>(r0) = make_float2(d[h][nb][0], d[h][nb][1]);
+                        *reinterpret_cast<float2 *>(r0 + MMA_TS) = make_float2(d[h][nb][2], d[h][nb][3]);
+                    }
+                __syncwarp();
+                float m[MMA_SUB];
+#pragma unroll
+                for (int j = 0; j < MMA_SUB / 4; j++) {
+                    const float4 t4 = *reinterpret_cast<const float4 *>(tr + lane * MMA_TS + 4 * j);
+                    m[4 * j] = t4.x; m[4 * j + 1] = t4.y; m[4 * j + 2] = t4.z; m[4 * j + 3] = t4.w;
+                }
+                // ---- compositing, as k_blend_tc ----
+                const uint32_t crow = smem_u32(&sm.rgb[g0]);
+#pragma unroll
+                for (int j = 0; j < MMA_SUB; j++) {
+                    const float mj = m[j];
+                    const bool live = mj >= thr;
+                    if (__any_sync(0xffffffffu, live)) {
+                        const float4 c = ld_shared_f4(crow + 16 * j);
+                        const float a = fminf(ALPHA_MAX, ex2_approx(mj));
+                        const float tT = fmaf(-a, T, T);
+                        const float w = a * T;
+                        const bool acc = live && tT >= T_MIN;
+                        C0 = acc ? fmaf(w, c.x, C0) : C0;
+                        C1 = acc ? fmaf(w, c.y, C1) : C1;
+                        C2 = acc ? fmaf(w, c.z, C2) : C2;
+                        T = acc ? tT : T;
+                        thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;
+                    }
+                }
+                if (__all_sync(0xffffffffu, thr > 0.f)) {
+                    wdone = true;
+                    break;
+                }
+            }
+        }
+        const int px = GS_TILE * (tile % gx) + x, py = GS_TILE * (tile / gx) + y;
+        if (px < W && py < H) {
+            const size_t pix = (size_t)py * W + px, plane = (size_t)W * H;
+            out_rgb[pix] = C0 + T * bg0;
+            out_rgb[plane + pix] = C1 + T * bg1;
+            out_rgb[2 * plane + pix] = C2 + T * bg2;
+            out_T[pix] = T;
+        }
+        __syncthreads();   // sm.tile / the batch buffers are reused by the next tile
+    }
+}
+
+template <int BATCH>
+static void launch_mma_b(cudaStream_t st, int grid, const float2 *xy, const float4 *conic_o, const float4 *rgb,
+                         const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
+                         const float bg[3], float *out_rgb, float *out_T, uint32_t *queue) {
+    const size_t smem = sizeof(SmemMMA<BATCH>) + 128;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_blend_mma<BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    launch_pdl(k_blend_mma<BATCH>, grid, MMA_THREADS, smem, st, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
+               bg[0], bg[1], bg[2], out_rgb, out_T, queue);
+}
+
+void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
+                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
+                      int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch) {
+    if (ntiles <= 0) return;
+    const int grid = std::max(1, std::min(GS_MMA_MINB * num_sms, ntiles));
+    uint32_t *queue = &ws.counters->tile_queue;
+    switch (batch) {
+        case 32: launch_mma_b<32>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 64: launch_mma_b<64>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 128: launch_mma_b<128>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        default: launch_mma_b<256>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+    }
+}
+
 }  // namespace gs

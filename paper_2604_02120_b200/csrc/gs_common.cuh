@@ -296,6 +296,9 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats);
 extern long long *g_blend_trace;
+void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
+                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
+                      int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch);
 void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
                          const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *counters);

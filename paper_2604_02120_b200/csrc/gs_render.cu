@@ -99,6 +99,9 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
     if (W > c->max_w || H > c->max_h) return GS_ERR_INVALID_ARG;
     if (N > c->max_points) return GS_ERR_CAPACITY;
     if (o->sh_degree > 3 || o->sh_degree < -1) return GS_ERR_INVALID_ARG;
+    if (o->blend < GS_BLEND_TC || o->blend > GS_BLEND_MMA) return GS_ERR_INVALID_ARG;
+    if (o->batch != 0 && o->batch != 32 && o->batch != 64 && o->batch != 128 && o->batch != 256)
+        return GS_ERR_INVALID_ARG;
     if (o->sh_degree >= 0 && o->sh_stride < (o->sh_degree + 1) * (o->sh_degree + 1)) return GS_ERR_INVALID_ARG;
     if (N > 0 && (!means || !scales || !rots || !opacity || !shs)) return GS_ERR_INVALID_ARG;
     if (!aligned16(rots)) return GS_ERR_ALIGNMENT;
@@ -181,6 +184,9 @@ void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const flo
     if (o.blend == GS_BLEND_DIRECT && !dump)
         gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
                                 w.counters);
+    else if (o.blend == GS_BLEND_MMA && !dump)
+        gs::launch_blend_mma(w, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+                             c->num_sms, o.batch);
     else
         gs::launch_blend_tc(w, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
                             dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_TC, GsError, synth
+from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GsError, synth
 
 from gpu_util import (MAX_ABS, MIN_PSNR, compare, gpu_binning, gpu_blend_from, gpu_preprocess, gpu_render,
                       make_ctx)
@@ -109,7 +109,7 @@ def test_binning_bit_exact(case):
     assert np.array_equal(got["ranges"], ref["ranges"])
 
 
-@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT], ids=["tc", "direct"])
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA], ids=["tc", "direct", "mma"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_blend_parity_on_oracle_binning(case, blend):
     """Stage (d) alone: oracle splats + oracle binning uploaded by the harness."""
@@ -124,7 +124,7 @@ def test_blend_parity_on_oracle_binning(case, blend):
     assert m["T_max"] <= MAX_ABS, m
 
 
-@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT], ids=["tc", "direct"])
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA], ids=["tc", "direct", "mma"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_render_parity_end_to_end(case, blend):
     scene, cam, bg = CASES[case]()
@@ -356,3 +356,27 @@ def test_view_groups_are_bit_identical_to_single_views(flags):
         assert np.array_equal(hr.numpy(), ref_rgb), g
         assert np.array_equal(ht.numpy(), ref_T), g
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["C2", "dense", "ragged"])
+def test_mma_blend_is_bit_identical_across_batch_sizes(case):
+    """SURVEY N2 / reading R-18: the batch size b is performance-only. The mma.sync
+    blend computes every exponent with the same MMA sum whatever b, so frames are
+    bit-identical for b in {32, 64, 128, 256}."""
+    import torch
+    from paper_2604_02120_b200 import camera, opts, scene_to_device
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    st = scene_to_device(scene)
+    outs = []
+    for b in (32, 64, 128, 256):
+        r = torch.full((3, cam.H, cam.W), float("nan"), device="cuda")
+        t = torch.full((cam.H, cam.W), float("nan"), device="cuda")
+        ctx.gs_render(st, camera(cam), cam.W, cam.H,
+                      opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA, flags=1, batch=b), r, t)
+        outs.append((r.cpu().numpy(), t.cpu().numpy()))
+    for r, t in outs[1:]:
+        assert np.array_equal(r, outs[0][0]) and np.array_equal(t, outs[0][1])
+    with pytest.raises(GsError):
+        ctx.gs_render(st, camera(cam), cam.W, cam.H, opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA,
+                                                          batch=48), r, t)

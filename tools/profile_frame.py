@@ -8,14 +8,15 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_TC, Context, camera, opts,  # noqa: E402
+from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, Context, camera, opts,  # noqa: E402
                                    scene_to_device, synth)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--frames", type=int, default=3)
 ap.add_argument("--view", type=int, default=0)
-ap.add_argument("--blend", default="tc")
+ap.add_argument("--blend", default="tc", choices=["tc", "direct", "mma"])
+ap.add_argument("--batch", type=int, default=0)
 a = ap.parse_args()
 scene, cams, bg = synth.make_config(a.config, views=64 if a.config == "C5" else 1)
 cam = cams[a.view % len(cams)]
@@ -23,7 +24,8 @@ ctx = Context(0, max_points=scene.n, max_keys=48 << 20, max_w=cam.W, max_h=cam.H
 st = scene_to_device(scene)
 rgb = torch.empty((3, cam.H, cam.W), device="cuda")
 T = torch.empty((cam.H, cam.W), device="cuda")
-o = opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_DIRECT if a.blend == "direct" else GS_BLEND_TC)
+o = opts(bg, sh_degree=scene.sh_degree, batch=a.batch,
+         blend={"tc": GS_BLEND_TC, "direct": GS_BLEND_DIRECT, "mma": GS_BLEND_MMA}[a.blend])
 for _ in range(a.frames):
     ctx.gs_render(st, camera(cam), cam.W, cam.H, o, rgb, T)
 torch.cuda.synchronize()

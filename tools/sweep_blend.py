@@ -34,5 +34,9 @@ else:
             d = json.loads(r.stdout.strip().splitlines()[-1])
             print(name, defs, round(d["value"], 1), {k: round(v, 4) for k, v in d["stage_ms_per_frame"].items()},
                   flush=True)
+            ab = d.get("ab_blend") or {}
+            if ab:
+                print("   direct", round(ab["blend_direct_ms"], 4), "mma",
+                      {b: round(v["blend_ms"], 4) for b, v in ab.get("mma_sync", {}).items()}, flush=True)
         except Exception:
             print(name, "FAILED", r.stdout[-500:], r.stderr[-2000:], flush=True)
