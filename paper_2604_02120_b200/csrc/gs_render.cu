@@ -5,6 +5,7 @@
 // a frame); the only optional synchronisation is GS_FLAG_SYNC / gs_last_stats.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -47,6 +48,9 @@ struct gs_ctx {
 };
 
 static constexpr int kMaxEvents = 4096;
+namespace gs {
+int g_pdl = 1;
+}
 
 namespace {
 
@@ -288,6 +292,7 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     if ((int64_t)gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE) > gs::MAX_TILES)
         return GS_ERR_INVALID_ARG;
     *out = nullptr;
+    if (const char *e = getenv("GS_PDL")) gs::g_pdl = atoi(e) != 0;
     const int arch = gs_device_arch(device);
     if (arch < 0) return arch;
     if (arch != 100) return GS_ERR_UNSUPPORTED_ARCH;
