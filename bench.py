@@ -31,6 +31,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "frames/sec at 1080p per B200 and 8-GPU; tensor-pipe % and HBM GB/s"
 UNIT = "frames/s"
+INTERSECT = {"vanilla": (0, "vanilla 3-sigma rect"),
+             "obox": (16, "GS_FLAG_OBOX: vanilla rect clipped to the opacity-aware alpha >= 1/255 box"),
+             "tight": (8, "GS_FLAG_TIGHT: opacity-aware box + per-row ellipse column runs")}
 VIEW_GROUP = 4   # views per preprocess launch (gs_set_view_group), binning chains concurrent
 WORKLOAD = "C5: 6M Gaussians SH3, 1920x1080, 64-view orbit (BASELINE.json configs[4])"
 
@@ -114,7 +117,7 @@ def run_reference(args):
     for k in range(args.warmup + args.steps):
         cam = cams[(k * 16) % len(cams)]
         t0 = time.perf_counter()
-        oracle.render(scene, cam, bg, threads=threads, mask=False)
+        oracle.render(scene, cam, bg, threads=threads, mask=False, obox=args.intersect == "obox")
         dt = time.perf_counter() - t0
         if k >= args.warmup:
             times.append(dt)
@@ -124,18 +127,19 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "views": args.views, "sample": "1 view per step"},
+            "config": {"workload": WORKLOAD, "views": args.views, "sample": "1 view per step",
+                       "intersection": INTERSECT[args.intersect][1] if args.intersect != "tight" else INTERSECT["vanilla"][1]},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(scene, cam, bg):
+def cpu_baseline(scene, cam, bg, obox):
     """Oracle timed on the host cores on one view of the same workload (~10-20 s)."""
     import oracle
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    oracle.render(scene, cam, bg, threads=threads, mask=False)
+    oracle.render(scene, cam, bg, threads=threads, mask=False, obox=obox)
     dt = time.perf_counter() - t0
     return {"value": 1.0 / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"one 1920x1080 view (view 0) of the C5 scene, {dt:.1f} s with {threads} threads"}
@@ -158,7 +162,7 @@ def run_ours(args):
     per = len(mine)
     my_cams = [camera(cams[v]) for v in mine]
     blend = GS_BLEND_DIRECT if args.blend == "direct" else GS_BLEND_TC
-    base_flags = GS_FLAG_TIGHT if args.tight else 0
+    base_flags = INTERSECT[args.intersect][0]
     ctx = Context(local, max_points=scene.n, max_keys=args.max_keys, max_w=W, max_h=H)
     ctx.gs_set_view_group(VIEW_GROUP, True)
     st = scene_to_device(scene)
@@ -302,10 +306,11 @@ def run_ours(args):
                                           flags=GS_FLAG_TIMING))
             ab["mma_sync"][f"b{b}"] = {"blend_ms": m_ms, "fps": m_fps, "speedup_tc_over_mma": m_ms / blend_ms}
 
-    # --- N3: tile-exact intersection (bit-identical frames, fewer pairs), one timed orbit ---
-    tight = None
-    if not args.tight and not args.no_ab:
-        o_t = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=GS_FLAG_TIMING | GS_FLAG_TIGHT)
+    # --- N3: the other intersection modes (bit-identical frames, fewer pairs), one timed orbit each ---
+    n3 = {}
+    for mode in ([] if args.no_ab else [m for m in INTERSECT if m != args.intersect]):
+        mflag = INTERSECT[mode][0]
+        o_t = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=GS_FLAG_TIMING | mflag)
         ctx.gs_render_views(st, my_cams, W, H, o_t, out_rgb, out_T, stream)   # warm
         torch.cuda.synchronize()
         ctx.gs_stage_times()
@@ -316,13 +321,14 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         tms, tfr = ctx.gs_stage_times()
-        ctx.gs_render(st, my_cams[0], W, H, opts(bg, sh_degree=scene.sh_degree, flags=GS_FLAG_STATS | GS_FLAG_TIGHT),
+        ctx.gs_render(st, my_cams[0], W, H, opts(bg, sh_degree=scene.sh_degree, flags=GS_FLAG_STATS | mflag),
                       out_rgb[0], out_T[0], stream)
         ts = ctx.gs_last_stats()
-        tight = {"fps": per / (e0.elapsed_time(e1) / 1e3),
-                 "stage_ms_per_frame": dict(zip(("preprocess", "binning", "blend"), (m / max(tfr, 1) for m in tms))),
-                 "n_keys_view0": ts.n_keys, "pairs_evaluated_view0": ts.pairs_evaluated,
-                 "note": "GS_FLAG_TIGHT: frames bit-identical to the vanilla-rect ones (tested)"}
+        n3[mode] = {"fps": per / (e0.elapsed_time(e1) / 1e3),
+                    "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"),
+                                                        (m / max(tfr, 1) for m in tms))),
+                    "n_keys_view0": ts.n_keys, "pairs_evaluated_view0": ts.pairs_evaluated,
+                    "note": INTERSECT[mode][1] + "; frames bit-identical to the vanilla-rect ones (tested)"}
 
     # --- N2: resolution sensitivity (1x / 2x / 3x of 1080p, same scene, orbit views) ---
     res_sweep = None
@@ -384,7 +390,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(scene, cams[0], bg)
+        cpu = cpu_baseline(scene, cams[0], bg, args.intersect == "obox")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -392,14 +398,14 @@ def run_ours(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "views": args.views, "n_gaussians": N, "W": W, "H": H,
                            "sh_degree": scene.sh_degree, "blend": args.blend,
-                           "intersection": "tile-exact (GS_FLAG_TIGHT)" if args.tight else "vanilla 3-sigma rect",
+                           "intersection": INTERSECT[args.intersect][1],
                            "parallelism": f"view-partition x{ws}" + (" + NCCL gather" if ws > 1 else ""),
                            "l2": "inputs larger than L2 (1.42 GB scene, 2.1 GB of frames per step)"},
                 "ms_per_frame": elapsed_ms / args.steps / per, "stage_ms_per_frame": {
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
                 "roofline": roof, "stages": stages, "clocks": clk,
-                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "tight_intersection": tight,
+                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3,
                 "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
                                    "pairs_kept": n_kept}}
@@ -422,7 +428,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ab", action="store_true")
-    ap.add_argument("--tight", action="store_true", help="time the GS_FLAG_TIGHT path as the headline")
+    ap.add_argument("--intersect", default="obox", choices=list(INTERSECT),
+                    help="intersection mode of the headline (the others are timed alongside, N3)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N2 resolution sweep")
     ap.add_argument("--sweep-views", type=int, default=8)
     args = ap.parse_args()

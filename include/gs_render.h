@@ -77,10 +77,16 @@ enum {
     GS_FLAG_SYNC = 1u,    /* synchronise the stream at the end and report device errors     */
     GS_FLAG_TIMING = 2u,  /* record CUDA events around the stages (read by gs_stage_times)  */
     GS_FLAG_STATS = 4u,   /* count blend work (pairs evaluated / kept) into gs_stats        */
-    GS_FLAG_TIGHT = 8u    /* tile-exact intersection: drop (Gaussian, tile) pairs whose
+    GS_FLAG_TIGHT = 8u,   /* tile-exact intersection: drop (Gaussian, tile) pairs whose
                            * maximum over the tile's pixel box is alpha < 1/255 (with a margin
                            * larger than the exponent error). Such pairs are alpha-skipped by the
                            * blend anyway, so the image is bit-identical; binning keeps a subset. */
+    GS_FLAG_OBOX = 16u    /* opacity-aware box (cheaper): the vanilla rect clipped to the
+                           * bounding box of the ellipse where alpha >= 1/255 can hold (margin
+                           * 5e-3 in ln alpha), and Gaussians with 255*opacity < 1 culled; no
+                           * per-row masks, so binning takes the plain-rect path. Frames are
+                           * bit-identical to the vanilla rect's; docs/preprocess_order.md 10b.
+                           * GS_FLAG_TIGHT takes precedence if both are set. */
 };
 
 typedef struct {

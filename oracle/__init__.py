@@ -52,6 +52,10 @@ def _load():
         lib.orc_preprocess.argtypes = [ctypes.c_int, P, P, P, P, P, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_float, ctypes.POINTER(_Cam), ctypes.c_int,
                                        ctypes.c_int, P, P, P, P, P, P, P]
+        lib.orc_preprocess_mode.restype = ctypes.c_int
+        lib.orc_preprocess_mode.argtypes = lib.orc_preprocess.argtypes + [ctypes.c_int]
+        lib.orc_ln_step10b.restype = ctypes.c_float
+        lib.orc_ln_step10b.argtypes = [ctypes.c_float]
         lib.orc_binning.restype = ctypes.c_int64
         lib.orc_binning.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, ctypes.c_int, P, P, P,
                                     ctypes.c_int64]
@@ -88,8 +92,9 @@ def camera_struct(cam):
     return c
 
 
-def preprocess(scene, cam, W=None, H=None, scale_modifier=1.0):
-    """Stage (a) per docs/preprocess_order.md. Returns a dict of numpy arrays."""
+def preprocess(scene, cam, W=None, H=None, scale_modifier=1.0, obox=False):
+    """Stage (a) per docs/preprocess_order.md (obox: with step 10b, the opacity-aware box
+    of GS_FLAG_OBOX). Returns a dict of numpy arrays."""
     lib = _load()
     W = cam.W if W is None else W
     H = cam.H if H is None else H
@@ -103,13 +108,18 @@ def preprocess(scene, cam, W=None, H=None, scale_modifier=1.0):
                rect=np.zeros((n, 4), np.int32), radius=np.zeros(n, np.int32),
                touched=np.zeros(n, np.uint32))
     c = camera_struct(cam)
-    nv = lib.orc_preprocess(n, _p(means), _p(scales), _p(rots), _p(op), _p(shs), deg, stride,
-                            scale_modifier, ctypes.byref(c), W, H, _p(out["depth"]), _p(out["xy"]),
-                            _p(out["conic"]), _p(out["rgb"]), _p(out["rect"]), _p(out["radius"]),
-                            _p(out["touched"]))
+    nv = lib.orc_preprocess_mode(n, _p(means), _p(scales), _p(rots), _p(op), _p(shs), deg, stride,
+                                 scale_modifier, ctypes.byref(c), W, H, _p(out["depth"]), _p(out["xy"]),
+                                 _p(out["conic"]), _p(out["rgb"]), _p(out["rect"]), _p(out["radius"]),
+                                 _p(out["touched"]), int(bool(obox)))
     out["n_visible"] = nv
     out["opacity"] = op
     return out
+
+
+def ln_step10b(t):
+    """docs/preprocess_order.md step 10b: the fixed-operation ln used by GS_FLAG_OBOX."""
+    return float(_load().orc_ln_step10b(float(t)))
 
 
 def binning(pre, W, H):
@@ -177,9 +187,9 @@ def vp(xb, yb):
     return v
 
 
-def render(scene, cam, bg=(0.0, 0.0, 0.0), threads=None, mask=True, delta_a=DELTA_A):
+def render(scene, cam, bg=(0.0, 0.0, 0.0), threads=None, mask=True, delta_a=DELTA_A, obox=False):
     """Whole path: preprocess -> binning -> blend."""
-    pre = preprocess(scene, cam)
+    pre = preprocess(scene, cam, obox=obox)
     b = binning(pre, cam.W, cam.H)
     out = blend(pre, b, cam.W, cam.H, bg, threads=threads, mask=mask, delta_a=delta_a)
     return pre, b, out

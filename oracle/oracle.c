@@ -62,13 +62,36 @@ static int rect_bound(float v, int g) {
     return (int)c;
 }
 
-/* Returns number of visible Gaussians. Outputs are zero for culled ones. */
-int orc_preprocess(int N, const float *means, const float *scales, const float *rots,
-                   const float *opacity, const float *shs, int sh_degree, int sh_stride,
-                   float scale_modifier, const orc_camera *cam, int W, int H,
-                   float *depth, float *xy, float *conic, float *rgb, int32_t *rect,
-                   int32_t *radius, uint32_t *touched) {
-    (void)opacity;
+/* Step 10b of docs/preprocess_order.md: natural log of t >= 1 by a fixed sequence
+ * of binary32 operations. t = 2^e * m with m in [1, 2);
+ * ln t = e * ln2 + 2 * atanh(s), s = (m - 1) / (m + 1), atanh(s) = s (1 + s^2/3 +
+ * s^4/5 + s^6/7 + s^8/9 + ...), the polynomial evaluated by Horner's rule. */
+static float ln_step10b(float t) {
+    uint32_t u;
+    memcpy(&u, &t, 4);
+    const int e = (int)((u >> 23) & 0xFFu) - 127;
+    const uint32_t mu = (u & 0x7FFFFFu) | 0x3F800000u;
+    float m;
+    memcpy(&m, &mu, 4);
+    const float s = (m - 1.0f) / (m + 1.0f);
+    const float s2 = s * s;
+    float h = s2 * 0.11111111f;           /* 1/9 */
+    h = (h + 0.14285715f) * s2;           /* 1/7 */
+    h = (h + 0.2f) * s2;                  /* 1/5 */
+    h = (h + 0.33333334f) * s2;           /* 1/3 */
+    h = h + 1.0f;
+    return (float)e * 0.6931472f + 2.0f * (s * h);
+}
+
+float orc_ln_step10b(float t) { return ln_step10b(t); }   /* exported for the pins */
+
+/* Returns number of visible Gaussians. Outputs are zero for culled ones.
+ * obox != 0: step 10b (GS_FLAG_OBOX), the rect clipped to the opacity-aware box. */
+int orc_preprocess_mode(int N, const float *means, const float *scales, const float *rots,
+                        const float *opacity, const float *shs, int sh_degree, int sh_stride,
+                        float scale_modifier, const orc_camera *cam, int W, int H,
+                        float *depth, float *xy, float *conic, float *rgb, int32_t *rect,
+                        int32_t *radius, uint32_t *touched, int obox) {
     const float *R = cam->R;
     const int gx = ceil_div(W, TILE), gy = ceil_div(H, TILE);
     int visible = 0;
@@ -163,6 +186,26 @@ int orc_preprocess(int N, const float *means, const float *scales, const float *
         int area = (xmax - xmin) * (ymax - ymin);
         if (area == 0) continue;
 
+        /* 10b. opacity-aware box (GS_FLAG_OBOX): alpha >= 1/255 needs
+         * d^T Sigma^-1 d <= lim = 2 (ln(255 o) + 0.005); that ellipse lies inside
+         * |dx| <= sqrt(lim a), |dy| <= sqrt(lim c). Tiles outside are dropped; 255 o < 1 culls. */
+        if (obox) {
+            const float t = 255.0f * opacity[i];
+            if (!(t >= 1.0f)) continue;
+            const float lim = 2.0f * (ln_step10b(t) + 0.005f);
+            const float ex = sqrtf(lim * a), ey = sqrtf(lim * c);
+            const int bx0 = rect_bound(floorf((mx - ex) * 0.0625f), gx);
+            const int bx1 = rect_bound(floorf((mx + ex) * 0.0625f) + 1.0f, gx);
+            const int by0 = rect_bound(floorf((my - ey) * 0.0625f), gy);
+            const int by1 = rect_bound(floorf((my + ey) * 0.0625f) + 1.0f, gy);
+            if (bx0 > xmin) xmin = bx0;
+            if (bx1 < xmax) xmax = bx1;
+            if (by0 > ymin) ymin = by0;
+            if (by1 < ymax) ymax = by1;
+            if (!(xmax > xmin && ymax > ymin)) continue;
+            area = (xmax - xmin) * (ymax - ymin);
+        }
+
         /* 11. colour */
         float col[3];
         if (sh_degree < 0) {
@@ -210,6 +253,15 @@ int orc_preprocess(int N, const float *means, const float *scales, const float *
         visible++;
     }
     return visible;
+}
+
+int orc_preprocess(int N, const float *means, const float *scales, const float *rots,
+                   const float *opacity, const float *shs, int sh_degree, int sh_stride,
+                   float scale_modifier, const orc_camera *cam, int W, int H,
+                   float *depth, float *xy, float *conic, float *rgb, int32_t *rect,
+                   int32_t *radius, uint32_t *touched) {
+    return orc_preprocess_mode(N, means, scales, rots, opacity, shs, sh_degree, sh_stride, scale_modifier, cam,
+                               W, H, depth, xy, conic, rgb, rect, radius, touched, 0);
 }
 
 /* ------------------------------------------------------------------------ */

@@ -66,6 +66,12 @@ struct Workspace {
     size_t stage_bytes;
 };
 
+// intersection mode of the preprocess: 0 vanilla rect, 1 GS_FLAG_TIGHT (box + per-row
+// column runs, tile masks), 2 GS_FLAG_OBOX (vanilla rect clipped to the opacity-aware box)
+inline int intersect_mode(unsigned flags) {
+    return (flags & GS_FLAG_TIGHT) ? 1 : ((flags & GS_FLAG_OBOX) ? 2 : 0);
+}
+
 // ---- per-view outputs of the preprocess (a view group shares one scene read) ----
 struct PreOut {
     uint32_t *depth_bits;
@@ -284,12 +290,12 @@ constexpr float ALPHA_MAX = 0.99f; // alpha cap (R-4)
 namespace gs {
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight,
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, int imode,
                        bool with_radius);
 PreOut pre_out_of(const Workspace &ws, bool with_radius);
 void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const float *means, const float *scales,
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
-                             int sh_stride, float scale_mod, int W, int H, bool tight);
+                             int sh_stride, float scale_mod, int W, int H, int imode);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
                    uint32_t &epoch, bool tight, float znear);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,

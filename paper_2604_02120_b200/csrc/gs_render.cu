@@ -170,7 +170,7 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
     const int e0 = mark(c, st, o);
     if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                          o.scale_modifier, cam, W, H, (o.flags & GS_FLAG_TIGHT) != 0, false);
+                          o.scale_modifier, cam, W, H, gs::intersect_mode(o.flags), false);
     c->launches += N > 0 ? 1 : 0;
     const int e1 = mark(c, st, o);
     enqueue_binning(c, c->ws, st, N, cam, W, H, o);
@@ -366,7 +366,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                              const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
                              int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of) {
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
-    const bool tight = (o.flags & GS_FLAG_TIGHT) != 0;
+    const int imode = gs::intersect_mode(o.flags);
     if (c->concurrent && G > 1 && !c->ev_pre) {
         if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming))) return rc;
         // the blends run on a high-priority stream: a blend gets every SM as soon as its
@@ -395,7 +395,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         if (N == 0)
             for (int j = 0; j < n; j++) cudaMemsetAsync(w[j]->counters, 0, sizeof(gs::Counters), st);
         gs::launch_preprocess_views(pv, st, N, means3D, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                                    o.scale_modifier, W, H, tight);
+                                    o.scale_modifier, W, H, imode);
         c->launches += N > 0 ? 1 : 0;
         int e_prev = mark(c, st, o);
         span(c, 0, e0, e_prev);
@@ -587,7 +587,7 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     gs::launch_preprocess(c->ws, st, N, means3D, scales, rots, opacity, shs, o->sh_degree, o->sh_stride,
-                          o->scale_modifier, *cam, W, H, (o->flags & GS_FLAG_TIGHT) != 0, true);
+                          o->scale_modifier, *cam, W, H, gs::intersect_mode(o->flags), true);
     c->last_counters = c->ws.counters;
     if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
     return finish(c, st, *o, N);

@@ -153,13 +153,46 @@ __device__ __forceinline__ void sh_colour(const float (&k)[48], int sh_degree, f
 // preprocess traffic is paid once per group instead of once per view. Per view the
 // operation order is the one of docs/preprocess_order.md (outputs bit-identical to a
 // single-view launch: the view-independent steps 2-4 are the same operations).
+// ln(t) for t >= 1 by a fixed sequence of IEEE +, -, *, / (bit-reproducible by the
+// oracle, unlike logf): t = 2^e m, m in [1, 2), ln t = e ln 2 + 2 atanh(s), s = (m-1)/(m+1)
+// in [0, 1/3), series to s^9 (truncation < 2e-6). docs/preprocess_order.md step 10b.
+__device__ __forceinline__ float ln_repro(float t) {
+    const uint32_t bits = __float_as_uint(t);
+    const float e = (float)((int)((bits >> 23) & 0xFFu) - 127);
+    const float m = __uint_as_float((bits & 0x7FFFFFu) | 0x3F800000u);
+    const float sn = (m - 1.0f) / (m + 1.0f);
+    const float s2 = sn * sn;
+    const float p = (((s2 * 0.11111111f + 0.14285715f) * s2 + 0.2f) * s2 + 0.33333334f) * s2 + 1.0f;
+    return e * 0.6931472f + 2.0f * (sn * p);
+}
+
+// Opacity-aware box (GS_FLAG_OBOX): a pixel p can have alpha >= 1/255 only
+// if d^T Q d <= lim = 2 (ln(255 o) + 5e-3) (Eq. 3 power, margin 5e-3 in ln alpha, 25x the
+// documented exponent error delta_a), i.e. inside the ellipse whose bounding box is
+// |dx| <= sqrt(lim a), |dy| <= sqrt(lim c) (a, c: the dilated 2-D covariance). The rect
+// becomes its intersection with that box (tiles whose pixel centres are all outside are
+// dropped): every dropped pair is alpha-skipped by the blend anyway, so frames are
+// bit-identical to the vanilla rect's. 255 o < 1.0 culls (alpha < 1/255 everywhere).
+__device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c, float op, int gx, int gy, int &xmin,
+                                            int &ymin, int &xmax, int &ymax) {
+    const float t = 255.0f * op;
+    if (!(t >= 1.0f)) return false;
+    const float lim = 2.0f * (ln_repro(t) + 5e-3f);
+    const float ex = sqrtf(lim * a), ey = sqrtf(lim * c);
+    xmin = max(xmin, rect_bound(floorf((mx - ex) * 0.0625f), gx));
+    xmax = min(xmax, rect_bound(floorf((mx + ex) * 0.0625f) + 1.0f, gx));
+    ymin = max(ymin, rect_bound(floorf((my - ey) * 0.0625f), gy));
+    ymax = min(ymax, rect_bound(floorf((my + ey) * 0.0625f) + 1.0f, gy));
+    return xmax > xmin && ymax > ymin;
+}
+
 __global__ void __launch_bounds__(PRE_THREADS, 2) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
                                                                const float4 *__restrict__ rots,
                                                                const float *__restrict__ opacity,
                                                                const float *__restrict__ shs, int sh_degree,
                                                                int sh_stride, float scale_mod, int W, int H,
-                                                               const PreViews pv, bool tight) {
+                                                               const PreViews pv, int imode) {
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0)   // the frames' device counters (no memset node: keeps PDL chained)
@@ -236,6 +269,8 @@ __global__ void __launch_bounds__(PRE_THREADS, 2) k_preprocess(int N, const floa
                 vis = (xmax - xmin) * (ymax - ymin) != 0;
             }
         }
+        const bool tight = imode == 1;
+        if (imode == 2 && vis) vis = opacity_box(mx, my, sxx, syy, op, gx, gy, xmin, ymin, xmax, ymax);
         uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
         if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
             unsigned long long m = 0ull;
@@ -297,23 +332,23 @@ PreOut pre_out_of(const Workspace &ws, bool with_radius) {
 
 void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const float *means, const float *scales,
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
-                             int sh_stride, float scale_mod, int W, int H, bool tight) {
+                             int sh_stride, float scale_mod, int W, int H, int imode) {
     if (N <= 0) return;
     launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
         N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
-        H, pv, tight);
+        H, pv, imode);
 }
 
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
-                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, bool tight,
+                       int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, int imode,
                        bool with_radius) {
     PreViews pv{};
     pv.n = 1;
     pv.cam[0] = cam;
     pv.out[0] = pre_out_of(ws, with_radius);
     launch_preprocess_views(pv, st, N, means, scales, rots, opacity, shs, sh_degree, sh_stride, scale_mod, W, H,
-                            tight);
+                            imode);
 }
 
 }  // namespace gs

@@ -13,7 +13,7 @@ def make_ctx(scene, cam, max_keys=None):
     return Context(0, max_points=max(scene.n, 1), max_keys=max_keys or (1 << 24), max_w=cam.W, max_h=cam.H)
 
 
-def gpu_preprocess(ctx, scene, cam, st=None):
+def gpu_preprocess(ctx, scene, cam, st=None, flags=0):
     import torch
     st = st or scene_to_device(scene)
     n = scene.n
@@ -23,7 +23,7 @@ def gpu_preprocess(ctx, scene, cam, st=None):
                 rect=torch.empty((n, 4), dtype=torch.int32, device=dev),
                 radius=torch.empty(n, dtype=torch.int32, device=dev),
                 touched=torch.empty(n, dtype=torch.int32, device=dev))
-    ctx.gs_debug_preprocess(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree), outs)
+    ctx.gs_debug_preprocess(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree, flags=flags), outs)
     torch.cuda.synchronize()
     out = {k: v.cpu().numpy() for k, v in outs.items()}
     out["touched"] = out["touched"].view(np.uint32)

@@ -230,29 +230,43 @@ def test_capacity_error_is_reported_not_truncated():
 
 
 @pytest.mark.slow
-def test_full_size_c5_view_sampled_parity():
-    """BASELINE.json configs[4] shape at full size (6M Gaussians, 1920x1080), the
-    launch configuration bench.py times: preprocess and binning bit-exact over
-    everything; pixels on 48 sampled tiles against the oracle."""
+@pytest.mark.parametrize("obox", [False, True], ids=["vanilla", "obox"])
+def test_full_size_c5_view_sampled_parity(obox):
+    """BASELINE.json configs[4] shape at full size (6M Gaussians, 1920x1080) in the
+    launch configuration bench.py times (gs_render_views, view group of 4, concurrent
+    binning chains; vanilla rect and GS_FLAG_OBOX): preprocess and binning bit-exact
+    over everything; the orbit's frame equals the single-view frame bit for bit;
+    pixels on 48 sampled tiles against the oracle."""
     import torch
-    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device
+    from paper_2604_02120_b200 import GS_FLAG_OBOX, Context, camera, opts, scene_to_device
+    flags = GS_FLAG_OBOX if obox else 0
     scene, cams, bg = synth.make_config("C5", views=64)
     cam = cams[0]
     ctx = Context(0, max_points=scene.n, max_keys=64 << 20, max_w=cam.W, max_h=cam.H)
     st = scene_to_device(scene)
-    got = gpu_preprocess(ctx, scene, cam, st)
-    pre = oracle.preprocess(scene, cam)
+    got = gpu_preprocess(ctx, scene, cam, st, flags=flags)
+    pre = oracle.preprocess(scene, cam, obox=obox)
     for k in BIT_EXACT_KEYS:
         a = got[k].view(np.uint32) if got[k].dtype == np.float32 else got[k].astype(np.int64)
         b = pre[k].view(np.uint32) if pre[k].dtype == np.float32 else pre[k].astype(np.int64)
-        assert np.array_equal(a, b), k
-    code, K, gb = gpu_binning(ctx, scene, cam, capacity=64 << 20, st=st)
+        vis = pre["touched"] > 0
+        assert np.array_equal(a[vis], b[vis]) and np.array_equal(got["touched"], pre["touched"]), k
+    code, K, gb = gpu_binning(ctx, scene, cam, capacity=64 << 20, st=st, flags=flags)
     assert code == 0
     ref_b = oracle.binning(pre, cam.W, cam.H)
     assert K == ref_b["K"]
     assert np.array_equal(gb["keys"], ref_b["keys"]) and np.array_equal(gb["vals"], ref_b["vals"])
     assert np.array_equal(gb["ranges"], ref_b["ranges"])
-    rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st)
+    rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=flags)
+    # the bench's path: 4 views in one group, chains concurrent; view 0 must match
+    ctx.gs_set_view_group(4, True)
+    orgb = torch.empty((4, 3, cam.H, cam.W), device="cuda")
+    oT = torch.empty((4, cam.H, cam.W), device="cuda")
+    ctx.gs_render_views(st, [camera(c) for c in cams[:4]], cam.W, cam.H,
+                        opts(bg, sh_degree=scene.sh_degree, flags=flags), orgb, oT)
+    torch.cuda.synchronize()
+    assert np.array_equal(orgb[0].cpu().numpy().astype(np.float64), rgb)
+    assert np.array_equal(oT[0].cpu().numpy().astype(np.float64), T)
     rng = np.random.default_rng(7)
     ntiles = len(ref_b["ranges"])
     sel = rng.choice(ntiles, 48, replace=False)
@@ -380,3 +394,36 @@ def test_mma_blend_is_bit_identical_across_batch_sizes(case):
     with pytest.raises(GsError):
         ctx.gs_render(st, camera(cam), cam.W, cam.H, opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA,
                                                           batch=48), r, t)
+
+
+# ---- GS_FLAG_OBOX: the opacity-aware box (docs/preprocess_order.md 10b) ----
+@pytest.mark.parametrize("case", list(CASES))
+def test_obox_preprocess_and_binning_bit_exact(case):
+    """With GS_FLAG_OBOX the rects, tiles_touched, sorted keys, values and tile ranges
+    are bit-exact against the oracle's step-10b preprocess and plain-definition binning."""
+    from paper_2604_02120_b200 import GS_FLAG_OBOX
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    got = gpu_preprocess(ctx, scene, cam, flags=GS_FLAG_OBOX)
+    pre = oracle.preprocess(scene, cam, obox=True)
+    vis = pre["touched"] > 0
+    assert np.array_equal(got["touched"], pre["touched"])
+    assert np.array_equal(got["rect"][vis], pre["rect"][vis])
+    code, K, b = gpu_binning(ctx, scene, cam, flags=GS_FLAG_OBOX)
+    assert code == 0
+    ref = oracle.binning(pre, cam.W, cam.H)
+    assert K == ref["K"]
+    assert np.array_equal(b["keys"], ref["keys"])
+    assert np.array_equal(b["vals"], ref["vals"])
+    assert np.array_equal(b["ranges"], ref["ranges"])
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_obox_renders_bit_identical(case):
+    """Dropped pairs are alpha-skipped anyway: the frame equals the vanilla-rect one."""
+    from paper_2604_02120_b200 import GS_FLAG_OBOX
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    a, ta = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC)
+    b, tb = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=GS_FLAG_OBOX)
+    assert np.array_equal(a, b) and np.array_equal(ta, tb)

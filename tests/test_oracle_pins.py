@@ -458,3 +458,51 @@ def test_end_to_end_single_gaussian_closed_form():
     a = np.where((alpha >= np.float32(1 / 255)) & inrect, alpha, 0.0)
     np.testing.assert_allclose(out["T"], 1 - a, rtol=0, atol=1e-6)
     np.testing.assert_allclose(out["rgb"][0], a * pre["rgb"][0, 0], rtol=0, atol=1e-6)
+
+
+# ---- step 10b: the opacity-aware box of GS_FLAG_OBOX -------------
+def test_ln_step10b_matches_the_natural_log():
+    """The fixed-operation ln (atanh series) is within 2e-6 of log on [1, 255]; the box
+    margin (5e-3 in ln alpha) dwarfs it."""
+    ts = np.concatenate([np.linspace(1.0, 255.0, 2001), 2.0 ** np.arange(0, 8), [1.0000001, 254.9999]])
+    err = max(abs(oracle.ln_step10b(float(np.float32(t))) - math.log(float(np.float32(t)))) for t in ts)
+    assert err < 2e-6, err
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_obox_lists_are_an_alpha_exact_ordered_subset(name):
+    """GS_FLAG_OBOX binning = the vanilla lists minus (Gaussian, tile) pairs whose alpha is
+    below 1/255 on every pixel of the tile (brute force in float64 from the splats), in the
+    vanilla order; Gaussians with 255*opacity < 1 are gone entirely."""
+    scene, cams, bg = synth.make_config(name)
+    cam = cams[0]
+    pre = oracle.preprocess(scene, cam)
+    pob = oracle.preprocess(scene, cam, obox=True)
+    for k in ("depth", "xy", "conic", "rgb"):   # only the rect (and culling) may change
+        vis = pob["touched"] > 0
+        assert np.array_equal(pre[k][vis], pob[k][vis])
+    assert not (pob["touched"][255.0 * pre["opacity"] < 1.0] > 0).any()
+    ref = oracle.binning(pre, cam.W, cam.H)
+    ob = oracle.binning(pob, cam.W, cam.H)
+    assert 0 < ob["K"] < ref["K"]
+    gx = (cam.W + 15) // 16
+    rng = np.random.default_rng(1)
+    tiles = np.nonzero(ref["ranges"][:, 1] > ref["ranges"][:, 0])[0]
+    n_dropped = 0
+    for t in rng.choice(tiles, min(40, len(tiles)), replace=False):
+        v_all = [int(v) for v in ref["vals"][ref["ranges"][t, 0]:ref["ranges"][t, 1]]]
+        v_ob = [int(v) for v in ob["vals"][ob["ranges"][t, 0]:ob["ranges"][t, 1]]]
+        kept = set(v_ob)
+        assert [v for v in v_all if v in kept] == v_ob
+        tx, ty = t % gx, t // gx
+        yy, xx = np.mgrid[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16]
+        for i in v_all:
+            if i in kept:
+                continue
+            n_dropped += 1
+            dx = float(pre["xy"][i, 0]) - xx
+            dy = float(pre["xy"][i, 1]) - yy
+            A, B, C = (float(c) for c in pre["conic"][i])
+            a = float(pre["opacity"][i]) * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
+            assert a.max() < (1.0 / 255.0) * math.exp(-0.004), (t, i, a.max())
+    assert n_dropped > 0
