@@ -219,6 +219,11 @@ int gs_debug_exponents(gs_ctx *ctx, void *stream, int N, const float *xy, const 
                        const float *opacity, const uint32_t *vals, int64_t K,
                        const uint32_t *ranges, int W, int H, float *out_m);
 
+/* Debug: the GS_FLAG_TIMING spans recorded since the last gs_stage_times (which
+ * clears them): out[3*i .. 3*i+2] = (stage 0/1/2, start ms, end ms), times relative
+ * to the first recorded event; *n_spans = count (at most max_spans). Synchronises. */
+int gs_debug_timeline(gs_ctx *ctx, double *out, int max_spans, int *n_spans);
+
 /* Debug: while `trace` is non-NULL, the tensor-core blend of CTA 0 records
  * clock64() timestamps of its per-batch pipeline events into trace[b*16 + e]
  * (b < 1024; e: 0/1 producer push begin/end, 2/3/4 builder got-raw /

@@ -33,18 +33,20 @@ struct gs_ctx {
     int64_t timed_frames = 0;
     // view groups (gs_render_views): per-view preprocess outputs + counters of views 1..G-1
     int view_group = gs::MAX_VIEW_GROUP;
-    gs::Workspace vws[gs::MAX_VIEW_GROUP] = {};
-    bool vws_alloc[gs::MAX_VIEW_GROUP] = {};
+    // slot s*MAX_VIEW_GROUP + j = view j of a group in slot set s (two sets: the preprocess of
+    // group g+1 runs while group g bins and blends); slot 0 is the context's own workspace
+    gs::Workspace vws[2 * gs::MAX_VIEW_GROUP] = {};
+    bool vws_alloc[2 * gs::MAX_VIEW_GROUP] = {};
     gs::Counters *last_counters = nullptr;   // counters of the last rendered view
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t group_done[2] = {}, copies_done[2] = {};
-    // gs_render_views: binning of slot v on bstream[v] (concurrent chains), joined by ev_binned[v]
+    // gs_render_views, concurrent mode: preprocess on pre_stream, the binning chain of view j
+    // of a group on bstream[j], blends on blend_stream (high priority); events per slot set
     bool concurrent = true;
-    cudaStream_t bstream[gs::MAX_VIEW_GROUP] = {};
-    cudaEvent_t ev_binned[gs::MAX_VIEW_GROUP] = {}, ev_pre = nullptr;
-    cudaStream_t blend_stream = nullptr;   // high priority
-    cudaEvent_t ev_blended = nullptr;
+    bool streams_ready = false;
+    cudaStream_t pre_stream = nullptr, blend_stream = nullptr, bstream[gs::MAX_VIEW_GROUP] = {};
+    cudaEvent_t ev_start = nullptr, ev_pre[2] = {}, ev_blended[2] = {}, ev_binned[2][gs::MAX_VIEW_GROUP] = {};
 };
 
 static constexpr int kMaxEvents = 4096;
@@ -323,15 +325,19 @@ int gs_ctx_destroy(gs_ctx *c) {
     free_ws(c->ws);
     for (void *p : {(void *)c->frame_rgb, (void *)c->frame_T})
         if (p) cudaFree(p);
-    for (int v = 1; v < gs::MAX_VIEW_GROUP; v++)
+    for (int v = 1; v < 2 * gs::MAX_VIEW_GROUP; v++)
         if (c->vws_alloc[v]) free_ws(c->vws[v]);
-    for (int v = 0; v < gs::MAX_VIEW_GROUP; v++) {
-        if (c->bstream[v]) cudaStreamDestroy(c->bstream[v]);
-        if (c->ev_binned[v]) cudaEventDestroy(c->ev_binned[v]);
+    for (int k = 0; k < 2; k++) {
+        for (int v = 0; v < gs::MAX_VIEW_GROUP; v++)
+            if (c->ev_binned[k][v]) cudaEventDestroy(c->ev_binned[k][v]);
+        if (c->ev_pre[k]) cudaEventDestroy(c->ev_pre[k]);
+        if (c->ev_blended[k]) cudaEventDestroy(c->ev_blended[k]);
     }
-    if (c->ev_pre) cudaEventDestroy(c->ev_pre);
-    if (c->ev_blended) cudaEventDestroy(c->ev_blended);
+    for (int v = 0; v < gs::MAX_VIEW_GROUP; v++)
+        if (c->bstream[v]) cudaStreamDestroy(c->bstream[v]);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
     if (c->blend_stream) cudaStreamDestroy(c->blend_stream);
+    if (c->pre_stream) cudaStreamDestroy(c->pre_stream);
     for (auto &e : c->ev) cudaEventDestroy(e);
     for (int k = 0; k < 2; k++) {
         if (c->group_done[k]) cudaEventDestroy(c->group_done[k]);
@@ -359,61 +365,96 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     return finish(c, st, *o, N);
 }
 
+// Optional per-group callbacks of render_views_impl (the host entry point's frame copies):
+// pre_blend(g) runs before group g's blends are enqueued, post_blend(g) right after, both
+// with the stream the blends run on.
+struct GroupHooks {
+    void *user;
+    void (*pre_blend)(void *user, cudaStream_t bl, int g);
+    void (*post_blend)(void *user, cudaStream_t bl, int g, int v0, int n);
+};
+
+static int ensure_streams(gs_ctx *c) {
+    if (c->streams_ready) return GS_OK;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaError_t e = cudaStreamCreateWithPriority(&c->pre_stream, cudaStreamNonBlocking, lo);
+    // the blends run on a high-priority stream: a blend gets the SMs as soon as its chain is done
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->blend_stream, cudaStreamNonBlocking, hi);
+    for (int j = 0; j < gs::MAX_VIEW_GROUP && e == cudaSuccess; j++)
+        e = cudaStreamCreateWithPriority(&c->bstream[j], cudaStreamNonBlocking, lo);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+    for (int k = 0; k < 2 && e == cudaSuccess; k++) {
+        e = cudaEventCreateWithFlags(&c->ev_pre[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_blended[k], cudaEventDisableTiming);
+        for (int j = 0; j < gs::MAX_VIEW_GROUP && e == cudaSuccess; j++)
+            e = cudaEventCreateWithFlags(&c->ev_binned[k][j], cudaEventDisableTiming);
+    }
+    if (int rc = check_cuda(e)) return rc;
+    c->streams_ready = true;
+    return GS_OK;
+}
+
 // n views of one scene in groups of view_group: one preprocess launch reads the scene
-// once per group (k_preprocess), then each view is binned and blended in turn (the
-// binning buffers are shared, the per-view preprocess outputs are not).
+// once per group (k_preprocess), then each view is binned and blended (P:109-117 per view).
+// Concurrent mode (default) is a three-stream software pipeline over two slot sets:
+//   pre_stream:   pre(g) into slot set g%2, after the blends of group g-2 released it
+//   bstream[j]:   binning chain of view j of group g, after pre(g) (the chains of a group
+//                 run concurrently: they are latency-bound chains of small kernels)
+//   blend_stream: blend of view j of group g, after chain (g, j)
+// so pre(g+1) overlaps the chains and blends of group g. The caller's stream is joined at
+// both ends (its earlier work before pre(0), the last blend before its later work).
+// Serial mode runs everything on the caller's stream with slot set 0.
 static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *means3D, const float *scales,
                              const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
-                             int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of) {
+                             int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of,
+                             const GroupHooks *hk = nullptr) {
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     const int imode = gs::intersect_mode(o.flags);
-    if (c->concurrent && G > 1 && !c->ev_pre) {
-        if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_pre, cudaEventDisableTiming))) return rc;
-        // the blends run on a high-priority stream: a blend gets every SM as soon as its
-        // chain is done; the other chains fill what the blend leaves
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (int rc = check_cuda(cudaStreamCreateWithPriority(&c->blend_stream, cudaStreamNonBlocking, hi))) return rc;
-        if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_blended, cudaEventDisableTiming))) return rc;
-        for (int j = 0; j < gs::MAX_VIEW_GROUP; j++) {
-            if (int rc = check_cuda(cudaStreamCreateWithPriority(&c->bstream[j], cudaStreamNonBlocking, lo)))
-                return rc;
-            if (int rc = check_cuda(cudaEventCreateWithFlags(&c->ev_binned[j], cudaEventDisableTiming))) return rc;
-        }
+    const bool conc = c->concurrent && G > 1;
+    if (conc) {
+        if (int rc = ensure_streams(c)) return rc;
+        cudaEventRecord(c->ev_start, st);
+        cudaStreamWaitEvent(c->pre_stream, c->ev_start, 0);
+        cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
     }
-    for (int v0 = 0; v0 < n_views; v0 += G) {
+    int last_set = 0;
+    for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
         const int n = std::min(G, n_views - v0);
+        const int set = conc ? (g & 1) : 0;
+        last_set = set;
         gs::PreViews pv{};
         pv.n = n;
         gs::Workspace *w[gs::MAX_VIEW_GROUP];
         for (int j = 0; j < n; j++) {
-            if (int rc = view_ws(c, j, &w[j])) return rc;
+            if (int rc = view_ws(c, set * gs::MAX_VIEW_GROUP + j, &w[j])) return rc;
             pv.cam[j] = cams[v0 + j];
             pv.out[j] = gs::pre_out_of(*w[j], false);
         }
-        const int e0 = mark(c, st, o);
+        cudaStream_t ps = conc ? c->pre_stream : st;
+        if (conc && g >= 2) cudaStreamWaitEvent(ps, c->ev_blended[set], 0);   // slot set free again
+        const int e0 = mark(c, ps, o);
         if (N == 0)
-            for (int j = 0; j < n; j++) cudaMemsetAsync(w[j]->counters, 0, sizeof(gs::Counters), st);
-        gs::launch_preprocess_views(pv, st, N, means3D, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
+            for (int j = 0; j < n; j++) cudaMemsetAsync(w[j]->counters, 0, sizeof(gs::Counters), ps);
+        gs::launch_preprocess_views(pv, ps, N, means3D, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
                                     o.scale_modifier, W, H, imode);
         c->launches += N > 0 ? 1 : 0;
-        int e_prev = mark(c, st, o);
+        int e_prev = mark(c, ps, o);
         span(c, 0, e0, e_prev);
-        if (c->concurrent && n > 1) {
-            // the views' binning chains run concurrently, one stream each (they are
-            // latency-bound chains of small kernels); blend j waits for chain j only
-            cudaEventRecord(c->ev_pre, st);
+        if (conc) {
+            cudaEventRecord(c->ev_pre[set], ps);
             for (int j = 0; j < n; j++) {
                 cudaStream_t bs = c->bstream[j];
-                cudaStreamWaitEvent(bs, c->ev_pre, 0);
+                cudaStreamWaitEvent(bs, c->ev_pre[set], 0);
                 const int b0 = mark(c, bs, o);
                 enqueue_binning(c, *w[j], bs, N, cams[v0 + j], W, H, o);
                 span(c, 1, b0, mark(c, bs, o));
-                cudaEventRecord(c->ev_binned[j], bs);
+                cudaEventRecord(c->ev_binned[set][j], bs);
             }
             cudaStream_t bl = c->blend_stream;
+            if (hk && hk->pre_blend) hk->pre_blend(hk->user, bl, g);
             for (int j = 0; j < n; j++) {
-                cudaStreamWaitEvent(bl, c->ev_binned[j], 0);
+                cudaStreamWaitEvent(bl, c->ev_binned[set][j], 0);
                 const int e1 = mark(c, bl, o);
                 enqueue_blend(c, *w[j], bl, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H,
                               o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
@@ -422,10 +463,11 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                 if (e2 >= 0) c->timed_frames++;
                 c->last_counters = w[j]->counters;
             }
-            cudaEventRecord(c->ev_blended, bl);
-            cudaStreamWaitEvent(st, c->ev_blended, 0);   // the frames are complete in stream order of st
+            if (hk && hk->post_blend) hk->post_blend(hk->user, bl, g, v0, n);
+            cudaEventRecord(c->ev_blended[set], bl);
             continue;
         }
+        if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, g);
         for (int j = 0; j < n; j++) {
             enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
             const int e1 = mark(c, st, o);
@@ -438,6 +480,11 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             if (e2 >= 0) c->timed_frames++;
             c->last_counters = w[j]->counters;
         }
+        if (hk && hk->post_blend) hk->post_blend(hk->user, st, g, v0, n);
+    }
+    if (conc) {   // the frames are complete in the caller's stream order
+        cudaStreamWaitEvent(st, c->ev_blended[last_set], 0);
+        cudaStreamWaitEvent(st, c->ev_blended[last_set ^ 1], 0);
     }
     return GS_OK;
 }
@@ -506,37 +553,70 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
     cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, st);
-    // Frames come back on a second stream, one view group behind: group g renders into
-    // staging slot g % 2 while the frames of group g - 1 are copied device -> host.
+    // Frames come back on the copy stream, one view group behind: group g renders into
+    // staging slot g % 2 (G frames) while the frames of group g - 1 are copied to the host.
     const size_t plane = (size_t)W * H, mplane = (size_t)c->max_w * c->max_h;
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     gs_opts ov = *o;
     ov.flags &= ~GS_FLAG_SYNC;
-    for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
-        const int n = std::min(G, n_views - v0), slot = g & 1;
-        if (g >= 2) cudaStreamWaitEvent(st, c->copies_done[slot], 0);   // staging slot free again
-        float *prgb[gs::MAX_VIEW_GROUP], *pT[gs::MAX_VIEW_GROUP];
-        for (int j = 0; j < n; j++) {
-            prgb[j] = c->frame_rgb + (size_t)(slot * gs::MAX_VIEW_GROUP + j) * 3 * mplane;
-            pT[j] = c->frame_T + (size_t)(slot * gs::MAX_VIEW_GROUP + j) * mplane;
-        }
-        if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams + v0, n, W, H, ov, prgb, pT)) return rc;
-        cudaEventRecord(c->group_done[slot], st);
-        cudaStreamWaitEvent(c->copy_stream, c->group_done[slot], 0);
-        for (int j = 0; j < n; j++) {
-            cudaMemcpyAsync(h_out_rgb + (size_t)(v0 + j) * 3 * plane, prgb[j], 3 * plane * 4, cudaMemcpyDeviceToHost,
-                            c->copy_stream);
-            cudaMemcpyAsync(h_out_T + (size_t)(v0 + j) * plane, pT[j], plane * 4, cudaMemcpyDeviceToHost,
-                            c->copy_stream);
-        }
-        cudaEventRecord(c->copies_done[slot], c->copy_stream);
+    std::vector<float *> prgb(n_views), pT(n_views);
+    for (int v = 0; v < n_views; v++) {
+        const size_t slot = (size_t)(((v / G) & 1) * gs::MAX_VIEW_GROUP + v % G);
+        prgb[v] = c->frame_rgb + slot * 3 * mplane;
+        pT[v] = c->frame_T + slot * mplane;
     }
+    struct Copies {
+        gs_ctx *c;
+        float *h_rgb, *h_T;
+        float *const *prgb, *const *pT;
+        size_t plane;
+    } cp{c, h_out_rgb, h_out_T, prgb.data(), pT.data(), plane};
+    GroupHooks hk;
+    hk.user = &cp;
+    hk.pre_blend = [](void *u, cudaStream_t bl, int g) {
+        Copies &k = *static_cast<Copies *>(u);
+        if (g >= 2) cudaStreamWaitEvent(bl, k.c->copies_done[g & 1], 0);   // staging slot free again
+    };
+    hk.post_blend = [](void *u, cudaStream_t bl, int g, int v0, int n) {
+        Copies &k = *static_cast<Copies *>(u);
+        cudaEventRecord(k.c->group_done[g & 1], bl);
+        cudaStreamWaitEvent(k.c->copy_stream, k.c->group_done[g & 1], 0);
+        for (int v = v0; v < v0 + n; v++) {
+            cudaMemcpyAsync(k.h_rgb + (size_t)v * 3 * k.plane, k.prgb[v], 3 * k.plane * 4, cudaMemcpyDeviceToHost,
+                            k.c->copy_stream);
+            cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost,
+                            k.c->copy_stream);
+        }
+        cudaEventRecord(k.c->copies_done[g & 1], k.c->copy_stream);
+    };
+    if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams, n_views, W, H, ov, prgb.data(), pT.data(),
+                                   &hk))
+        return rc;
     int rc = check_cuda(cudaStreamSynchronize(c->copy_stream));
     if (!rc) rc = check_cuda(cudaStreamSynchronize(st));
     if (rc) return rc;
     gs_opts os = *o;
     os.flags |= GS_FLAG_SYNC;
     return finish(c, st, os, N);
+}
+
+int gs_debug_timeline(gs_ctx *c, double *out, int max_spans, int *n_spans) {
+    if (!c || !out || !n_spans || max_spans < 0) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    int n = 0;
+    for (const auto &sp : c->spans) cudaEventSynchronize(c->ev[sp.e1]);
+    for (const auto &sp : c->spans) {
+        if (n >= max_spans) break;
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, c->ev[0], c->ev[sp.e0]);
+        cudaEventElapsedTime(&t1, c->ev[0], c->ev[sp.e1]);
+        out[3 * n] = sp.stage;
+        out[3 * n + 1] = t0;
+        out[3 * n + 2] = t1;
+        n++;
+    }
+    *n_spans = n;
+    return check_cuda(cudaGetLastError());
 }
 
 int gs_set_view_group(gs_ctx *c, int g, int concurrent) {
