@@ -52,7 +52,11 @@ namespace gs {
 #ifndef GS_BLEND_CH
 #define GS_BLEND_CH 16
 #endif
-constexpr int NB = 32;                  // Gaussians per batch (MMA N)
+#ifndef GS_BLEND_NB
+#define GS_BLEND_NB 32
+#endif
+constexpr int NB = GS_BLEND_NB;         // Gaussians per batch (MMA N: 16 or 32)
+static_assert(NB == 16 || NB == 32, "batch = MMA N = 16 or 32 (one producer / builder lane per Gaussian)");
 constexpr int CH = GS_BLEND_CH;         // TMEM columns per compositor load (16 or 32)
 constexpr int STAGES = GS_BLEND_STAGES; // M_g / TMEM ring depth
 constexpr int NCW = 8;                  // compositor warps: 256 pixels
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 if (!DUMP && tile_done(sm, lane, (uint32_t)hd.y)) hd.z = -1;   // tile already terminated
             }
             if (hd.z > 0) {
-                build_row(sm, s, slot, hd, sm.raw[r][lane], lane, gx);
+                if (lane < NB) build_row(sm, s, slot, hd, sm.raw[r][lane], lane, gx);
                 fence_proxy_async_smem();
             }
             if (lane == 0) sm.hdr[slot] = hd;

@@ -17,6 +17,7 @@ ap.add_argument("--frames", type=int, default=3)
 ap.add_argument("--view", type=int, default=0)
 ap.add_argument("--blend", default="tc", choices=["tc", "direct", "mma"])
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--obox", action="store_true")
 ap.add_argument("--group", type=int, default=0, help="render views [view, view+group) with gs_render_views "
                 "(one view-group preprocess launch, chains serialised on one stream) instead of gs_render")
 a = ap.parse_args()
@@ -26,7 +27,7 @@ ctx = Context(0, max_points=scene.n, max_keys=48 << 20, max_w=cam.W, max_h=cam.H
 st = scene_to_device(scene)
 rgb = torch.empty((3, cam.H, cam.W), device="cuda")
 T = torch.empty((cam.H, cam.W), device="cuda")
-o = opts(bg, sh_degree=scene.sh_degree, batch=a.batch,
+o = opts(bg, sh_degree=scene.sh_degree, batch=a.batch, flags=16 if a.obox else 0,
          blend={"tc": GS_BLEND_TC, "direct": GS_BLEND_DIRECT, "mma": GS_BLEND_MMA}[a.blend])
 if a.group:
     ctx.gs_set_view_group(a.group, False)
