@@ -151,7 +151,7 @@ def run_ours(args):
 
     from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
                                        Context, camera, opts, scene_to_device, scene_to_host, synth)
-    from paper_2604_02120_b200.orbit import gather_frames, partition_views
+    from paper_2604_02120_b200.orbit import gather_frames_pipelined, partition_views
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     if ws > 1:
@@ -172,9 +172,15 @@ def run_ours(args):
     o_timed = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=GS_FLAG_TIMING | base_flags)
     stream = torch.cuda.current_stream()
 
+    gather_out = None
+    if ws > 1 and rank == 0:   # receive buffers of the frame gather, allocated once (untimed)
+        gather_out = (torch.empty((ws, per, 3, H, W), device="cuda"), torch.empty((ws, per, H, W), device="cuda"))
+
     def step(o):
         ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
-        gather_frames(out_rgb, out_T, ws, rank, dist)    # NCCL frame gather to rank 0
+        # NCCL frame gather to rank 0, view group by view group as the groups finish
+        gather_frames_pipelined(out_rgb, out_T, ws, rank, VIEW_GROUP,
+                                wait_group=lambda s, g: ctx.gs_stream_wait_group(s, g), dist=dist, out=gather_out)
 
     for _ in range(args.warmup):
         step(o_plain)

@@ -164,6 +164,14 @@ int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
  * GS_ERR_INVALID_ARG for g outside 1..4. */
 int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
 
+/* Makes `stream` wait (device-side, cudaStreamWaitEvent) until view group g of
+ * the last gs_render_views / gs_render_views_host call has finished blending,
+ * i.e. until frames [g*G, min(n_views, (g+1)*G)) are complete (G = the view
+ * group size in effect for that call). Lets a consumer of the frames -- the
+ * NCCL frame gather of the multi-GPU orbit -- start on early groups while later
+ * ones still render. GS_ERR_INVALID_ARG if g is not a group of that call. */
+int gs_stream_wait_group(gs_ctx *ctx, void *stream, int g);
+
 /* Synchronises the last stream used by ctx and reports counts and the status
  * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */
 int gs_last_stats(gs_ctx *ctx, gs_stats *out);

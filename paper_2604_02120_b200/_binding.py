@@ -37,7 +37,7 @@ GS_FLAG_OBOX = 16
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
            "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times",
-           "gs_debug_set_trace", "gs_set_view_group", "gs_debug_timeline")
+           "gs_debug_set_trace", "gs_set_view_group", "gs_debug_timeline", "gs_stream_wait_group")
 
 
 class GsError(RuntimeError):
@@ -95,6 +95,7 @@ def load():
         "gs_stage_times": [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)],
         "gs_debug_set_trace": [P, P],
         "gs_set_view_group": [P, I, I],
+        "gs_stream_wait_group": [P, P, I],
         "gs_debug_timeline": [P, ctypes.POINTER(ctypes.c_double), I, ctypes.POINTER(I)],
     }
     for name, args in sig.items():
@@ -212,6 +213,11 @@ class Context:
         n = ctypes.c_int(0)
         _check(self.lib.gs_debug_timeline(self.h, buf, max_spans, ctypes.byref(n)), "gs_debug_timeline")
         return [(int(buf[3 * i]), buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+    def gs_stream_wait_group(self, stream, g):
+        """Device-side wait of `stream` (torch.cuda.Stream) for view group g of the last
+        gs_render_views call."""
+        _check(self.lib.gs_stream_wait_group(self.h, _stream(stream), int(g)), "gs_stream_wait_group")
 
     def gs_set_view_group(self, g, concurrent=True):
         _check(self.lib.gs_set_view_group(self.h, int(g), int(bool(concurrent))), "gs_set_view_group")

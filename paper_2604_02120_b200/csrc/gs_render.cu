@@ -47,6 +47,11 @@ struct gs_ctx {
     bool streams_ready = false;
     cudaStream_t pre_stream = nullptr, blend_stream = nullptr, bstream[gs::MAX_VIEW_GROUP] = {};
     cudaEvent_t ev_start = nullptr, ev_pre[2] = {}, ev_blended[2] = {}, ev_binned[2][gs::MAX_VIEW_GROUP] = {};
+    // one event per view group of the last gs_render_views call, recorded after the group's
+    // blends (gs_stream_wait_group: a consumer of the frames, e.g. the NCCL frame gather,
+    // starts on group g while later groups still render)
+    std::vector<cudaEvent_t> ev_group;
+    int n_groups = 0;
 };
 
 static constexpr int kMaxEvents = 4096;
@@ -336,6 +341,7 @@ int gs_ctx_destroy(gs_ctx *c) {
     for (int v = 0; v < gs::MAX_VIEW_GROUP; v++)
         if (c->bstream[v]) cudaStreamDestroy(c->bstream[v]);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
+    for (auto e : c->ev_group) cudaEventDestroy(e);
     if (c->blend_stream) cudaStreamDestroy(c->blend_stream);
     if (c->pre_stream) cudaStreamDestroy(c->pre_stream);
     for (auto &e : c->ev) cudaEventDestroy(e);
@@ -373,6 +379,16 @@ struct GroupHooks {
     void (*pre_blend)(void *user, cudaStream_t bl, int g);
     void (*post_blend)(void *user, cudaStream_t bl, int g, int v0, int n);
 };
+
+static int record_group(gs_ctx *c, cudaStream_t s, int g) {
+    while ((int)c->ev_group.size() <= g) {
+        cudaEvent_t e = nullptr;
+        if (int rc = check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return rc;
+        c->ev_group.push_back(e);
+    }
+    c->n_groups = g + 1;
+    return check_cuda(cudaEventRecord(c->ev_group[g], s));
+}
 
 static int ensure_streams(gs_ctx *c) {
     if (c->streams_ready) return GS_OK;
@@ -465,6 +481,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             }
             if (hk && hk->post_blend) hk->post_blend(hk->user, bl, g, v0, n);
             cudaEventRecord(c->ev_blended[set], bl);
+            if (int rc = record_group(c, bl, g)) return rc;
             continue;
         }
         if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, g);
@@ -481,6 +498,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             c->last_counters = w[j]->counters;
         }
         if (hk && hk->post_blend) hk->post_blend(hk->user, st, g, v0, n);
+        if (int rc = record_group(c, st, g)) return rc;
     }
     if (conc) {   // the frames are complete in the caller's stream order
         cudaStreamWaitEvent(st, c->ev_blended[last_set], 0);
@@ -617,6 +635,12 @@ int gs_debug_timeline(gs_ctx *c, double *out, int max_spans, int *n_spans) {
     }
     *n_spans = n;
     return check_cuda(cudaGetLastError());
+}
+
+int gs_stream_wait_group(gs_ctx *c, void *stream, int g) {
+    if (!c || g < 0 || g >= c->n_groups) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    return check_cuda(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), c->ev_group[g], 0));
 }
 
 int gs_set_view_group(gs_ctx *c, int g, int concurrent) {

@@ -34,3 +34,48 @@ def gather_frames(rgb, T, world: int, rank: int, dist=None):
     if rank != 0:
         return None, None
     return torch.cat(lr, 0), torch.cat(lt, 0)
+
+
+def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_group=None, dist=None, out=None):
+    """gather_frames, one view group at a time, overlapped with the rendering.
+
+    rgb [per,3,H,W] / T [per,H,W] are this rank's frames, rendered in view groups of
+    `group` by gs_render_views. For each group g, `wait_group(stream, g)` (the C-ABI's
+    gs_stream_wait_group) makes a side stream wait until that group has finished
+    blending, and an asynchronous NCCL gather of the group's frames is issued on it,
+    so the transfer of group g overlaps the rendering of groups g+1, ... The current
+    stream waits for every gather before returning. `out`: optional preallocated
+    (rgb_all [world,per,3,H,W], T_all [world,per,H,W]) receive buffers on rank 0.
+    Returns (rgb_all [world*per,3,H,W], T_all [world*per,H,W]) on rank 0 (view order:
+    ranks own contiguous view blocks), (None, None) elsewhere."""
+    import contextlib
+
+    import torch
+    if world == 1:
+        return rgb, T
+    if dist is None:
+        import torch.distributed as dist
+    per = rgb.shape[0]
+    if rank == 0:
+        if out is None:
+            out = (torch.empty((world,) + tuple(rgb.shape), dtype=rgb.dtype, device=rgb.device),
+                   torch.empty((world,) + tuple(T.shape), dtype=T.dtype, device=T.device))
+        all_rgb, all_T = out
+    side = torch.cuda.Stream(device=rgb.device) if rgb.is_cuda else None
+    works = []
+    for g0 in range(0, per, group):
+        sl = slice(g0, min(per, g0 + group))
+        if wait_group is not None and side is not None:
+            wait_group(side, g0 // group)
+        with (torch.cuda.stream(side) if side is not None else contextlib.nullcontext()):
+            lr = [all_rgb[r, sl] for r in range(world)] if rank == 0 else None
+            lt = [all_T[r, sl] for r in range(world)] if rank == 0 else None
+            works.append(dist.gather(rgb[sl], lr, dst=0, async_op=True))
+            works.append(dist.gather(T[sl], lt, dst=0, async_op=True))
+    for w in works:
+        w.wait()
+    if side is not None:
+        torch.cuda.current_stream(rgb.device).wait_stream(side)
+    if rank != 0:
+        return None, None
+    return all_rgb.view((world * per,) + tuple(rgb.shape[1:])), all_T.view((world * per,) + tuple(T.shape[1:]))

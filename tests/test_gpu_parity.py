@@ -427,3 +427,31 @@ def test_obox_renders_bit_identical(case):
     a, ta = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC)
     b, tb = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=GS_FLAG_OBOX)
     assert np.array_equal(a, b) and np.array_equal(ta, tb)
+
+
+def test_stream_wait_group_orders_frame_consumers():
+    """gs_stream_wait_group(stream, g): a side stream that waits for view group g sees
+    the finished frames of that group (the multi-GPU gather consumes frames this way);
+    groups outside the last call are rejected."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device
+    scene = synth.unbounded_scene(40000, 109, sh_degree=3)
+    cams = synth.orbit_cameras(7, 256, 160, 1.0)
+    ctx = Context(0, max_points=scene.n, max_keys=1 << 22, max_w=256, max_h=160)
+    ctx.gs_set_view_group(3, True)
+    st = scene_to_device(scene)
+    o = opts((0.0, 0.0, 0.0), sh_degree=3)
+    r = torch.full((7, 3, 160, 256), float("nan"), device="cuda")
+    t = torch.full((7, 160, 256), float("nan"), device="cuda")
+    side = torch.cuda.Stream()
+    copies = torch.empty_like(r)
+    ctx.gs_render_views(st, [camera(c) for c in cams], 256, 160, o, r, t)
+    for g in range(3):
+        ctx.gs_stream_wait_group(side, g)
+        with torch.cuda.stream(side):
+            copies[3 * g:3 * g + 3].copy_(r[3 * g:3 * g + 3])
+    torch.cuda.synchronize()
+    assert torch.equal(copies, r) and not torch.isnan(r).any()
+    with pytest.raises(GsError):
+        ctx.gs_stream_wait_group(side, 3)
+    ctx.close()

@@ -7,7 +7,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_02120_b200.orbit import gather_frames, partition_views
+from paper_2604_02120_b200.orbit import gather_frames, gather_frames_pipelined, partition_views
 
 
 def test_partition_covers_views_once():
@@ -36,8 +36,13 @@ def _worker(rank, world, port, q):
     rgb = torch.stack([torch.full((3, H, W), float(v)) for v in views])
     T = torch.stack([torch.full((H, W), -float(v)) for v in views])
     a, b = gather_frames(rgb, T, world, rank)
+    # the group-pipelined gather (views in groups of 3: a ragged last group)
+    c, d = gather_frames_pipelined(rgb, T, world, rank, 3)
     if rank == 0:
+        assert torch.equal(a, c) and torch.equal(b, d)
         q.put((a.clone(), b.clone()))
+    else:
+        assert c is None and d is None
     dist.barrier()
     dist.destroy_process_group()
 
