@@ -336,6 +336,30 @@ def run_ours(args):
                     "n_keys_view0": ts.n_keys, "pairs_evaluated_view0": ts.pairs_evaluated,
                     "note": INTERSECT[mode][1] + "; frames bit-identical to the vanilla-rect ones (tested)"}
 
+    # --- SURVEY 8(e) option: tile-row split of ONE view. Per-band device time of band k
+    # of n (what each of n GPUs would render; the band gather is not included) ---
+    row_split = None
+    if not args.no_ab and ws == 1:
+        row_split = {}
+        c0 = my_cams[0]
+        for nb in (1, 2, 4, 8):
+            worst = 0.0
+            for k in range(nb):
+                o_b = opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=base_flags, band=k, n_bands=nb)
+                for _ in range(2):
+                    ctx.gs_render(st, c0, W, H, o_b, out_rgb[0], out_T[0], stream)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(5):
+                    ctx.gs_render(st, c0, W, H, o_b, out_rgb[0], out_T[0], stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                worst = max(worst, e0.elapsed_time(e1) / 5)
+            row_split[f"{nb}_bands"] = {"max_band_ms": worst, "speedup_vs_1": None}
+        for v in row_split.values():
+            v["speedup_vs_1"] = row_split["1_bands"]["max_band_ms"] / v["max_band_ms"]
+
     # --- N2: resolution sensitivity (1x / 2x / 3x of 1080p, same scene, orbit views) ---
     res_sweep = None
     if not args.no_sweep and ws == 1:
@@ -411,7 +435,7 @@ def run_ours(args):
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
                 "roofline": roof, "stages": stages, "clocks": clk,
-                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3,
+                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3, "row_split_one_view": row_split,
                 "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
                                    "pairs_kept": n_kept}}

@@ -99,6 +99,12 @@ typedef struct {
     int batch;             /* GS_BLEND_MMA: Gaussians per shared-memory batch, 32/64/128/256
                             * (0 = 256); output bit-identical for every value. The
                             * tcgen05 blend streams fixed 32-Gaussian batches (ignored). */
+    int band, n_bands;     /* row band of a split frame (SURVEY 8(e) option): n_bands > 1
+                            * renders only tile rows [band*gy/n_bands, (band+1)*gy/n_bands)
+                            * (gy = ceil(H/16)); pixels of the other bands are not written,
+                            * the band's pixels are bit-identical to the full frame's. The
+                            * preprocess still projects every Gaussian; binning and blending
+                            * only cover the band. n_bands <= 1: the whole frame. */
 } gs_opts;
 
 typedef struct {

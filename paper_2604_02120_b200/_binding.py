@@ -56,7 +56,7 @@ class gs_camera(ctypes.Structure):
 class gs_opts(ctypes.Structure):
     _fields_ = [("bg", ctypes.c_float * 3), ("sh_degree", ctypes.c_int), ("sh_stride", ctypes.c_int),
                 ("scale_modifier", ctypes.c_float), ("blend", ctypes.c_int), ("flags", ctypes.c_uint),
-                ("batch", ctypes.c_int)]
+                ("batch", ctypes.c_int), ("band", ctypes.c_int), ("n_bands", ctypes.c_int)]
 
 
 class gs_stats(ctypes.Structure):
@@ -130,7 +130,7 @@ def camera(cam) -> gs_camera:
 
 
 def opts(bg=(0.0, 0.0, 0.0), sh_degree=3, sh_stride=None, scale_modifier=1.0, blend=GS_BLEND_TC, flags=0,
-         batch=0):
+         batch=0, band=0, n_bands=0):
     o = gs_opts()
     o.bg[:] = [float(v) for v in bg]
     o.sh_degree = int(sh_degree)
@@ -139,6 +139,8 @@ def opts(bg=(0.0, 0.0, 0.0), sh_degree=3, sh_stride=None, scale_modifier=1.0, bl
     o.blend = int(blend)
     o.flags = int(flags)
     o.batch = int(batch)
+    o.band = int(band)
+    o.n_bands = int(n_bands)
     return o
 
 

@@ -201,8 +201,8 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
 template <bool DUMP, bool STATS, bool TRACE>
 __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
-               const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W,
-               int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
+               const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
+               int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
                unsigned long long *stat_kept, long long *trace) {
     extern __shared__ uint8_t smem_raw[];
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         uint32_t b_idx = 0;
         unsigned long long n_eval = 0;
         int tile = 0;
-        if (lane == 0) tile = (int)atomicAdd(tile_queue, 1u);
+        if (lane == 0) tile = tile0 + (int)atomicAdd(tile_queue, 1u);   // tiles [tile0, ntiles)
         tile = __shfl_sync(0xffffffffu, tile, 0);
         uint2 rg = tile < ntiles ? ranges[tile] : make_uint2(0u, 0u);
         uint32_t seq = 1;
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         auto head_step = [&]() {
             switch (hstate) {
                 case 0:
-                    if (lane == 0) ntile_l0 = (int)atomicAdd(tile_queue, 1u);
+                    if (lane == 0) ntile_l0 = tile0 + (int)atomicAdd(tile_queue, 1u);
                     break;
                 case 1:
                     ntile = __shfl_sync(0xffffffffu, ntile_l0, 0);
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
 long long *g_blend_trace = nullptr;   // set by gs_debug_set_trace (debug only)
 
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
+                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats) {
     const size_t smem = sizeof(SmemTC) + 1024;
@@ -506,10 +506,10 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
         cudaFuncSetAttribute(k_blend_tc<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    const int grid = std::max(1, std::min(GS_BLEND_MINB * num_sms, ntiles));
+    const int grid = std::max(1, std::min(GS_BLEND_MINB * num_sms, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
-#define ARGS xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
+#define ARGS xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
         launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
     else if (stats)
@@ -527,14 +527,14 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
 // ===========================================================================
 __global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o,
                                                       const float4 *__restrict__ rgb, const uint32_t *__restrict__ vals,
-                                                      const uint2 *__restrict__ ranges, int gx, int W, int H,
+                                                      const uint2 *__restrict__ ranges, int tile0, int gx, int W, int H,
                                                       float bg0, float bg1, float bg2, float *__restrict__ out_rgb,
                                                       float *__restrict__ out_T) {
     pdl_wait();
     __shared__ float4 s_g[256];     // (x, y, A, B)
     __shared__ float2 s_g2[256];    // (C, log2 o)
     __shared__ float4 s_c[256];
-    const int tile = blockIdx.x;
+    const int tile = tile0 + blockIdx.x;
     const int p = threadIdx.x;
     int x, y;
     pixel_of(p, x, y);
@@ -581,10 +581,10 @@ __global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__
 }
 
 void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
+                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *) {
-    if (ntiles <= 0) return;
-    launch_pdl(k_blend_direct, ntiles, 256, 0, st, xy, conic_o, rgb, vals, ranges, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
+    if (ntiles - tile0 <= 0) return;
+    launch_pdl(k_blend_direct, ntiles - tile0, 256, 0, st, xy, conic_o, rgb, vals, ranges, tile0, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
                                            out_T);
 }
 
@@ -647,8 +647,8 @@ __device__ __forceinline__ uint32_t mp_word(int x, int y, int k) {
 template <int BATCH>
 __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
     k_blend_mma(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
-                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int ntiles, int gx, int W, int H,
-                float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
+                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
+                int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                 uint32_t *tile_queue) {
     extern __shared__ uint8_t smem_raw[];
     SmemMMA<BATCH> &sm = *reinterpret_cast<SmemMMA<BATCH> *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
     float *tr = sm.tr[warp];
     pdl_wait();
     for (;;) {
-        if (threadIdx.x == 0) sm.tile = (int)atomicAdd(tile_queue, 1u);
+        if (threadIdx.x == 0) sm.tile = tile0 + (int)atomicAdd(tile_queue, 1u);
         __syncthreads();
         const int tile = sm.tile;
         if (tile >= ntiles) break;
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
 
 template <int BATCH>
 static void launch_mma_b(cudaStream_t st, int grid, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
+                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, uint32_t *queue) {
     const size_t smem = sizeof(SmemMMA<BATCH>) + 128;
     static bool attr = false;
@@ -810,21 +810,21 @@ static void launch_mma_b(cudaStream_t st, int grid, const float2 *xy, const floa
         cudaFuncSetAttribute(k_blend_mma<BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    launch_pdl(k_blend_mma<BATCH>, grid, MMA_THREADS, smem, st, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H,
+    launch_pdl(k_blend_mma<BATCH>, grid, MMA_THREADS, smem, st, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H,
                bg[0], bg[1], bg[2], out_rgb, out_T, queue);
 }
 
 void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
-                      int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch) {
-    if (ntiles <= 0) return;
-    const int grid = std::max(1, std::min(GS_MMA_MINB * num_sms, ntiles));
+                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
+                      int W, int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch) {
+    if (ntiles - tile0 <= 0) return;
+    const int grid = std::max(1, std::min(GS_MMA_MINB * num_sms, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     switch (batch) {
-        case 32: launch_mma_b<32>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        case 64: launch_mma_b<64>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        case 128: launch_mma_b<128>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        default: launch_mma_b<256>(st, grid, xy, conic_o, rgb, vals, ranges, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 32: launch_mma_b<32>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 64: launch_mma_b<64>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 128: launch_mma_b<128>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        default: launch_mma_b<256>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
     }
 }
 

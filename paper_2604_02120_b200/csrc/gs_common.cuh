@@ -89,7 +89,19 @@ struct PreViews {
     gs_camera cam[MAX_VIEW_GROUP];
     PreOut out[MAX_VIEW_GROUP];
     int n;
+    int band_y0, band_y1;      // tile rows rendered (row band of a split frame; 0, gy = all)
 };
+
+// tile rows [y0, y1) of band `band` of n_bands (n_bands <= 1: the whole grid of gy rows)
+inline void band_rows(int gy, int band, int n_bands, int &y0, int &y1) {
+    if (n_bands <= 1) {
+        y0 = 0;
+        y1 = gy;
+        return;
+    }
+    y0 = (int)((long long)band * gy / n_bands);
+    y1 = (int)((long long)(band + 1) * gy / n_bands);
+}
 
 // Chunk geometry of the single-pass scans / onesweep radix passes.
 constexpr int SORT_THREADS = 256;
@@ -291,7 +303,7 @@ namespace gs {
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
                        int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, int imode,
-                       bool with_radius);
+                       bool with_radius, int band_y0, int band_y1);
 PreOut pre_out_of(const Workspace &ws, bool with_radius);
 void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const float *means, const float *scales,
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
@@ -299,14 +311,14 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
                    uint32_t &epoch, bool tight, float znear);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
+                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats);
 extern long long *g_blend_trace;
 void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W,
-                      int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch);
+                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
+                      int W, int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch);
 void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int ntiles, int gx, int W, int H,
+                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *counters);
 }  // namespace gs

@@ -113,6 +113,8 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
     if (o->blend < GS_BLEND_TC || o->blend > GS_BLEND_MMA) return GS_ERR_INVALID_ARG;
     if (o->batch != 0 && o->batch != 32 && o->batch != 64 && o->batch != 128 && o->batch != 256)
         return GS_ERR_INVALID_ARG;
+    if (o->n_bands < 0 || (o->n_bands > 1 && (o->band < 0 || o->band >= o->n_bands)))
+        return GS_ERR_INVALID_ARG;
     if (o->sh_degree >= 0 && o->sh_stride < (o->sh_degree + 1) * (o->sh_degree + 1)) return GS_ERR_INVALID_ARG;
     if (N > 0 && (!means || !scales || !rots || !opacity || !shs)) return GS_ERR_INVALID_ARG;
     if (!aligned16(rots)) return GS_ERR_ALIGNMENT;
@@ -176,8 +178,10 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
                   const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
     const int e0 = mark(c, st, o);
     if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
+    int y0 = 0, y1 = 0;
+    gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, y0, y1);
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                          o.scale_modifier, cam, W, H, gs::intersect_mode(o.flags), false);
+                          o.scale_modifier, cam, W, H, gs::intersect_mode(o.flags), false, y0, y1);
     c->launches += N > 0 ? 1 : 0;
     const int e1 = mark(c, st, o);
     enqueue_binning(c, c->ws, st, N, cam, W, H, o);
@@ -192,14 +196,17 @@ void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const flo
                    const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o,
                    float *out_rgb, float *out_T, float *dump) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
+    int y0 = 0, y1 = gy;   // the row band's tiles only (a split frame's other bands are untouched)
+    gs::band_rows(gy, o.band, o.n_bands, y0, y1);
+    const int t0 = y0 * gx, t1 = y1 * gx;
     if (o.blend == GS_BLEND_DIRECT && !dump)
-        gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                                 w.counters);
     else if (o.blend == GS_BLEND_MMA && !dump)
-        gs::launch_blend_mma(w, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_mma(w, st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                              c->num_sms, o.batch);
     else
-        gs::launch_blend_tc(w, st, xy, conic_o, rgb, vals, ranges, gx * gy, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_tc(w, st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                             dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
     c->launches += 1;
 }
@@ -441,6 +448,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         last_set = set;
         gs::PreViews pv{};
         pv.n = n;
+        gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, pv.band_y0, pv.band_y1);
         gs::Workspace *w[gs::MAX_VIEW_GROUP];
         for (int j = 0; j < n; j++) {
             if (int rc = view_ws(c, set * gs::MAX_VIEW_GROUP + j, &w[j])) return rc;
@@ -691,7 +699,8 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     gs::launch_preprocess(c->ws, st, N, means3D, scales, rots, opacity, shs, o->sh_degree, o->sh_stride,
-                          o->scale_modifier, *cam, W, H, gs::intersect_mode(o->flags), true);
+                          o->scale_modifier, *cam, W, H, gs::intersect_mode(o->flags), true, 0,
+                          gs::ceil_div_i(H, GS_TILE));
     c->last_counters = c->ws.counters;
     if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
     return finish(c, st, *o, N);

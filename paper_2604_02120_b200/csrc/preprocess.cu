@@ -271,6 +271,11 @@ __global__ void __launch_bounds__(PRE_THREADS, 2) k_preprocess(int N, const floa
         }
         const bool tight = imode == 1;
         if (imode == 2 && vis) vis = opacity_box(mx, my, sxx, syy, op, gx, gy, xmin, ymin, xmax, ymax);
+        if (vis && (pv.band_y0 > 0 || pv.band_y1 < gy)) {   // row band of a split frame: its rows only
+            ymin = max(ymin, pv.band_y0);
+            ymax = min(ymax, pv.band_y1);
+            vis = ymax > ymin;
+        }
         uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
         if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
             unsigned long long m = 0ull;
@@ -342,9 +347,11 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
 void launch_preprocess(const Workspace &ws, cudaStream_t st, int N, const float *means, const float *scales,
                        const float *rots, const float *opacity, const float *shs, int sh_degree,
                        int sh_stride, float scale_mod, const gs_camera &cam, int W, int H, int imode,
-                       bool with_radius) {
+                       bool with_radius, int band_y0, int band_y1) {
     PreViews pv{};
     pv.n = 1;
+    pv.band_y0 = band_y0;
+    pv.band_y1 = band_y1;
     pv.cam[0] = cam;
     pv.out[0] = pre_out_of(ws, with_radius);
     launch_preprocess_views(pv, st, N, means, scales, rots, opacity, shs, sh_degree, sh_stride, scale_mod, W, H,

@@ -79,3 +79,46 @@ def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_grou
     if rank != 0:
         return None, None
     return all_rgb.view((world * per,) + tuple(rgb.shape[1:])), all_T.view((world * per,) + tuple(T.shape[1:]))
+
+
+def band_pixel_rows(H: int, band: int, n_bands: int) -> range:
+    """Pixel rows of row band `band` of `n_bands` (the C-ABI's gs_opts.band / n_bands:
+    tile rows [band*gy/n, (band+1)*gy/n), gy = ceil(H/16))."""
+    gy = (H + 15) // 16
+    if n_bands <= 1:
+        return range(0, H)
+    y0, y1 = band * gy // n_bands, (band + 1) * gy // n_bands
+    return range(16 * y0, min(H, 16 * y1))
+
+
+def gather_bands(rgb, T, n_bands: int, rank: int, dist=None):
+    """Tile-row split of ONE view across ranks (SURVEY 8(e) option): rank r rendered
+    band r of `n_bands` (= world size) into its full-size rgb [3,H,W] / T [H,W] (other
+    rows unwritten). Gathers the bands to rank 0 (NCCL over NVLink on GPUs, gloo on
+    CPU; bands padded to the tallest one) and returns the assembled (rgb, T) there,
+    (None, None) elsewhere. No reduction: every pixel comes from exactly one rank."""
+    import torch
+    if n_bands == 1:
+        return rgb, T
+    if dist is None:
+        import torch.distributed as dist
+    H, W = T.shape
+    rows = [band_pixel_rows(H, b, n_bands) for b in range(n_bands)]
+    hmax = max(len(r) for r in rows)
+    mine = rows[rank]
+    prgb = torch.zeros((3, hmax, W), dtype=rgb.dtype, device=rgb.device)
+    pT = torch.zeros((hmax, W), dtype=T.dtype, device=T.device)
+    prgb[:, :len(mine)] = rgb[:, mine.start:mine.stop]
+    pT[:len(mine)] = T[mine.start:mine.stop]
+    lr = [torch.empty_like(prgb) for _ in range(n_bands)] if rank == 0 else None
+    lt = [torch.empty_like(pT) for _ in range(n_bands)] if rank == 0 else None
+    dist.gather(prgb, lr, dst=0)
+    dist.gather(pT, lt, dst=0)
+    if rank != 0:
+        return None, None
+    out_rgb = torch.empty_like(rgb)
+    out_T = torch.empty_like(T)
+    for b, r in enumerate(rows):
+        out_rgb[:, r.start:r.stop] = lr[b][:, :len(r)]
+        out_T[r.start:r.stop] = lt[b][:len(r)]
+    return out_rgb, out_T

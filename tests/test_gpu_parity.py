@@ -455,3 +455,56 @@ def test_stream_wait_group_orders_frame_consumers():
     with pytest.raises(GsError):
         ctx.gs_stream_wait_group(side, 3)
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["C2", "ragged", "tall"])
+@pytest.mark.parametrize("n_bands", [3, 5])
+def test_row_bands_compose_the_full_frame(case, n_bands):
+    """SURVEY 8(e) option, tile-row split of one view: rendering band k of n into a
+    shared buffer writes only that band's rows, bit-identical to the full frame, and
+    the band's binning is the oracle's lists on the band's tiles (empty elsewhere)."""
+    import torch
+    from paper_2604_02120_b200 import camera, opts, scene_to_device
+    from paper_2604_02120_b200.orbit import band_pixel_rows
+    scene, cam, bg = CASES[case]()
+    ctx = make_ctx(scene, cam)
+    st = scene_to_device(scene)
+    full, fT = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=16)
+    r = torch.full((3, cam.H, cam.W), float("nan"), device="cuda")
+    t = torch.full((cam.H, cam.W), float("nan"), device="cuda")
+    for k in range(n_bands):
+        before = r.clone()
+        ctx.gs_render(st, camera(cam), cam.W, cam.H,
+                      opts(bg, sh_degree=scene.sh_degree, flags=1 | 16, band=k, n_bands=n_bands), r, t)
+        torch.cuda.synchronize()
+        rows = band_pixel_rows(cam.H, k, n_bands)
+        other = torch.ones(cam.H, dtype=torch.bool, device="cuda")
+        other[rows.start:rows.stop] = False
+        assert torch.equal(r[:, other].isnan(), before[:, other].isnan())   # nothing else written
+    assert np.array_equal(r.cpu().numpy().astype(np.float64), full)
+    assert np.array_equal(t.cpu().numpy().astype(np.float64), fT)
+    # binning of one band = the oracle's (OBOX) lists on the band's tiles
+    pre = oracle.preprocess(scene, cam, obox=True)
+    ref = oracle.binning(pre, cam.W, cam.H)
+    gx = (cam.W + 15) // 16
+    k = n_bands // 2
+    code, K, b = None, None, None
+    keys = torch.empty(1 << 22, dtype=torch.int64, device="cuda")
+    vals = torch.empty(1 << 22, dtype=torch.int32, device="cuda")
+    ranges = torch.empty((len(ref["ranges"]), 2), dtype=torch.int32, device="cuda")
+    code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H,
+                                   opts(sh_degree=scene.sh_degree, flags=16, band=k, n_bands=n_bands),
+                                   keys, vals, ranges)
+    assert code == 0
+    rg = ranges.cpu().numpy().view(np.uint32)
+    kv = keys[:K].cpu().numpy().view(np.uint64)
+    vv = vals[:K].cpu().numpy().view(np.uint32)
+    gy = (cam.H + 15) // 16
+    y0, y1 = k * gy // n_bands, (k + 1) * gy // n_bands
+    for tile in range(len(rg)):
+        a0, a1 = ref["ranges"][tile]
+        if y0 <= tile // gx < y1:
+            g0, g1 = rg[tile]
+            assert np.array_equal(vv[g0:g1], ref["vals"][a0:a1]) and np.array_equal(kv[g0:g1], ref["keys"][a0:a1])
+        else:
+            assert rg[tile, 1] == rg[tile, 0]

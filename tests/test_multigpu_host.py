@@ -7,7 +7,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2604_02120_b200.orbit import gather_frames, gather_frames_pipelined, partition_views
+from paper_2604_02120_b200.orbit import (band_pixel_rows, gather_bands, gather_frames, gather_frames_pipelined,
+                                         partition_views)
 
 
 def test_partition_covers_views_once():
@@ -35,6 +36,18 @@ def _worker(rank, world, port, q):
     # frame content encodes its view id, as a render of view v would
     rgb = torch.stack([torch.full((3, H, W), float(v)) for v in views])
     T = torch.stack([torch.full((H, W), -float(v)) for v in views])
+    # tile-row split of one 70-row view (5 tile rows, bands of 2 and 3 tile rows): each
+    # rank fills only its band; the rest is garbage that must not leak into the result
+    Hv, Wv = 70, 9
+    frgb = torch.full((3, Hv, Wv), -7.0)
+    fT = torch.full((Hv, Wv), -7.0)
+    yy = torch.arange(Hv, dtype=torch.float32).view(Hv, 1).expand(Hv, Wv)
+    r = band_pixel_rows(Hv, rank, world)
+    frgb[:, r.start:r.stop] = yy[r.start:r.stop]
+    fT[r.start:r.stop] = -yy[r.start:r.stop]
+    brgb, bT = gather_bands(frgb, fT, world, rank)
+    if rank == 0:
+        assert torch.equal(brgb, yy.expand(3, Hv, Wv)) and torch.equal(bT, -yy)
     a, b = gather_frames(rgb, T, world, rank)
     # the group-pipelined gather (views in groups of 3: a ragged last group)
     c, d = gather_frames_pipelined(rgb, T, world, rank, 3)
@@ -62,3 +75,10 @@ def test_gather_frames_gloo_world2():
     assert rgb.shape == (8, 3, 3, 5) and T.shape == (8, 3, 5)
     for v in range(8):
         assert (rgb[v] == v).all() and (T[v] == -v).all()
+
+
+def test_band_rows_partition_the_frame():
+    for H in (1, 16, 45, 1080, 8400):
+        for n in (1, 2, 3, 5, 8):
+            rows = [v for b in range(n) for v in band_pixel_rows(H, b, n)]
+            assert rows == list(range(H))
