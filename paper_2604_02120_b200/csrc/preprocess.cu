@@ -186,7 +186,10 @@ __device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c
     return xmax > xmin && ymax > ymin;
 }
 
-__global__ void __launch_bounds__(PRE_THREADS, 2) k_preprocess(int N, const float *__restrict__ means,
+#ifndef GS_PRE_MINB
+#define GS_PRE_MINB 2
+#endif
+__global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
                                                                const float4 *__restrict__ rots,
                                                                const float *__restrict__ opacity,
