@@ -483,40 +483,43 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
     }
 }
 
-// step 2: one block per digit: exclusive scan of its row over the chunks; row totals
-__global__ void __launch_bounds__(1024) k_rs_scanrows(const Counters *cnt, int which, uint64_t max_keys,
-                                                      uint32_t *cmat, uint32_t ldm, uint32_t *row_total) {
+// step 2: one warp per digit: exclusive scan of its row over the chunks; row totals.
+// Each lane keeps 8 chunk counts in flight (coalesced loads), then the warp scans them
+// in order with shuffles (no block barriers: rows are independent).
+constexpr int SCANROWS_WARPS = 8;
+__global__ void __launch_bounds__(SCANROWS_WARPS * 32) k_rs_scanrows(const Counters *cnt, int which, uint64_t max_keys,
+                                                                   uint32_t *cmat, uint32_t ldm, uint32_t *row_total,
+                                                                   int ndig) {
     pdl_wait();
-    __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_carry;
     const uint32_t n = count_of(cnt, which, 0, max_keys);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t *row = cmat + (size_t)blockIdx.x * ldm;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t base = 0; base < nchunks; base += 1024) {
-        const uint32_t c = base + threadIdx.x;
-        const uint32_t v = c < nchunks ? row[c] : 0u;
-        uint32_t x = v;
+    const int lane = threadIdx.x & 31;
+    const int d = blockIdx.x * SCANROWS_WARPS + (threadIdx.x >> 5);
+    if (d >= ndig) return;
+    uint32_t *row = cmat + (size_t)d * ldm;
+    constexpr int U = 8;
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < nchunks; base += 32 * U) {
+        uint32_t v[U];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int u = 0; u < U; u++) {
+            const uint32_t c = base + u * 32 + lane;
+            v[u] = c < nchunks ? row[c] : 0u;
         }
-        if (lane == 31) s_w[warp] = x;
-        __syncthreads();
-        uint32_t wb = 0, tot = 0;
-        for (int w = 0; w < 32; w++) {
-            if (w < warp) wb += s_w[w];
-            tot += s_w[w];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            uint32_t x = v[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const uint32_t c = base + u * 32 + lane;
+            if (c < nchunks) row[c] = carry + x - v[u];
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (c < nchunks) row[c] = s_carry + wb + x - v;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
     }
-    if (threadIdx.x == 0) row_total[blockIdx.x] = s_carry;
+    if (lane == 0) row_total[d] = carry;
 }
 
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
@@ -1182,8 +1185,9 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
     const size_t ldm = ws.max_chunks;
     if (dbits > 8) launch_count<Loader, 512>(ws, st, grid, ld, which, mk, shift);
     else launch_count<Loader, 256>(ws, st, grid, ld, which, mk, shift);
-    launch_pdl(k_rs_scanrows, dbits > 8 ? 512 : 256, 1024, 0, st, ws.counters, which, mk, ws.cmat, (uint32_t)ldm,
-               ws.row_total);
+    const int ndig = dbits > 8 ? 512 : 256;
+    launch_pdl(k_rs_scanrows, ndig / SCANROWS_WARPS, SCANROWS_WARPS * 32, 0, st, ws.counters, which, mk, ws.cmat,
+               (uint32_t)ldm, ws.row_total, ndig);
     switch (dbits) {
     case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 2: launch_scatter<Loader, 2>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
