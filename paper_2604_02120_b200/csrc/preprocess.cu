@@ -109,7 +109,8 @@ __device__ __forceinline__ void cov3d(const float4 &q, float s0, float s1, float
 }
 
 // Step 11: SH colour for the view direction normalize(p - campos).
-__device__ __forceinline__ void sh_colour(const float (&k)[48], int sh_degree, float px, float py, float pz,
+template <class KF>
+__device__ __forceinline__ void sh_colour(KF k, int sh_degree, float px, float py, float pz,
                                           const gs_camera &cam, float (&res3)[3]) {
     const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
     const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
@@ -122,7 +123,7 @@ __device__ __forceinline__ void sh_colour(const float (&k)[48], int sh_degree, f
                 C36 = -0.5900435899266435f;
 #pragma unroll
     for (int ch = 0; ch < 3; ch++) {
-#define SHK(j) k[(j) * 3 + ch]
+#define SHK(j) k((j) * 3 + ch)
         float res = C0 * SHK(0);
         if (sh_degree >= 1) res = ((res - (C1 * Y) * SHK(1)) + (C1 * Z) * SHK(2)) - (C1 * X) * SHK(3);
         if (sh_degree >= 2) {
@@ -187,7 +188,7 @@ __device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c
 }
 
 #ifndef GS_PRE_MINB
-#define GS_PRE_MINB 2
+#define GS_PRE_MINB 3
 #endif
 __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
@@ -209,7 +210,10 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
     const float op = __ldcs(opacity + i);
     float S[3][3];
     bool have_cov = false, have_sh = false;
-    float k[48];
+    // the SH record, once loaded, lives in shared memory (coefficient-major: conflict-free)
+    // rather than in 48 registers, so the kernel keeps 3 blocks per SM
+    __shared__ float s_sh[48][PRE_THREADS];
+    auto K = [&](int j) { return s_sh[j][threadIdx.x]; };
 
 #pragma unroll 1
     for (int view = 0; view < pv.n; view++) {
@@ -309,17 +313,18 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
                     for (int j = 0; j < 12; j++) {
                         if (4 * j < ncoef * 3) {
                             const float4 t4 = __ldcs(sh4 + j);
-                            k[4 * j] = t4.x; k[4 * j + 1] = t4.y; k[4 * j + 2] = t4.z; k[4 * j + 3] = t4.w;
+                            s_sh[4 * j][threadIdx.x] = t4.x; s_sh[4 * j + 1][threadIdx.x] = t4.y;
+                            s_sh[4 * j + 2][threadIdx.x] = t4.z; s_sh[4 * j + 3][threadIdx.x] = t4.w;
                         }
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 48; j++)
-                        if (j < ncoef * 3) k[j] = __ldg(sh + j);
+                        if (j < ncoef * 3) s_sh[j][threadIdx.x] = __ldg(sh + j);
                 }
                 have_sh = true;
             }
-            sh_colour(k, sh_degree, px, py, pz, cam, col);
+            sh_colour(K, sh_degree, px, py, pz, cam, col);
         }
         // 12. outputs
         out.depth_bits[i] = __float_as_uint(vz);
