@@ -25,7 +25,8 @@
  *                      float64, used only by the algebra pins.
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread
- * (no FMA contraction, no FTZ/DAZ: the fp32 preprocess must be bit-reproducible).
+ * (no implicit FMA contraction -- fmaf() only where docs/preprocess_order.md writes fma --,
+ * no FTZ/DAZ: the fp32 preprocess must be bit-reproducible).
  */
 #include <math.h>
 #include <pthread.h>
@@ -104,16 +105,17 @@ int orc_preprocess_mode(int N, const float *means, const float *scales, const fl
 
         const float px = means[3 * i], py = means[3 * i + 1], pz = means[3 * i + 2];
         /* 1. view-space point */
-        float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam->t[0];
-        float vy = ((R[3] * px + R[4] * py) + R[5] * pz) + cam->t[1];
-        float vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam->t[2];
+        float vx = fmaf(R[2], pz, fmaf(R[1], py, fmaf(R[0], px, cam->t[0])));
+        float vy = fmaf(R[5], pz, fmaf(R[4], py, fmaf(R[3], px, cam->t[1])));
+        float vz = fmaf(R[8], pz, fmaf(R[7], py, fmaf(R[6], px, cam->t[2])));
         if (!(vz > cam->znear)) continue;
 
         /* 2. quaternion normalisation */
         float qw = rots[4 * i], qx = rots[4 * i + 1], qy = rots[4 * i + 2], qz = rots[4 * i + 3];
-        float n2 = ((qw * qw + qx * qx) + qy * qy) + qz * qz;
+        float n2 = fmaf(qz, qz, fmaf(qy, qy, fmaf(qx, qx, qw * qw)));
         float nr = sqrtf(n2);
-        float w = qw / nr, x = qx / nr, y = qy / nr, z = qz / nr;
+        float inr = 1.0f / nr;
+        float w = qw * inr, x = qx * inr, y = qy * inr, z = qz * inr;
 
         /* 3. rotation matrix */
         float xx = x * x, yy = y * y, zz = z * z, xy_ = x * y, xz = x * z, yz = y * z;
@@ -135,47 +137,49 @@ int orc_preprocess_mode(int N, const float *means, const float *scales, const fl
         float S[3][3];
         for (int a = 0; a < 3; a++)
             for (int b = a; b < 3; b++) {
-                S[a][b] = (u[a][0] * M[b][0] + u[a][1] * M[b][1]) + u[a][2] * M[b][2];
+                S[a][b] = fmaf(u[a][2], M[b][2], fmaf(u[a][1], M[b][1], u[a][0] * M[b][0]));
                 S[b][a] = S[a][b];
             }
 
         /* 5. clamped Jacobian */
         float lx = 1.3f * cam->tan_fovx, ly = 1.3f * cam->tan_fovy;
-        float ux = vx / vz, uy = vy / vz;
+        float iz = 1.0f / vz;
+        float ux = vx * iz, uy = vy * iz;
         float cxz = fminf(lx, fmaxf(-lx, ux));
         float cyz = fminf(ly, fmaxf(-ly, uy));
-        float j00 = cam->fx / vz, j02 = -((cam->fx * cxz) / vz);
-        float j11 = cam->fy / vz, j12 = -((cam->fy * cyz) / vz);
+        float j00 = cam->fx * iz, j02 = -((cam->fx * cxz) * iz);
+        float j11 = cam->fy * iz, j12 = -((cam->fy * cyz) * iz);
 
         /* 6. EWA 2D covariance, T = J R (2x3) */
         float T[2][3];
         for (int k = 0; k < 3; k++) {
-            T[0][k] = j00 * R[0 + k] + j02 * R[6 + k];
-            T[1][k] = j11 * R[3 + k] + j12 * R[6 + k];
+            T[0][k] = fmaf(j02, R[6 + k], j00 * R[0 + k]);
+            T[1][k] = fmaf(j12, R[6 + k], j11 * R[3 + k]);
         }
         float U[2][3];
         for (int a = 0; a < 2; a++)
             for (int k = 0; k < 3; k++)
-                U[a][k] = (T[a][0] * S[0][k] + T[a][1] * S[1][k]) + T[a][2] * S[2][k];
-        float c00 = (U[0][0] * T[0][0] + U[0][1] * T[0][1]) + U[0][2] * T[0][2];
-        float c01 = (U[0][0] * T[1][0] + U[0][1] * T[1][1]) + U[0][2] * T[1][2];
-        float c11 = (U[1][0] * T[1][0] + U[1][1] * T[1][1]) + U[1][2] * T[1][2];
+                U[a][k] = fmaf(T[a][2], S[2][k], fmaf(T[a][1], S[1][k], T[a][0] * S[0][k]));
+        float c00 = fmaf(U[0][2], T[0][2], fmaf(U[0][1], T[0][1], U[0][0] * T[0][0]));
+        float c01 = fmaf(U[0][2], T[1][2], fmaf(U[0][1], T[1][1], U[0][0] * T[1][0]));
+        float c11 = fmaf(U[1][2], T[1][2], fmaf(U[1][1], T[1][1], U[1][0] * T[1][0]));
         float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
 
         /* 7. conic */
-        float det = a * c - b * b;
+        float det = fmaf(a, c, -(b * b));
         if (!(det > 0.0f)) continue;
-        float cA = c / det, cB = -(b / det), cC = a / det;
+        float id = 1.0f / det;
+        float cA = c * id, cB = -(b * id), cC = a * id;
 
         /* 8. radius */
         float mid = 0.5f * (a + c);
-        float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
+        float lam = mid + sqrtf(fmaxf(0.1f, fmaf(mid, mid, -det)));
         float rr = ceilf(3.0f * sqrtf(lam));
         int r = (int)rr;
 
         /* 9. projected mean */
-        float mx = cam->fx * ux + cam->cx;
-        float my = cam->fy * uy + cam->cy;
+        float mx = fmaf(cam->fx, ux, cam->cx);
+        float my = fmaf(cam->fy, uy, cam->cy);
 
         /* 10. tile rectangle */
         float rf = (float)r;
@@ -212,30 +216,33 @@ int orc_preprocess_mode(int N, const float *means, const float *scales, const fl
             for (int ch = 0; ch < 3; ch++) col[ch] = shs[3 * (size_t)i + ch];
         } else {
             float dx = px - cam->campos[0], dy = py - cam->campos[1], dz = pz - cam->campos[2];
-            float len = sqrtf((dx * dx + dy * dy) + dz * dz);
-            float X = dx / len, Y = dy / len, Z = dz / len;
+            float len = sqrtf(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+            float il = 1.0f / len;
+            float X = dx * il, Y = dy * il, Z = dz * il;
             const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
             for (int ch = 0; ch < 3; ch++) {
 #define SH(k) sh[(k) * 3 + ch]
                 float res = SH_C0 * SH(0);
                 if (sh_degree >= 1) {
-                    res = ((res - (SH_C1 * Y) * SH(1)) + (SH_C1 * Z) * SH(2)) - (SH_C1 * X) * SH(3);
+                    res = fmaf(-(SH_C1 * Y), SH(1), res);
+                    res = fmaf(SH_C1 * Z, SH(2), res);
+                    res = fmaf(-(SH_C1 * X), SH(3), res);
                 }
                 if (sh_degree >= 2) {
                     float XX = X * X, YY = Y * Y, ZZ = Z * Z, XY = X * Y, YZ = Y * Z, XZ = X * Z;
-                    res = res + (SH_C2[0] * XY) * SH(4);
-                    res = res + (SH_C2[1] * YZ) * SH(5);
-                    res = res + (SH_C2[2] * (((2.0f * ZZ) - XX) - YY)) * SH(6);
-                    res = res + (SH_C2[3] * XZ) * SH(7);
-                    res = res + (SH_C2[4] * (XX - YY)) * SH(8);
+                    res = fmaf((SH_C2[0] * XY), SH(4), res);
+                    res = fmaf((SH_C2[1] * YZ), SH(5), res);
+                    res = fmaf((SH_C2[2] * (((2.0f * ZZ) - XX) - YY)), SH(6), res);
+                    res = fmaf((SH_C2[3] * XZ), SH(7), res);
+                    res = fmaf((SH_C2[4] * (XX - YY)), SH(8), res);
                     if (sh_degree >= 3) {
-                        res = res + ((SH_C3[0] * Y) * ((3.0f * XX) - YY)) * SH(9);
-                        res = res + ((SH_C3[1] * XY) * Z) * SH(10);
-                        res = res + ((SH_C3[2] * Y) * (((4.0f * ZZ) - XX) - YY)) * SH(11);
-                        res = res + ((SH_C3[3] * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))) * SH(12);
-                        res = res + ((SH_C3[4] * X) * (((4.0f * ZZ) - XX) - YY)) * SH(13);
-                        res = res + ((SH_C3[5] * Z) * (XX - YY)) * SH(14);
-                        res = res + ((SH_C3[6] * X) * (XX - (3.0f * YY))) * SH(15);
+                        res = fmaf(((SH_C3[0] * Y) * ((3.0f * XX) - YY)), SH(9), res);
+                        res = fmaf(((SH_C3[1] * XY) * Z), SH(10), res);
+                        res = fmaf(((SH_C3[2] * Y) * (((4.0f * ZZ) - XX) - YY)), SH(11), res);
+                        res = fmaf(((SH_C3[3] * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))), SH(12), res);
+                        res = fmaf(((SH_C3[4] * X) * (((4.0f * ZZ) - XX) - YY)), SH(13), res);
+                        res = fmaf(((SH_C3[5] * Z) * (XX - YY)), SH(14), res);
+                        res = fmaf(((SH_C3[6] * X) * (XX - (3.0f * YY))), SH(15), res);
                     }
                 }
 #undef SH

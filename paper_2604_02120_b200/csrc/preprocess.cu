@@ -76,9 +76,10 @@ __device__ __forceinline__ bool tight_rect(float mx, float my, float A, float B,
 // Steps 2-4 (view-independent): quaternion normalisation, rotation matrix, 3D covariance.
 __device__ __forceinline__ void cov3d(const float4 &q, float s0, float s1, float s2, float scale_mod, float (&S)[3][3]) {
     // 2. quaternion normalisation
-    const float n2 = ((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w;
+    const float n2 = __fmaf_rn(q.w, q.w, __fmaf_rn(q.z, q.z, __fmaf_rn(q.y, q.y, q.x * q.x)));
     const float nr = sqrtf(n2);
-    const float w = q.x / nr, x = q.y / nr, y = q.z / nr, z = q.w / nr;
+    const float inr = 1.0f / nr;
+    const float w = q.x * inr, x = q.y * inr, y = q.z * inr, z = q.w * inr;
     // 3. rotation matrix
     const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
     const float wx = w * x, wy = w * y, wz = w * z;
@@ -103,7 +104,7 @@ __device__ __forceinline__ void cov3d(const float4 &q, float s0, float s1, float
     for (int a = 0; a < 3; a++)
 #pragma unroll
         for (int b = a; b < 3; b++) {
-            S[a][b] = (u[a][0] * M[b][0] + u[a][1] * M[b][1]) + u[a][2] * M[b][2];
+            S[a][b] = __fmaf_rn(u[a][2], M[b][2], __fmaf_rn(u[a][1], M[b][1], u[a][0] * M[b][0]));
             S[b][a] = S[a][b];
         }
 }
@@ -113,8 +114,9 @@ template <class KF>
 __device__ __forceinline__ void sh_colour(KF k, int sh_degree, float px, float py, float pz,
                                           const gs_camera &cam, float (&res3)[3]) {
     const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
-    const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
-    const float X = dx / len, Y = dy / len, Z = dz / len;
+    const float len = sqrtf(__fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx)));
+    const float il = 1.0f / len;
+    const float X = dx * il, Y = dy * il, Z = dz * il;
     const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
     const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
                 C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
@@ -125,22 +127,26 @@ __device__ __forceinline__ void sh_colour(KF k, int sh_degree, float px, float p
     for (int ch = 0; ch < 3; ch++) {
 #define SHK(j) k((j) * 3 + ch)
         float res = C0 * SHK(0);
-        if (sh_degree >= 1) res = ((res - (C1 * Y) * SHK(1)) + (C1 * Z) * SHK(2)) - (C1 * X) * SHK(3);
+        if (sh_degree >= 1) {
+            res = __fmaf_rn(-(C1 * Y), SHK(1), res);
+            res = __fmaf_rn(C1 * Z, SHK(2), res);
+            res = __fmaf_rn(-(C1 * X), SHK(3), res);
+        }
         if (sh_degree >= 2) {
             const float XX = X * X, YY = Y * Y, ZZ = Z * Z, XY = X * Y, YZ = Y * Z, XZ = X * Z;
-            res = res + (C20 * XY) * SHK(4);
-            res = res + (C21 * YZ) * SHK(5);
-            res = res + (C22 * (((2.0f * ZZ) - XX) - YY)) * SHK(6);
-            res = res + (C23 * XZ) * SHK(7);
-            res = res + (C24 * (XX - YY)) * SHK(8);
+            res = __fmaf_rn((C20 * XY), SHK(4), res);
+            res = __fmaf_rn((C21 * YZ), SHK(5), res);
+            res = __fmaf_rn((C22 * (((2.0f * ZZ) - XX) - YY)), SHK(6), res);
+            res = __fmaf_rn((C23 * XZ), SHK(7), res);
+            res = __fmaf_rn((C24 * (XX - YY)), SHK(8), res);
             if (sh_degree >= 3) {
-                res = res + ((C30 * Y) * ((3.0f * XX) - YY)) * SHK(9);
-                res = res + ((C31 * XY) * Z) * SHK(10);
-                res = res + ((C32 * Y) * (((4.0f * ZZ) - XX) - YY)) * SHK(11);
-                res = res + ((C33 * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))) * SHK(12);
-                res = res + ((C34 * X) * (((4.0f * ZZ) - XX) - YY)) * SHK(13);
-                res = res + ((C35 * Z) * (XX - YY)) * SHK(14);
-                res = res + ((C36 * X) * (XX - (3.0f * YY))) * SHK(15);
+                res = __fmaf_rn(((C30 * Y) * ((3.0f * XX) - YY)), SHK(9), res);
+                res = __fmaf_rn(((C31 * XY) * Z), SHK(10), res);
+                res = __fmaf_rn(((C32 * Y) * (((4.0f * ZZ) - XX) - YY)), SHK(11), res);
+                res = __fmaf_rn(((C33 * Z) * (((2.0f * ZZ) - (3.0f * XX)) - (3.0f * YY))), SHK(12), res);
+                res = __fmaf_rn(((C34 * X) * (((4.0f * ZZ) - XX) - YY)), SHK(13), res);
+                res = __fmaf_rn(((C35 * Z) * (XX - YY)), SHK(14), res);
+                res = __fmaf_rn(((C36 * X) * (XX - (3.0f * YY))), SHK(15), res);
             }
         }
 #undef SHK
@@ -224,9 +230,9 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f;
         int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
         // 1. view-space point
-        const float vx = ((R[0] * px + R[1] * py) + R[2] * pz) + cam.t[0];
-        const float vy = ((R[3] * px + R[4] * py) + R[5] * pz) + cam.t[1];
-        const float vz = ((R[6] * px + R[7] * py) + R[8] * pz) + cam.t[2];
+        const float vx = __fmaf_rn(R[2], pz, __fmaf_rn(R[1], py, __fmaf_rn(R[0], px, cam.t[0])));
+        const float vy = __fmaf_rn(R[5], pz, __fmaf_rn(R[4], py, __fmaf_rn(R[3], px, cam.t[1])));
+        const float vz = __fmaf_rn(R[8], pz, __fmaf_rn(R[7], py, __fmaf_rn(R[6], px, cam.t[2])));
         if (vz > cam.znear) {
             if (!have_cov) {   // 2-4, once per Gaussian
                 cov3d(q, s0, s1, s2, scale_mod, S);
@@ -234,39 +240,41 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
             }
             // 5. clamped Jacobian
             const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
-            const float ux = vx / vz, uy = vy / vz;
+            const float iz = 1.0f / vz;
+            const float ux = vx * iz, uy = vy * iz;
             const float cxz = fminf(lx, fmaxf(-lx, ux));
             const float cyz = fminf(ly, fmaxf(-ly, uy));
-            const float j00 = cam.fx / vz, j02 = -((cam.fx * cxz) / vz);
-            const float j11 = cam.fy / vz, j12 = -((cam.fy * cyz) / vz);
+            const float j00 = cam.fx * iz, j02 = -((cam.fx * cxz) * iz);
+            const float j11 = cam.fy * iz, j12 = -((cam.fy * cyz) * iz);
             // 6. EWA 2D covariance, T = J R
             float T[2][3], U[2][3];
 #pragma unroll
             for (int kk = 0; kk < 3; kk++) {
-                T[0][kk] = j00 * R[0 + kk] + j02 * R[6 + kk];
-                T[1][kk] = j11 * R[3 + kk] + j12 * R[6 + kk];
+                T[0][kk] = __fmaf_rn(j02, R[6 + kk], j00 * R[0 + kk]);
+                T[1][kk] = __fmaf_rn(j12, R[6 + kk], j11 * R[3 + kk]);
             }
 #pragma unroll
             for (int a = 0; a < 2; a++)
 #pragma unroll
                 for (int kk = 0; kk < 3; kk++)
-                    U[a][kk] = (T[a][0] * S[0][kk] + T[a][1] * S[1][kk]) + T[a][2] * S[2][kk];
-            const float c00 = (U[0][0] * T[0][0] + U[0][1] * T[0][1]) + U[0][2] * T[0][2];
-            const float c01 = (U[0][0] * T[1][0] + U[0][1] * T[1][1]) + U[0][2] * T[1][2];
-            const float c11 = (U[1][0] * T[1][0] + U[1][1] * T[1][1]) + U[1][2] * T[1][2];
+                    U[a][kk] = __fmaf_rn(T[a][2], S[2][kk], __fmaf_rn(T[a][1], S[1][kk], T[a][0] * S[0][kk]));
+            const float c00 = __fmaf_rn(U[0][2], T[0][2], __fmaf_rn(U[0][1], T[0][1], U[0][0] * T[0][0]));
+            const float c01 = __fmaf_rn(U[0][2], T[1][2], __fmaf_rn(U[0][1], T[1][1], U[0][0] * T[1][0]));
+            const float c11 = __fmaf_rn(U[1][2], T[1][2], __fmaf_rn(U[1][1], T[1][1], U[1][0] * T[1][0]));
             const float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
             // 7. conic
-            const float det = a * c - b * b;
+            const float det = __fmaf_rn(a, c, -(b * b));
             if (det > 0.0f) {
-                cA = c / det; cB = -(b / det); cC = a / det;
+                const float id = 1.0f / det;
+                cA = c * id; cB = -(b * id); cC = a * id;
                 sxx = a; sxy = b; syy = c;
                 // 8. radius
                 const float mid = 0.5f * (a + c);
-                const float lam = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
+                const float lam = mid + sqrtf(fmaxf(0.1f, __fmaf_rn(mid, mid, -det)));
                 r = (int)ceilf(3.0f * sqrtf(lam));
                 // 9. projected mean
-                mx = cam.fx * ux + cam.cx;
-                my = cam.fy * uy + cam.cy;
+                mx = __fmaf_rn(cam.fx, ux, cam.cx);
+                my = __fmaf_rn(cam.fy, uy, cam.cy);
                 // 10. tile rectangle
                 const float rf = (float)r;
                 xmin = rect_bound((mx - rf) / 16.0f, gx);
