@@ -508,3 +508,26 @@ def test_row_bands_compose_the_full_frame(case, n_bands):
             assert np.array_equal(vv[g0:g1], ref["vals"][a0:a1]) and np.array_equal(kv[g0:g1], ref["keys"][a0:a1])
         else:
             assert rg[tile, 1] == rg[tile, 0]
+
+
+def test_obox_opacity_edge_cases_bit_exact():
+    """Step 10b at its edges: 255*o just below / at / above 1 (cull boundary), o -> 1,
+    huge and tiny splats; rects and culls bit-exact against the oracle."""
+    from paper_2604_02120_b200 import GS_FLAG_OBOX
+    scene = synth.object_scene(4096, 110, sh_degree=1)
+    edge = np.array([np.nextafter(np.float32(1 / 255), np.float32(0)), np.float32(1 / 255),
+                     np.nextafter(np.float32(1 / 255), np.float32(1)), np.float32(0.004), np.float32(0.99999),
+                     np.float32(1.0), np.float32(0.5), np.float32(1e-6)], np.float32)
+    scene.opacity[:] = edge[np.arange(scene.n) % len(edge)]
+    scene.scales[::7] *= 40.0
+    scene.scales[3::7] *= 0.01
+    cam = synth.look_at((0.3, -0.4, -3.0), (0, 0, 0), 200, 136, 0.9)
+    ctx = make_ctx(scene, cam)
+    got = gpu_preprocess(ctx, scene, cam, flags=GS_FLAG_OBOX)
+    pre = oracle.preprocess(scene, cam, obox=True)
+    assert np.array_equal(got["touched"], pre["touched"])
+    vis = pre["touched"] > 0
+    assert np.array_equal(got["rect"][vis], pre["rect"][vis])
+    t = np.float32(255.0) * scene.opacity.astype(np.float32)   # the binary32 product step 10b tests
+    assert not vis[t < 1.0].any()
+    assert vis[t >= 1.0].any()
