@@ -34,7 +34,7 @@ UNIT = "frames/s"
 INTERSECT = {"vanilla": (0, "vanilla 3-sigma rect"),
              "obox": (16, "GS_FLAG_OBOX: vanilla rect clipped to the opacity-aware alpha >= 1/255 box"),
              "tight": (8, "GS_FLAG_TIGHT: opacity-aware box + per-row ellipse column runs")}
-VIEW_GROUP = 4   # views per preprocess launch (gs_set_view_group), binning chains concurrent
+VIEW_GROUP = int(os.environ.get("GS_BENCH_GROUP", "16"))   # views per preprocess launch (gs_set_view_group), binning chains concurrent
 WORKLOAD = "C5: 6M Gaussians SH3, 1920x1080, 64-view orbit (BASELINE.json configs[4])"
 
 

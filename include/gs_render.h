@@ -141,7 +141,7 @@ int gs_render(gs_ctx *ctx, void *stream, int N, const float *means3D, const floa
 /* Renders n_views cameras (host array cams[n_views]) of the same scene into
  * out_rgb [n_views,3,H,W] and out_T [n_views,H,W] (device), on `stream`.
  * Frames are bit-identical to n_views gs_render calls. The views are processed
- * in groups (gs_set_view_group, default 4): one preprocess launch reads each
+ * in groups (gs_set_view_group, default 4, at most 16): one preprocess launch reads each
  * Gaussian's record (means, scales, rotation, opacity, SH) from HBM once for
  * the whole group and writes the group's per-view splats; binning and blending
  * then run view by view (P:109-117 per view). */
@@ -160,14 +160,14 @@ int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
                          const float *shs_or_colors, const gs_camera *cams, int n_views,
                          int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
 
-/* Sets the view-group size of gs_render_views / gs_render_views_host (g = 1..4;
+/* Sets the view-group size of gs_render_views / gs_render_views_host (g = 1..16;
  * 1 = one preprocess launch per view) and whether the group's per-view binning
  * chains run concurrently on context-owned streams (concurrent != 0, default) or
  * back to back on the caller's stream. Output does not depend on either. The
  * first multi-view call with group g allocates g-1 extra workspaces (as
  * gs_ctx_create: about 36 B x max_points + 16 B x max_keys each). With
  * GS_FLAG_TIMING and concurrent chains the per-stage times overlap.
- * GS_ERR_INVALID_ARG for g outside 1..4. */
+ * GS_ERR_INVALID_ARG for g outside 1..16. */
 int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
 
 /* Makes `stream` wait (device-side, cudaStreamWaitEvent) until view group g of

@@ -84,7 +84,7 @@ struct PreOut {
     int32_t *radius;           // nullptr: not written (debug output only)
     Counters *counters;        // zeroed by the preprocess
 };
-constexpr int MAX_VIEW_GROUP = 4;
+constexpr int MAX_VIEW_GROUP = 16;  // views per preprocess launch (gs_set_view_group; default 4)
 struct PreViews {
     gs_camera cam[MAX_VIEW_GROUP];
     PreOut out[MAX_VIEW_GROUP];

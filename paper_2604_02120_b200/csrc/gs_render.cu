@@ -32,7 +32,7 @@ struct gs_ctx {
     double stage_ms[3] = {0, 0, 0};
     int64_t timed_frames = 0;
     // view groups (gs_render_views): per-view preprocess outputs + counters of views 1..G-1
-    int view_group = gs::MAX_VIEW_GROUP;
+    int view_group = 4;
     // slot s*MAX_VIEW_GROUP + j = view j of a group in slot set s (two sets: the preprocess of
     // group g+1 runs while group g bins and blends); slot 0 is the context's own workspace
     gs::Workspace vws[2 * gs::MAX_VIEW_GROUP] = {};
@@ -40,7 +40,8 @@ struct gs_ctx {
     gs::Counters *last_counters = nullptr;   // counters of the last rendered view
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t group_done[2] = {}, copies_done[2] = {};
+    // per staging slot (2 * MAX_VIEW_GROUP frames): the view's blend done / its copy done
+    cudaEvent_t view_done[2 * gs::MAX_VIEW_GROUP] = {}, copies_done[2 * gs::MAX_VIEW_GROUP] = {};
     // gs_render_views, concurrent mode: preprocess on pre_stream, the binning chain of view j
     // of a group on bstream[j], blends on blend_stream (high priority); events per slot set
     bool concurrent = true;
@@ -353,7 +354,10 @@ int gs_ctx_destroy(gs_ctx *c) {
     if (c->pre_stream) cudaStreamDestroy(c->pre_stream);
     for (auto &e : c->ev) cudaEventDestroy(e);
     for (int k = 0; k < 2; k++) {
-        if (c->group_done[k]) cudaEventDestroy(c->group_done[k]);
+        (void)k;
+    }
+    for (int k = 0; k < 2 * gs::MAX_VIEW_GROUP; k++) {
+        if (c->view_done[k]) cudaEventDestroy(c->view_done[k]);
         if (c->copies_done[k]) cudaEventDestroy(c->copies_done[k]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -379,12 +383,12 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
 }
 
 // Optional per-group callbacks of render_views_impl (the host entry point's frame copies):
-// pre_blend(g) runs before group g's blends are enqueued, post_blend(g) right after, both
+// pre_blend(v) runs before view v's blend is enqueued, post_blend(v) right after, both
 // with the stream the blends run on.
 struct GroupHooks {
     void *user;
-    void (*pre_blend)(void *user, cudaStream_t bl, int g);
-    void (*post_blend)(void *user, cudaStream_t bl, int g, int v0, int n);
+    void (*pre_blend)(void *user, cudaStream_t bl, int v);
+    void (*post_blend)(void *user, cudaStream_t bl, int v);
 };
 
 static int record_group(gs_ctx *c, cudaStream_t s, int g) {
@@ -476,36 +480,36 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                 cudaEventRecord(c->ev_binned[set][j], bs);
             }
             cudaStream_t bl = c->blend_stream;
-            if (hk && hk->pre_blend) hk->pre_blend(hk->user, bl, g);
             for (int j = 0; j < n; j++) {
                 cudaStreamWaitEvent(bl, c->ev_binned[set][j], 0);
+                if (hk && hk->pre_blend) hk->pre_blend(hk->user, bl, v0 + j);
                 const int e1 = mark(c, bl, o);
                 enqueue_blend(c, *w[j], bl, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H,
                               o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
                 const int e2 = mark(c, bl, o);
+                if (hk && hk->post_blend) hk->post_blend(hk->user, bl, v0 + j);
                 span(c, 2, e1, e2);
                 if (e2 >= 0) c->timed_frames++;
                 c->last_counters = w[j]->counters;
             }
-            if (hk && hk->post_blend) hk->post_blend(hk->user, bl, g, v0, n);
             cudaEventRecord(c->ev_blended[set], bl);
             if (int rc = record_group(c, bl, g)) return rc;
             continue;
         }
-        if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, g);
         for (int j = 0; j < n; j++) {
             enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
+            if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, v0 + j);
             const int e1 = mark(c, st, o);
             enqueue_blend(c, *w[j], st, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H, o,
                           rgb_of[v0 + j], T_of[v0 + j], nullptr);
             const int e2 = mark(c, st, o);
+            if (hk && hk->post_blend) hk->post_blend(hk->user, st, v0 + j);
             span(c, 1, e_prev, e1);
             span(c, 2, e1, e2);
             e_prev = e2;
             if (e2 >= 0) c->timed_frames++;
             c->last_counters = w[j]->counters;
         }
-        if (hk && hk->post_blend) hk->post_blend(hk->user, st, g, v0, n);
         if (int rc = record_group(c, st, g)) return rc;
     }
     if (conc) {   // the frames are complete in the caller's stream order
@@ -563,8 +567,8 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
         if (check_cuda(cudaMalloc(&c->frame_rgb, 3 * fr * sizeof(float)))) return GS_ERR_CUDA;
         if (check_cuda(cudaMalloc(&c->frame_T, fr * sizeof(float)))) return GS_ERR_CUDA;
         if (check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking))) return GS_ERR_CUDA;
-        for (int k = 0; k < 2; k++) {
-            cudaEventCreateWithFlags(&c->group_done[k], cudaEventDisableTiming);
+        for (int k = 0; k < 2 * gs::MAX_VIEW_GROUP; k++) {
+            cudaEventCreateWithFlags(&c->view_done[k], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&c->copies_done[k], cudaEventDisableTiming);
         }
     }
@@ -579,15 +583,16 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
     cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, st);
-    // Frames come back on the copy stream, one view group behind: group g renders into
-    // staging slot g % 2 (G frames) while the frames of group g - 1 are copied to the host.
+    // Frames come back on the copy stream view by view: view v renders into staging slot
+    // v % (2G) and is copied to the host as soon as its blend is done, while later views
+    // render; the slot is reused 2G views later, after its copy completed.
     const size_t plane = (size_t)W * H, mplane = (size_t)c->max_w * c->max_h;
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     gs_opts ov = *o;
     ov.flags &= ~GS_FLAG_SYNC;
     std::vector<float *> prgb(n_views), pT(n_views);
     for (int v = 0; v < n_views; v++) {
-        const size_t slot = (size_t)(((v / G) & 1) * gs::MAX_VIEW_GROUP + v % G);
+        const size_t slot = (size_t)(v % (2 * G));
         prgb[v] = c->frame_rgb + slot * 3 * mplane;
         pT[v] = c->frame_T + slot * mplane;
     }
@@ -596,24 +601,23 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
         float *h_rgb, *h_T;
         float *const *prgb, *const *pT;
         size_t plane;
-    } cp{c, h_out_rgb, h_out_T, prgb.data(), pT.data(), plane};
+        int nslots;
+    } cp{c, h_out_rgb, h_out_T, prgb.data(), pT.data(), plane, 2 * G};
     GroupHooks hk;
     hk.user = &cp;
-    hk.pre_blend = [](void *u, cudaStream_t bl, int g) {
+    hk.pre_blend = [](void *u, cudaStream_t bl, int v) {
         Copies &k = *static_cast<Copies *>(u);
-        if (g >= 2) cudaStreamWaitEvent(bl, k.c->copies_done[g & 1], 0);   // staging slot free again
+        if (v >= k.nslots) cudaStreamWaitEvent(bl, k.c->copies_done[v % k.nslots], 0);   // slot free again
     };
-    hk.post_blend = [](void *u, cudaStream_t bl, int g, int v0, int n) {
+    hk.post_blend = [](void *u, cudaStream_t bl, int v) {
         Copies &k = *static_cast<Copies *>(u);
-        cudaEventRecord(k.c->group_done[g & 1], bl);
-        cudaStreamWaitEvent(k.c->copy_stream, k.c->group_done[g & 1], 0);
-        for (int v = v0; v < v0 + n; v++) {
-            cudaMemcpyAsync(k.h_rgb + (size_t)v * 3 * k.plane, k.prgb[v], 3 * k.plane * 4, cudaMemcpyDeviceToHost,
-                            k.c->copy_stream);
-            cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost,
-                            k.c->copy_stream);
-        }
-        cudaEventRecord(k.c->copies_done[g & 1], k.c->copy_stream);
+        const int s = v % k.nslots;
+        cudaEventRecord(k.c->view_done[s], bl);
+        cudaStreamWaitEvent(k.c->copy_stream, k.c->view_done[s], 0);
+        cudaMemcpyAsync(k.h_rgb + (size_t)v * 3 * k.plane, k.prgb[v], 3 * k.plane * 4, cudaMemcpyDeviceToHost,
+                        k.c->copy_stream);
+        cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost, k.c->copy_stream);
+        cudaEventRecord(k.c->copies_done[s], k.c->copy_stream);
     };
     if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams, n_views, W, H, ov, prgb.data(), pT.data(),
                                    &hk))

@@ -258,11 +258,11 @@ def test_full_size_c5_view_sampled_parity(obox):
     assert np.array_equal(gb["keys"], ref_b["keys"]) and np.array_equal(gb["vals"], ref_b["vals"])
     assert np.array_equal(gb["ranges"], ref_b["ranges"])
     rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=flags)
-    # the bench's path: 4 views in one group, chains concurrent; view 0 must match
-    ctx.gs_set_view_group(4, True)
-    orgb = torch.empty((4, 3, cam.H, cam.W), device="cuda")
-    oT = torch.empty((4, cam.H, cam.W), device="cuda")
-    ctx.gs_render_views(st, [camera(c) for c in cams[:4]], cam.W, cam.H,
+    # the bench's path: views in one group of up to 16, chains concurrent; view 0 must match
+    ctx.gs_set_view_group(16, True)
+    orgb = torch.empty((6, 3, cam.H, cam.W), device="cuda")
+    oT = torch.empty((6, cam.H, cam.W), device="cuda")
+    ctx.gs_render_views(st, [camera(c) for c in cams[:6]], cam.W, cam.H,
                         opts(bg, sh_degree=scene.sh_degree, flags=flags), orgb, oT)
     torch.cuda.synchronize()
     assert np.array_equal(orgb[0].cpu().numpy().astype(np.float64), rgb)
@@ -356,7 +356,7 @@ def test_view_groups_are_bit_identical_to_single_views(flags):
         ref_rgb.append(r.cpu().numpy())
         ref_T.append(t.cpu().numpy())
     ref_rgb, ref_T = np.stack(ref_rgb), np.stack(ref_T)
-    for g, conc in ((1, True), (2, True), (3, False), (3, True), (4, False), (4, True)):
+    for g, conc in ((1, True), (2, True), (3, False), (3, True), (4, False), (4, True), (5, True), (16, True)):
         ctx.gs_set_view_group(g, conc)
         r = torch.full((7, 3, 200, 320), float("nan"), device="cuda")
         t = torch.full((7, 200, 320), float("nan"), device="cuda")
