@@ -395,6 +395,44 @@ def run_ours(args):
                 ctx_s.close()
         torch.cuda.empty_cache()
 
+    # --- the other BASELINE.json config shapes (parity cases; reported for context):
+    # single-view gs_render latency and an 8-view orbit of each, same intersection ---
+    per_config = None
+    if not args.no_configs and ws == 1:
+        per_config = {}
+        for name in ("C2", "C3", "C4a", "C4b"):
+            sc_c, cams_c, bg_c = synth.make_config(name, views=8)
+            Wc, Hc = cams_c[0].W, cams_c[0].H
+            ctx_c = Context(local, max_points=sc_c.n, max_keys=args.max_keys, max_w=Wc, max_h=Hc)
+            ctx_c.gs_set_view_group(8, True)
+            st_c = scene_to_device(sc_c)
+            cc = [camera(c) for c in cams_c]
+            rgb_c = torch.empty((len(cc), 3, Hc, Wc), device="cuda")
+            T_c = torch.empty((len(cc), Hc, Wc), device="cuda")
+            o_c = opts(bg_c, sh_degree=sc_c.sh_degree, blend=blend, flags=base_flags)
+            for _ in range(2):
+                ctx_c.gs_render_views(st_c, cc, Wc, Hc, o_c, rgb_c, T_c, stream)
+                ctx_c.gs_render(st_c, cc[0], Wc, Hc, o_c, rgb_c[0], T_c[0], stream)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            for _ in range(3):
+                ctx_c.gs_render_views(st_c, cc, Wc, Hc, o_c, rgb_c, T_c, stream)
+            e1.record(stream)
+            for _ in range(5):
+                ctx_c.gs_render(st_c, cc[0], Wc, Hc, o_c, rgb_c[0], T_c[0], stream)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            ctx_c.gs_render(st_c, cc[0], Wc, Hc, opts(bg_c, sh_degree=sc_c.sh_degree, flags=GS_FLAG_STATS | base_flags),
+                            rgb_c[0], T_c[0], stream)
+            s_c = ctx_c.gs_last_stats()
+            per_config[name] = {"n_gaussians": sc_c.n, "W": Wc, "H": Hc,
+                                "fps_orbit8": 3 * len(cc) / (e0.elapsed_time(e1) / 1e3),
+                                "ms_single_view": e1.elapsed_time(e2) / 5, "n_visible_view0": s_c.n_visible,
+                                "n_keys_view0": s_c.n_keys, "pairs_evaluated_view0": s_c.pairs_evaluated}
+            ctx_c.close()
+            del st_c, rgb_c, T_c
+        torch.cuda.empty_cache()
+
     # --- end to end through the host-pointer C-ABI entry point ---------------
     e2e = None
     if not args.no_e2e:
@@ -435,7 +473,7 @@ def run_ours(args):
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
                 "roofline": roof, "stages": stages, "clocks": clk,
-                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3, "row_split_one_view": row_split,
+                "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3, "row_split_one_view": row_split, "other_configs": per_config,
                 "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
                                    "pairs_kept": n_kept}}
@@ -461,6 +499,7 @@ def main():
     ap.add_argument("--intersect", default="obox", choices=list(INTERSECT),
                     help="intersection mode of the headline (the others are timed alongside, N3)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N2 resolution sweep")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C2-C4b config shapes")
     ap.add_argument("--sweep-views", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
