@@ -196,10 +196,15 @@ __global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, ui
     if (threadIdx.x == 0) op.finish(s_carry);
 }
 
+// Each block computes its chunk's exclusive prefix itself, as the 64-bit sum of the
+// chunk sums before it (at most a few thousand L2-resident words: no separate
+// single-block scan of the sums, one launch and one dependency fewer); the block of
+// the last chunk also reports the total (op.finish).
 template <class Op>
 __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
     pdl_wait();
     __shared__ uint32_t s_w[NWARP];
+    __shared__ unsigned long long s_pre[NWARP], s_tot[NWARP], s_base;
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -210,6 +215,36 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
         for (int r = 0; r < SORT_ITEMS; r++) {
             const uint32_t e = c * SORT_CHUNK + elem_of(warp, r, lane);
             v[r] = e < n ? op.load(e, aux[r]) : 0u;
+        }
+        // (the element loads above are in flight meanwhile)
+        {   // prefix of the chunk sums before c (and, for the last chunk, the total)
+            const bool last = c + 1 == nchunks;
+            unsigned long long acc = 0, tot = 0;
+            for (uint32_t k = threadIdx.x; k < (last ? nchunks : c); k += SORT_THREADS) {
+                const unsigned long long x = sums[k];
+                if (k < c) acc += x;
+                tot += x;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            }
+            if (lane == 0) {
+                s_pre[warp] = acc;
+                s_tot[warp] = tot;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long p = 0, t = 0;
+                for (int w = 0; w < NWARP; w++) {
+                    p += s_pre[w];
+                    t += s_tot[w];
+                }
+                s_base = p;
+                if (last) op.finish(t);
+            }
+            __syncthreads();
         }
 #pragma unroll
         for (int r = 0; r < SORT_ITEMS; r++) {
@@ -224,7 +259,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
         }
         if (lane == 0) s_w[warp] = wrun;
         __syncthreads();
-        uint64_t base = sums[c];
+        uint64_t base = s_base;
         for (int w = 0; w < warp; w++) base += s_w[w];
 #pragma unroll
         for (int r = 0; r < SORT_ITEMS; r++) {
@@ -1205,9 +1240,8 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
 template <class Op>
 static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint32_t n_points) {
     launch_pdl(k_scan_reduce<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
-    launch_pdl(k_scan_sums<Op>, 1, 1024, 0, st, op, n_points, ws.sums);
     launch_pdl(k_scan_apply<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
-    return 3;
+    return 2;
 }
 
 template <class L>
