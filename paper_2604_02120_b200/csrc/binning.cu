@@ -1041,28 +1041,26 @@ __global__ void __launch_bounds__(256) k_depth_wide_copy(const Counters *cnt, co
     }
 }
 
-// Capacity error path: when the row entries alone overflowed max_keys, the pair
-// offsets were not computed; K (= sum of tiles touched) is still reported.
-__global__ void __launch_bounds__(256) k_keys_on_overflow(const uint32_t *__restrict__ sorted_idx,
-                                                          const uint32_t *__restrict__ touched, Counters *cnt) {
-    pdl_wait();
-    if (!cnt->err || cnt->n_keys != 0) return;
-    const uint32_t nv = cnt->n_visible;
-    unsigned long long acc = 0;
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nv; r += gridDim.x * blockDim.x)
-        acc += touched[sorted_idx[r]];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd((unsigned long long *)&cnt->n_keys, acc);
-}
 
 // one block: per tile row, first entry / first pair / first column chunk; chunk count
+// (Capacity error path: when the row entries alone overflowed max_keys, the pair offsets
+// were not computed; K = the sum of tiles touched is still reported, summed here.)
 __global__ void __launch_bounds__(512) k_row_bounds(const uint32_t *__restrict__ rows_per_ty,
                                                     const uint32_t *__restrict__ poff, Counters *cnt, int gy,
-                                                    uint64_t max_keys, uint32_t *rowinfo) {
+                                                    uint64_t max_keys, uint32_t *rowinfo,
+                                                    const uint32_t *__restrict__ sorted_idx,
+                                                    const uint32_t *__restrict__ touched) {
     pdl_wait();
     __shared__ uint32_t s_w[16];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (cnt->err && cnt->n_keys == 0) {
+        const uint32_t nv = cnt->n_visible;
+        unsigned long long acc = 0;
+        for (uint32_t r = t; r < nv; r += blockDim.x) acc += touched[sorted_idx[r]];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0 && acc) atomicAdd((unsigned long long *)&cnt->n_keys, acc);
+    }
     auto excl = [&](uint32_t v) -> uint32_t {
         uint32_t x = v;
 #pragma unroll
@@ -1331,14 +1329,14 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
                                ws.kt[1], ws.kv[1], CNT_RENT, mk, 0, std::max(1, tby));
         // 5. pair offsets of the entries (kt[0])
         launches += scan_pass(ws, st, grid_k, PairOffsetsOp{ws.kt[1], ws.kt[0], cnt, mk}, (uint32_t)N);
-        launch_pdl(k_keys_on_overflow, nsm, 256, 0, st, ws.sv[0], ws.touched, cnt);
         // 6. row bounds and row-aligned column chunks
-        launch_pdl(k_row_bounds, 1, 512, 0, st, ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo);
+        launch_pdl(k_row_bounds, 1, 512, 0, st, ws.row_total, ws.kt[0], cnt, gy, mk, ws.rowinfo,
+                   (const uint32_t *)ws.sv[0], (const uint32_t *)ws.touched);
         launch_pdl(k_chunk_desc, nsm * 2, 256, 0, st, ws.rowinfo, ws.kt[0], cnt, gy, ws.cdesc, ws.cdesc_last);
         // 7. columns: counts, per-(row, column) scans, tile ranges, stable scatter of the indices
         if (tbx > 8) column_pass<9>(ws, st, grid_k, N, gx, gy, tbx, mk);
         else column_pass<8>(ws, st, grid_k, N, gx, gy, tbx, mk);
-        return launches + 8;
+        return launches + 6;   // row bounds, chunk descriptors, column count / scan / ranges / scatter
     }
     // 3. pair offsets in depth order
     launches += scan_pass(ws, st, grid_n,
