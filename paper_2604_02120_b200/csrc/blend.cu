@@ -56,6 +56,10 @@ namespace gs {
 #define GS_BLEND_NB 32
 #endif
 constexpr int NB = GS_BLEND_NB;         // Gaussians per batch (MMA N: 16 or 32)
+#ifndef GS_BLEND_KSTEPS
+#define GS_BLEND_KSTEPS 2   // K = 8 * KSTEPS: 2 = TF32 hi/lo (R-11); 1 = single TF32 pass (A/B evidence only)
+#endif
+static_assert(GS_BLEND_KSTEPS == 1 || GS_BLEND_KSTEPS == 2, "K = 8 (single TF32) or 16 (hi/lo)");
 static_assert(NB == 16 || NB == 32, "batch = MMA N = 16 or 32 (one producer / builder lane per Gaussian)");
 constexpr int CH = GS_BLEND_CH;         // TMEM columns per compositor load (16 or 32)
 constexpr int STAGES = GS_BLEND_STAGES; // M_g / TMEM ring depth
@@ -178,7 +182,7 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
             const uint32_t hi = f32_to_tf32_rna(v[k]);
             const uint32_t lo = f32_to_tf32_rna(v[k] - __uint_as_float(hi));
             u[k] = hi;
-            u[6 + k] = lo;
+            u[6 + k] = GS_BLEND_KSTEPS == 2 ? lo : 0u;   // K = 8: hi only, the lo columns stay zero
         }
     } else {
 #pragma unroll
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                         const uint32_t a_base = smem_u32(&sm.A[0][0]);
                         const uint32_t b_base = smem_u32(&sm.B[s][0]);
 #pragma unroll
-                        for (int kk = 0; kk < 2; kk++)
+                        for (int kk = 0; kk < GS_BLEND_KSTEPS; kk++)
 #pragma unroll
                             for (int h = 0; h < 2; h++)
                                 mma_tf32(tmem + s * (2 * NB) + h * NB,
