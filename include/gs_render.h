@@ -178,6 +178,18 @@ int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
  * ones still render. GS_ERR_INVALID_ARG if g is not a group of that call. */
 int gs_stream_wait_group(gs_ctx *ctx, void *stream, int g);
 
+/* Asynchronous form of gs_render_views_host (same arguments): returns once the
+ * work is enqueued; `stream` reaches completion only after every frame is in
+ * h_out_rgb / h_out_T. The host inputs must stay valid and unmodified, and the
+ * outputs unread, until then (cudaMemcpyAsync rules; pinned memory). The scene
+ * upload runs on a context stream into one of two device staging buffers, so the
+ * upload of the next call overlaps the rendering of this one (a serving loop of
+ * back-to-back calls pipelines H2D, compute and D2H). */
+int gs_render_views_host_async(gs_ctx *ctx, void *stream, int N, const float *means3D,
+                               const float *scales, const float *rots, const float *opacity,
+                               const float *shs_or_colors, const gs_camera *cams, int n_views,
+                               int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
+
 /* Synchronises the last stream used by ctx and reports counts and the status
  * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */
 int gs_last_stats(gs_ctx *ctx, gs_stats *out);

@@ -37,7 +37,8 @@ GS_FLAG_OBOX = 16
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
            "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times",
-           "gs_debug_set_trace", "gs_set_view_group", "gs_debug_timeline", "gs_stream_wait_group")
+           "gs_debug_set_trace", "gs_set_view_group", "gs_debug_timeline", "gs_stream_wait_group",
+           "gs_render_views_host_async")
 
 
 class GsError(RuntimeError):
@@ -84,6 +85,7 @@ def load():
         "gs_render": [P, P, I, P, P, P, P, P, cam_p, I, I, opt_p, P, P],
         "gs_render_views": [P, P, I, P, P, P, P, P, cam_p, I, I, I, opt_p, P, P],
         "gs_render_views_host": [P, P, I, P, P, P, P, P, cam_p, I, I, I, opt_p, P, P],
+        "gs_render_views_host_async": [P, P, I, P, P, P, P, P, cam_p, I, I, I, opt_p, P, P],
         "gs_last_stats": [P, ctypes.POINTER(gs_stats)],
         "gs_status_string": [I],
         "gs_device_arch": [I],
@@ -202,12 +204,12 @@ class Context:
                                         _ptr(sh), arr, len(cams), W, H, ctypes.byref(o), _ptr(out_rgb),
                                         _ptr(out_T)), "gs_render_views")
 
-    def gs_render_views_host(self, scene_np, cams, W, H, o, h_out_rgb, h_out_T, stream=None):
+    def gs_render_views_host(self, scene_np, cams, W, H, o, h_out_rgb, h_out_T, stream=None, async_=False):
         m, s, r, op, sh, n = scene_np
         arr = (gs_camera * len(cams))(*cams)
-        _check(self.lib.gs_render_views_host(self.h, _stream(stream), n, _ptr(m), _ptr(s), _ptr(r), _ptr(op),
-                                             _ptr(sh), arr, len(cams), W, H, ctypes.byref(o),
-                                             _ptr(h_out_rgb), _ptr(h_out_T)), "gs_render_views_host")
+        fn = self.lib.gs_render_views_host_async if async_ else self.lib.gs_render_views_host
+        _check(fn(self.h, _stream(stream), n, _ptr(m), _ptr(s), _ptr(r), _ptr(op), _ptr(sh), arr, len(cams), W, H,
+                  ctypes.byref(o), _ptr(h_out_rgb), _ptr(h_out_T)), "gs_render_views_host")
 
     def gs_debug_timeline(self, max_spans=4096):
         """[(stage, start_ms, end_ms)] of the GS_FLAG_TIMING spans since gs_stage_times."""

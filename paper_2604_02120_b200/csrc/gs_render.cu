@@ -40,6 +40,13 @@ struct gs_ctx {
     gs::Counters *last_counters = nullptr;   // counters of the last rendered view
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
+    // scene staging, double-buffered (the async entry point uploads call k+1's scene while
+    // call k renders): up_stream copies, ev_scene_free[b] = the last preprocess reading b
+    float *stage[2] = {};
+    size_t stage_cap = 0;
+    int stage_idx = 0;
+    cudaStream_t up_stream = nullptr;
+    cudaEvent_t ev_scene_ready[2] = {}, ev_scene_free[2] = {}, ev_copies_all = nullptr;
     // per staging slot (2 * MAX_VIEW_GROUP frames): the view's blend done / its copy done
     cudaEvent_t view_done[2 * gs::MAX_VIEW_GROUP] = {}, copies_done[2 * gs::MAX_VIEW_GROUP] = {};
     // gs_render_views, concurrent mode: preprocess on pre_stream, the binning chain of view j
@@ -361,6 +368,13 @@ int gs_ctx_destroy(gs_ctx *c) {
         if (c->copies_done[k]) cudaEventDestroy(c->copies_done[k]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (int k = 0; k < 2; k++) {
+        if (c->stage[k]) cudaFree(c->stage[k]);
+        if (c->ev_scene_ready[k]) cudaEventDestroy(c->ev_scene_ready[k]);
+        if (c->ev_scene_free[k]) cudaEventDestroy(c->ev_scene_free[k]);
+    }
+    if (c->ev_copies_all) cudaEventDestroy(c->ev_copies_all);
+    if (c->up_stream) cudaStreamDestroy(c->up_stream);
     delete c;
     return GS_OK;
 }
@@ -435,7 +449,7 @@ static int ensure_streams(gs_ctx *c) {
 static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *means3D, const float *scales,
                              const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
                              int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of,
-                             const GroupHooks *hk = nullptr) {
+                             const GroupHooks *hk = nullptr, cudaEvent_t after_last_pre = nullptr) {
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     const int imode = gs::intersect_mode(o.flags);
     const bool conc = c->concurrent && G > 1;
@@ -469,6 +483,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         c->launches += N > 0 ? 1 : 0;
         int e_prev = mark(c, ps, o);
         span(c, 0, e0, e_prev);
+        if (after_last_pre && v0 + G >= n_views) cudaEventRecord(after_last_pre, ps);   // scene no longer read
         if (conc) {
             cudaEventRecord(c->ev_pre[set], ps);
             for (int j = 0; j < n; j++) {
@@ -543,12 +558,21 @@ int gs_render_views(gs_ctx *c, void *stream, int N, const float *means3D, const 
     return finish(c, st, *o, N);
 }
 
-int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
-                         const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
-                         int n_views, int W, int H, const gs_opts *o, float *h_out_rgb, float *h_out_T) {
+// The host-buffer entry points. The scene is uploaded into one of two device staging
+// buffers on the context's upload stream (after the last preprocess that read that buffer
+// two calls ago), the views render as in gs_render_views, and every frame is copied back
+// on the copy stream as soon as its blend is done (staging slot v % 2G, reused once its
+// previous copy completed). sync: the call returns after `stream` and the copies are
+// done. async: it returns at once; `stream` reaches completion only after the frames are
+// on the host, and the next call's upload overlaps this call's rendering.
+static int render_views_host_impl(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
+                                  const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
+                                  int n_views, int W, int H, const gs_opts *o, float *h_out_rgb, float *h_out_T,
+                                  bool async) {
     if (!c || !o || !cams || n_views < 0 || N < 0) return GS_ERR_INVALID_ARG;
     if (N > c->max_points) return GS_ERR_CAPACITY;
     if (W <= 0 || H <= 0 || W > c->max_w || H > c->max_h) return GS_ERR_INVALID_ARG;
+    if (!h_out_rgb || !h_out_T) return GS_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int ncoef = o->sh_degree < 0 ? 1 : o->sh_stride;
@@ -556,13 +580,24 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
                  f_sh = 3 * (size_t)N * ncoef;
     auto pad4 = [](size_t x) { return (x + 3) & ~size_t(3); };
     const size_t total = pad4(f_means) + pad4(f_scales) + pad4(f_rots) + pad4(f_op) + pad4(f_sh);
-    if (total * sizeof(float) > c->ws.stage_bytes) {
-        if (c->ws.stage) cudaFree(c->ws.stage);
-        c->ws.stage = nullptr;
-        if (check_cuda(cudaMalloc(&c->ws.stage, total * sizeof(float)))) return GS_ERR_CUDA;
-        c->ws.stage_bytes = total * sizeof(float);
+    if (!c->up_stream) {
+        if (check_cuda(cudaStreamCreateWithFlags(&c->up_stream, cudaStreamNonBlocking))) return GS_ERR_CUDA;
+        for (int k = 0; k < 2; k++) {
+            cudaEventCreateWithFlags(&c->ev_scene_ready[k], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&c->ev_scene_free[k], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&c->ev_copies_all, cudaEventDisableTiming);
     }
-    if (!c->frame_rgb) {   // 2 staging slots of MAX_VIEW_GROUP frames, a copy stream and its events
+    if (total * sizeof(float) > c->stage_cap) {
+        if (check_cuda(cudaDeviceSynchronize())) return GS_ERR_CUDA;   // staging in use by earlier calls
+        for (int k = 0; k < 2; k++) {
+            if (c->stage[k]) cudaFree(c->stage[k]);
+            c->stage[k] = nullptr;
+            if (check_cuda(cudaMalloc(&c->stage[k], total * sizeof(float)))) return GS_ERR_CUDA;
+        }
+        c->stage_cap = total * sizeof(float);
+    }
+    if (!c->frame_rgb) {   // 2G staging frames (G <= MAX_VIEW_GROUP), a copy stream and its events
         const size_t fr = 2 * gs::MAX_VIEW_GROUP * (size_t)c->max_w * c->max_h;
         if (check_cuda(cudaMalloc(&c->frame_rgb, 3 * fr * sizeof(float)))) return GS_ERR_CUDA;
         if (check_cuda(cudaMalloc(&c->frame_T, fr * sizeof(float)))) return GS_ERR_CUDA;
@@ -572,20 +607,22 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
             cudaEventCreateWithFlags(&c->copies_done[k], cudaEventDisableTiming);
         }
     }
-    float *d = c->ws.stage;
+    const int b = c->stage_idx;
+    c->stage_idx ^= 1;
+    float *d = c->stage[b];
     float *dm = d, *ds = dm + pad4(f_means), *dr = ds + pad4(f_scales), *dop = dr + pad4(f_rots),
           *dsh = dop + pad4(f_op);
     for (int v = 0; v < n_views; v++)
         if (int rc = validate(c, N, dm, ds, dr, dop, dsh, &cams[v], W, H, o)) return rc;
-    if (!h_out_rgb || !h_out_T) return GS_ERR_INVALID_ARG;
-    cudaMemcpyAsync(dm, means3D, f_means * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(ds, scales, f_scales * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, st);
-    // Frames come back on the copy stream view by view: view v renders into staging slot
-    // v % (2G) and is copied to the host as soon as its blend is done, while later views
-    // render; the slot is reused 2G views later, after its copy completed.
+    cudaStream_t up = c->up_stream;
+    cudaStreamWaitEvent(up, c->ev_scene_free[b], 0);   // no preprocess still reads buffer b
+    cudaMemcpyAsync(dm, means3D, f_means * 4, cudaMemcpyHostToDevice, up);
+    cudaMemcpyAsync(ds, scales, f_scales * 4, cudaMemcpyHostToDevice, up);
+    cudaMemcpyAsync(dr, rots, f_rots * 4, cudaMemcpyHostToDevice, up);
+    cudaMemcpyAsync(dop, opacity, f_op * 4, cudaMemcpyHostToDevice, up);
+    cudaMemcpyAsync(dsh, shs, f_sh * 4, cudaMemcpyHostToDevice, up);
+    cudaEventRecord(c->ev_scene_ready[b], up);
+    cudaStreamWaitEvent(st, c->ev_scene_ready[b], 0);
     const size_t plane = (size_t)W * H, mplane = (size_t)c->max_w * c->max_h;
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     gs_opts ov = *o;
@@ -605,29 +642,45 @@ int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, c
     } cp{c, h_out_rgb, h_out_T, prgb.data(), pT.data(), plane, 2 * G};
     GroupHooks hk;
     hk.user = &cp;
-    hk.pre_blend = [](void *u, cudaStream_t bl, int v) {
+    hk.pre_blend = [](void *u, cudaStream_t bl, int v) {   // the staging slot's previous copy is done
         Copies &k = *static_cast<Copies *>(u);
-        if (v >= k.nslots) cudaStreamWaitEvent(bl, k.c->copies_done[v % k.nslots], 0);   // slot free again
+        cudaStreamWaitEvent(bl, k.c->copies_done[v % k.nslots], 0);
     };
     hk.post_blend = [](void *u, cudaStream_t bl, int v) {
         Copies &k = *static_cast<Copies *>(u);
-        const int s = v % k.nslots;
-        cudaEventRecord(k.c->view_done[s], bl);
-        cudaStreamWaitEvent(k.c->copy_stream, k.c->view_done[s], 0);
+        const int sl = v % k.nslots;
+        cudaEventRecord(k.c->view_done[sl], bl);
+        cudaStreamWaitEvent(k.c->copy_stream, k.c->view_done[sl], 0);
         cudaMemcpyAsync(k.h_rgb + (size_t)v * 3 * k.plane, k.prgb[v], 3 * k.plane * 4, cudaMemcpyDeviceToHost,
                         k.c->copy_stream);
         cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost, k.c->copy_stream);
-        cudaEventRecord(k.c->copies_done[s], k.c->copy_stream);
+        cudaEventRecord(k.c->copies_done[sl], k.c->copy_stream);
     };
     if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams, n_views, W, H, ov, prgb.data(), pT.data(),
-                                   &hk))
+                                   &hk, c->ev_scene_free[b]))
         return rc;
-    int rc = check_cuda(cudaStreamSynchronize(c->copy_stream));
-    if (!rc) rc = check_cuda(cudaStreamSynchronize(st));
+    cudaEventRecord(c->ev_copies_all, c->copy_stream);
+    cudaStreamWaitEvent(st, c->ev_copies_all, 0);   // st completes only once the frames are on the host
+    if (async) return finish(c, st, ov, N);
+    int rc = check_cuda(cudaStreamSynchronize(st));
     if (rc) return rc;
     gs_opts os = *o;
     os.flags |= GS_FLAG_SYNC;
     return finish(c, st, os, N);
+}
+
+int gs_render_views_host(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
+                         const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
+                         int n_views, int W, int H, const gs_opts *o, float *h_out_rgb, float *h_out_T) {
+    return render_views_host_impl(c, stream, N, means3D, scales, rots, opacity, shs, cams, n_views, W, H, o, h_out_rgb,
+                                  h_out_T, false);
+}
+
+int gs_render_views_host_async(gs_ctx *c, void *stream, int N, const float *means3D, const float *scales,
+                               const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
+                               int n_views, int W, int H, const gs_opts *o, float *h_out_rgb, float *h_out_T) {
+    return render_views_host_impl(c, stream, N, means3D, scales, rots, opacity, shs, cams, n_views, W, H, o, h_out_rgb,
+                                  h_out_T, true);
 }
 
 int gs_debug_timeline(gs_ctx *c, double *out, int max_spans, int *n_spans) {

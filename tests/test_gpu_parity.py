@@ -531,3 +531,30 @@ def test_obox_opacity_edge_cases_bit_exact():
     t = np.float32(255.0) * scene.opacity.astype(np.float32)   # the binary32 product step 10b tests
     assert not vis[t < 1.0].any()
     assert vis[t >= 1.0].any()
+
+
+def test_host_async_entry_point_matches_device_frames():
+    """gs_render_views_host_async back to back (double-buffered scene staging, frames
+    copied back on a side stream) gives the frames of gs_render_views, call after call."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device, scene_to_host
+    scene = synth.unbounded_scene(30000, 111, sh_degree=3)
+    cams = synth.orbit_cameras(9, 192, 128, 1.0)
+    ctx = Context(0, max_points=scene.n, max_keys=1 << 22, max_w=192, max_h=128)
+    ctx.gs_set_view_group(4, True)
+    o = opts((0.2, 0.1, 0.0), sh_degree=3, flags=16)
+    st = scene_to_device(scene)
+    r = torch.empty((9, 3, 128, 192), device="cuda")
+    t = torch.empty((9, 128, 192), device="cuda")
+    ctx.gs_render_views(st, [camera(c) for c in cams], 192, 128, o, r, t)
+    torch.cuda.synchronize()
+    ref_r, ref_t = r.cpu(), t.cpu()
+    hs = scene_to_host(scene)
+    outs = [(torch.full((9, 3, 128, 192), float("nan")).pin_memory(), torch.full((9, 128, 192), float("nan")).pin_memory())
+            for _ in range(3)]
+    for hr, ht in outs:   # three calls in flight on one stream
+        ctx.gs_render_views_host(hs, [camera(c) for c in cams], 192, 128, o, hr, ht, async_=True)
+    torch.cuda.synchronize()
+    for hr, ht in outs:
+        assert torch.equal(hr, ref_r) and torch.equal(ht, ref_t)
+    ctx.close()
