@@ -449,15 +449,20 @@ static int ensure_streams(gs_ctx *c) {
 static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *means3D, const float *scales,
                              const float *rots, const float *opacity, const float *shs, const gs_camera *cams,
                              int n_views, int W, int H, const gs_opts &o, float *const *rgb_of, float *const *T_of,
-                             const GroupHooks *hk = nullptr, cudaEvent_t after_last_pre = nullptr) {
+                             const GroupHooks *hk = nullptr, cudaEvent_t after_last_pre = nullptr,
+                             cudaEvent_t start_event = nullptr) {
     const int G = std::max(1, std::min(c->view_group, gs::MAX_VIEW_GROUP));
     const int imode = gs::intersect_mode(o.flags);
     const bool conc = c->concurrent && G > 1;
     if (conc) {
         if (int rc = ensure_streams(c)) return rc;
-        cudaEventRecord(c->ev_start, st);
-        cudaStreamWaitEvent(c->pre_stream, c->ev_start, 0);
-        cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
+        if (start_event) {   // the caller orders the inputs itself (the host entry point's upload)
+            cudaStreamWaitEvent(c->pre_stream, start_event, 0);
+        } else {
+            cudaEventRecord(c->ev_start, st);
+            cudaStreamWaitEvent(c->pre_stream, c->ev_start, 0);
+            cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
+        }
     }
     int last_set = 0;
     for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
@@ -474,7 +479,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             pv.out[j] = gs::pre_out_of(*w[j], false);
         }
         cudaStream_t ps = conc ? c->pre_stream : st;
-        if (conc && g >= 2) cudaStreamWaitEvent(ps, c->ev_blended[set], 0);   // slot set free again
+        if (conc) cudaStreamWaitEvent(ps, c->ev_blended[set], 0);   // slot set free again (this or an earlier call)
         const int e0 = mark(c, ps, o);
         if (N == 0)
             for (int j = 0; j < n; j++) cudaMemsetAsync(w[j]->counters, 0, sizeof(gs::Counters), ps);
@@ -656,8 +661,11 @@ static int render_views_host_impl(gs_ctx *c, void *stream, int N, const float *m
         cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost, k.c->copy_stream);
         cudaEventRecord(k.c->copies_done[sl], k.c->copy_stream);
     };
+    // async: the views' preprocess waits for this call's upload only (not for the caller's
+    // stream, which still waits for the previous call's last copies), so back-to-back calls
+    // overlap; the slot sets and staging frames are protected by their own events
     if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams, n_views, W, H, ov, prgb.data(), pT.data(),
-                                   &hk, c->ev_scene_free[b]))
+                                   &hk, c->ev_scene_free[b], async ? c->ev_scene_ready[b] : nullptr))
         return rc;
     cudaEventRecord(c->ev_copies_all, c->copy_stream);
     cudaStreamWaitEvent(st, c->ev_copies_all, 0);   // st completes only once the frames are on the host
