@@ -81,6 +81,11 @@ enum {
                            * maximum over the tile's pixel box is alpha < 1/255 (with a margin
                            * larger than the exponent error). Such pairs are alpha-skipped by the
                            * blend anyway, so the image is bit-identical; binning keeps a subset. */
+    GS_FLAG_STATIC_SCENE = 32u, /* gs_render_views: no work pending on `stream` writes the scene
+                           * arrays (they are resident and unchanged, as in an orbit or serving
+                           * loop), so the call's preprocess and binning may start before the
+                           * caller's earlier work on `stream` (e.g. the previous call's last
+                           * blends) has finished; frames are still written in stream order. */
     GS_FLAG_OBOX = 16u    /* opacity-aware box (cheaper): the vanilla rect clipped to the
                            * bounding box of the ellipse where alpha >= 1/255 can hold (margin
                            * 5e-3 in ln alpha), and Gaussians with 255*opacity < 1 culled; no

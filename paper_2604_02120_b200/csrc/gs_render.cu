@@ -460,7 +460,11 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             cudaStreamWaitEvent(c->pre_stream, start_event, 0);
         } else {
             cudaEventRecord(c->ev_start, st);
-            cudaStreamWaitEvent(c->pre_stream, c->ev_start, 0);
+            // GS_FLAG_STATIC_SCENE: no pending work on `stream` writes the scene, so the
+            // preprocess (and binning) of this call may start while the caller's earlier
+            // work -- e.g. the previous call's last blends -- still runs; the blends still
+            // wait for it (they write the caller's frame buffers)
+            if (!(o.flags & GS_FLAG_STATIC_SCENE)) cudaStreamWaitEvent(c->pre_stream, c->ev_start, 0);
             cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
         }
     }
@@ -661,11 +665,11 @@ static int render_views_host_impl(gs_ctx *c, void *stream, int N, const float *m
         cudaMemcpyAsync(k.h_T + (size_t)v * k.plane, k.pT[v], k.plane * 4, cudaMemcpyDeviceToHost, k.c->copy_stream);
         cudaEventRecord(k.c->copies_done[sl], k.c->copy_stream);
     };
-    // async: the views' preprocess waits for this call's upload only (not for the caller's
-    // stream, which still waits for the previous call's last copies), so back-to-back calls
+    // the views' preprocess waits for this call's upload only (not for the caller's stream,
+    // which still waits for the previous call's last copies), so back-to-back async calls
     // overlap; the slot sets and staging frames are protected by their own events
     if (int rc = render_views_impl(c, st, N, dm, ds, dr, dop, dsh, cams, n_views, W, H, ov, prgb.data(), pT.data(),
-                                   &hk, c->ev_scene_free[b], async ? c->ev_scene_ready[b] : nullptr))
+                                   &hk, c->ev_scene_free[b], c->ev_scene_ready[b]))
         return rc;
     cudaEventRecord(c->ev_copies_all, c->copy_stream);
     cudaStreamWaitEvent(st, c->ev_copies_all, 0);   // st completes only once the frames are on the host

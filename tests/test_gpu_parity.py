@@ -334,7 +334,7 @@ def test_tight_binning_is_an_alpha_exact_subset(case):
             assert a.max() < 1.0 / 255.0, (t, i, a.max())
 
 
-@pytest.mark.parametrize("flags", [0, 8])
+@pytest.mark.parametrize("flags", [0, 8, 16 | 32])
 def test_view_groups_are_bit_identical_to_single_views(flags):
     """gs_render_views reads the scene once per view group (k_preprocess over up to 4
     views); every frame must equal the single-view gs_render of the same camera, for
