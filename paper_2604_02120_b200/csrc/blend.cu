@@ -616,7 +616,7 @@ template <int BATCH>
 struct SmemMMA {
     uint32_t Mg[BATCH][16];            // rows: word 4q + j holds K index q + 4j
     float4 rgb[BATCH];
-    float tr[NCW][32 * MMA_TS];        // per-warp transpose buffer
+    float tr[MMA_THREADS / 32][32 * MMA_TS];   // per-warp transpose buffer
     int tile;
 };
 
