@@ -44,7 +44,7 @@ namespace gs {
 #define GS_BLEND_RAW 4
 #endif
 #ifndef GS_BLEND_PF
-#define GS_BLEND_PF 4
+#define GS_BLEND_PF 2
 #endif
 #ifndef GS_BLEND_MINB
 #define GS_BLEND_MINB 4      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
