@@ -86,8 +86,8 @@ __device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint3
 // Every visible z > znear > 0, so the subtraction keeps the order of the raw bits
 // (R-13), and depths below znear * 2^16 (13107 at znear 0.2) give keys < 2^27:
 // three 9-bit passes sort them; a larger key sets wide_depth and a 4th pass runs.
-struct CompactOp {   // visible flags -> (depth key, index) of the visible Gaussians, index order
-    const uint32_t *touched, *depth_bits;
+struct CompactOp {   // used slots -> (depth key, slot) of the visible Gaussians, index order
+    const uint32_t *wcount, *depth_bits;   // slot s is used iff s % 32 < wcount[s / 32]
     uint32_t *out_k, *out_v;
     Counters *cnt;
     uint32_t dbase;   // bits(znear) if znear > 0, else 0 (raw bits, always 4 passes)
@@ -95,10 +95,10 @@ struct CompactOp {   // visible flags -> (depth key, index) of the visible Gauss
     struct Aux {
         uint32_t depth;
     };
-    __device__ uint32_t load(uint32_t i) const { return touched[i] > 0 ? 1u : 0u; }
+    __device__ uint32_t load(uint32_t i) const { return (i & 31u) < wcount[i >> 5] ? 1u : 0u; }
     __device__ uint32_t load(uint32_t i, Aux &a) const {
         a.depth = depth_bits[i];   // unconditional: both loads in flight at once
-        return touched[i] > 0 ? 1u : 0u;
+        return (i & 31u) < wcount[i >> 5] ? 1u : 0u;
     }
     __device__ void emit(uint32_t i, uint64_t pos, uint32_t v, const Aux &a) const {
         if (v) {
@@ -1290,7 +1290,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
     // 1. compaction of the visible Gaussians (index order), keys relative to the near plane
     uint32_t dbase = 0;
     if (znear > 0.f) memcpy(&dbase, &znear, 4);
-    launches += scan_pass(ws, st, grid_n, CompactOp{ws.touched, ws.depth_bits, ws.sk[1], ws.sv[1], cnt, dbase},
+    launches += scan_pass(ws, st, grid_n, CompactOp{ws.wcount, ws.depth_bits, ws.sk[1], ws.sv[1], cnt, dbase},
                           (uint32_t)N);
     // 2. depth sort: 3 stable passes of 9 bits (sk/sv 1 -> 0 -> 1 -> 0); the last one also
     //    gathers each Gaussian's rect (and tile mask) into depth order. Keys >= 2^27 (a

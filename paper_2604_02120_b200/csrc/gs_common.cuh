@@ -30,7 +30,12 @@ constexpr int MAX_TILES = 1 << 20;   // 16384 x 16384 px; one-level binning sort
 
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
-    // per Gaussian (max_points)
+    // per Gaussian SLOT (max_points): the preprocess packs the visible Gaussians of each
+    // warp of 32 (index order) at the start of the warp's 32 slots (culled ones write
+    // nothing); slot s is used iff s % 32 < wcount[s / 32]. The per-Gaussian arrays below
+    // are slot-addressed; the binning's values, and hence the blend's gathers, are slots.
+    uint32_t *wcount;          // [N/32+1] visible Gaussians per warp of 32
+    uint32_t *orig;            // [N] Gaussian index of each used slot (debug outputs)
     uint32_t *depth_bits;      // [N] raw IEEE bits of the camera depth
     float2 *xy;                // [N] projected mean (pixels)
     float4 *conic_o;           // [N] (A, B, C, opacity)
@@ -74,6 +79,8 @@ inline int intersect_mode(unsigned flags) {
 
 // ---- per-view outputs of the preprocess (a view group shares one scene read) ----
 struct PreOut {
+    uint32_t *wcount;
+    uint32_t *orig;
     uint32_t *depth_bits;
     float2 *xy;
     float4 *conic_o;

@@ -91,6 +91,7 @@ cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
     cudaError_t e = cudaSuccess;
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
+    A(w.wcount, N / 32 + 1); A(w.orig, N);
     A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
     A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
     A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
@@ -103,7 +104,7 @@ cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
 }
 
 void free_ws(gs::Workspace &w) {
-    void *ptrs[] = {w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+    void *ptrs[] = {w.wcount, w.orig, w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
                     w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
                     w.ranges, w.sums, w.cmat, w.row_total, w.cdesc, w.cdesc_last, w.tile_cnt, w.rowinfo,
                     w.counters, w.stage};
@@ -244,40 +245,33 @@ __global__ void k_pack_splats(int N, const float *xy, const float *conic, const 
     if (rgb) orgb[i] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
 }
 
+// debug preprocess: scatter the slot-addressed outputs back to Gaussian order (the
+// outputs were zeroed first, so culled Gaussians read all zero)
 __global__ void k_unpack_pre(int N, gs::Workspace ws, float *depth, float *xy, float *conic, float *rgb,
                              int32_t *rect, int32_t *radius, uint32_t *touched) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    if (ws.touched[i] == 0) {   // culled: the preprocess writes only touched = 0
-        depth[i] = 0.f;
-        xy[2 * i] = xy[2 * i + 1] = 0.f;
-        conic[3 * i] = conic[3 * i + 1] = conic[3 * i + 2] = 0.f;
-        rgb[3 * i] = rgb[3 * i + 1] = rgb[3 * i + 2] = 0.f;
-        rect[4 * i] = rect[4 * i + 1] = rect[4 * i + 2] = rect[4 * i + 3] = 0;
-        radius[i] = 0;
-        touched[i] = 0u;
-        return;
-    }
-    depth[i] = __uint_as_float(ws.depth_bits[i]);
-    xy[2 * i] = ws.xy[i].x;
-    xy[2 * i + 1] = ws.xy[i].y;
-    const float4 co = ws.conic_o[i];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= N || (uint32_t)(s & 31) >= ws.wcount[s >> 5]) return;
+    const uint32_t i = ws.orig[s];
+    depth[i] = __uint_as_float(ws.depth_bits[s]);
+    xy[2 * i] = ws.xy[s].x;
+    xy[2 * i + 1] = ws.xy[s].y;
+    const float4 co = ws.conic_o[s];
     conic[3 * i] = co.x; conic[3 * i + 1] = co.y; conic[3 * i + 2] = co.z;
-    const float4 c = ws.rgb[i];
+    const float4 c = ws.rgb[s];
     rgb[3 * i] = c.x; rgb[3 * i + 1] = c.y; rgb[3 * i + 2] = c.z;
-    const ushort4 r = ws.rect[i];
+    const ushort4 r = ws.rect[s];
     rect[4 * i] = r.x; rect[4 * i + 1] = r.y; rect[4 * i + 2] = r.z; rect[4 * i + 3] = r.w;
-    radius[i] = ws.radius[i];
-    touched[i] = ws.touched[i];
+    radius[i] = ws.radius[s];
+    touched[i] = ws.touched[s];
 }
 
-__global__ void k_keys_out(const uint2 *ranges, const uint32_t *idx, const uint32_t *depth_bits, uint64_t *keys,
-                           uint32_t *vals) {
+__global__ void k_keys_out(const uint2 *ranges, const uint32_t *idx, const uint32_t *depth_bits,
+                           const uint32_t *orig, uint64_t *keys, uint32_t *vals) {
     const uint2 rg = ranges[blockIdx.x];
     for (uint32_t k = rg.x + threadIdx.x; k < rg.y; k += blockDim.x) {
-        const uint32_t i = idx[k];
-        keys[k] = ((uint64_t)blockIdx.x << 32) | depth_bits[i];
-        vals[k] = i;
+        const uint32_t s = idx[k];   // slot -> (tile << 32 | depth bits, Gaussian index)
+        keys[k] = ((uint64_t)blockIdx.x << 32) | depth_bits[s];
+        vals[k] = orig[s];
     }
 }
 
@@ -771,7 +765,16 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
                           o->scale_modifier, *cam, W, H, gs::intersect_mode(o->flags), true, 0,
                           gs::ceil_div_i(H, GS_TILE));
     c->last_counters = c->ws.counters;
-    if (N > 0) k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
+    if (N > 0) {
+        cudaMemsetAsync(depth, 0, sizeof(float) * N, st);
+        cudaMemsetAsync(xy, 0, sizeof(float) * 2 * N, st);
+        cudaMemsetAsync(conic, 0, sizeof(float) * 3 * N, st);
+        cudaMemsetAsync(rgb, 0, sizeof(float) * 3 * N, st);
+        cudaMemsetAsync(rect, 0, sizeof(int32_t) * 4 * N, st);
+        cudaMemsetAsync(radius, 0, sizeof(int32_t) * N, st);
+        cudaMemsetAsync(touched, 0, sizeof(uint32_t) * N, st);
+        k_unpack_pre<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, c->ws, depth, xy, conic, rgb, rect, radius, touched);
+    }
     return finish(c, st, *o, N);
 }
 
@@ -792,7 +795,8 @@ int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const
     if (s.status) return s.status;
     if (s.n_keys > capacity) return GS_ERR_CAPACITY;
     const int ntiles = gs::ceil_div_i(W, GS_TILE) * gs::ceil_div_i(H, GS_TILE);
-    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[0], c->ws.depth_bits, keys, vals);
+    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[0], c->ws.depth_bits, c->ws.orig, keys,
+                                                          vals);
     cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
     if (check_cuda(cudaStreamSynchronize(st))) return GS_ERR_CUDA;
     return GS_OK;

@@ -207,13 +207,16 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0)   // the frames' device counters (no memset node: keeps PDL chained)
         for (int v = 0; v < pv.n; v++) *pv.out[v].counters = Counters{};
-    if (i >= N) return;
+    if ((i & ~31) >= N) return;   // whole warps only: the slot packing below votes per warp
+    const bool in = i < N;
+    const uint32_t lane = threadIdx.x & 31u;
     const int gx = (W + GS_TILE - 1) / GS_TILE, gy = (H + GS_TILE - 1) / GS_TILE;
 
-    const float px = __ldcs(means + 3 * i), py = __ldcs(means + 3 * i + 1), pz = __ldcs(means + 3 * i + 2);
-    const float4 q = __ldcs(rots + i);
-    const float s0 = __ldcs(scales + 3 * i), s1 = __ldcs(scales + 3 * i + 1), s2 = __ldcs(scales + 3 * i + 2);
-    const float op = __ldcs(opacity + i);
+    const int ii = in ? i : N - 1;   // tail lanes read a valid record and are culled below
+    const float px = __ldcs(means + 3 * ii), py = __ldcs(means + 3 * ii + 1), pz = __ldcs(means + 3 * ii + 2);
+    const float4 q = __ldcs(rots + ii);
+    const float s0 = __ldcs(scales + 3 * ii), s1 = __ldcs(scales + 3 * ii + 1), s2 = __ldcs(scales + 3 * ii + 2);
+    const float op = __ldcs(opacity + ii);
     float S[3][3];
     bool have_cov = false, have_sh = false;
     // the SH record, once loaded, lives in shared memory (coefficient-major: conflict-free)
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         const float vx = __fmaf_rn(R[2], pz, __fmaf_rn(R[1], py, __fmaf_rn(R[0], px, cam.t[0])));
         const float vy = __fmaf_rn(R[5], pz, __fmaf_rn(R[4], py, __fmaf_rn(R[3], px, cam.t[1])));
         const float vz = __fmaf_rn(R[8], pz, __fmaf_rn(R[7], py, __fmaf_rn(R[6], px, cam.t[2])));
-        if (vz > cam.znear) {
+        if (in && vz > cam.znear) {
             if (!have_cov) {   // 2-4, once per Gaussian
                 cov3d(q, s0, s1, s2, scale_mod, S);
                 have_cov = true;
@@ -292,21 +295,16 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
             vis = ymax > ymin;
         }
         uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
-        if (tight && vis) {   // the stored rect becomes the opacity-aware box, the mask its kept tiles
-            unsigned long long m = 0ull;
-            vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, m, n_tiles);
-            out.tmask[i] = m;
-        }
-        if (!vis) {   // culled: every array is still written (full sectors: no L2 partial-write fills)
-            out.depth_bits[i] = 0u;
-            out.xy[i] = make_float2(0.f, 0.f);
-            out.conic_o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            out.rgb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            out.rect[i] = make_ushort4(0, 0, 0, 0);
-            out.touched[i] = 0u;
-            if (out.radius) out.radius[i] = 0;
-            continue;
-        }
+        unsigned long long tm = ~0ull;
+        if (tight && vis)   // the stored rect becomes the opacity-aware box, the mask its kept tiles
+            vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, tm, n_tiles);
+        // slot packing: the warp's visible Gaussians (index order) take slots warp*32 + 0, 1, ...;
+        // culled ones write nothing (dense writes, no partial-sector fills but one per warp)
+        const uint32_t bal = __ballot_sync(0xffffffffu, vis);
+        if (lane == 0) out.wcount[i >> 5] = __popc(bal);
+        if (!vis) continue;
+        const int slot = (i & ~31) + __popc(bal & ((1u << lane) - 1u));
+        if (tight) out.tmask[slot] = tm;
         // 11. colour
         float col[3];
         if (sh_degree < 0) {
@@ -334,20 +332,21 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
             }
             sh_colour(K, sh_degree, px, py, pz, cam, col);
         }
-        // 12. outputs
-        out.depth_bits[i] = __float_as_uint(vz);
-        out.xy[i] = make_float2(mx, my);
-        out.conic_o[i] = make_float4(cA, cB, cC, op);
-        out.rgb[i] = make_float4(col[0], col[1], col[2], 0.f);
-        out.rect[i] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
-                                   (unsigned short)ymax);
-        out.touched[i] = n_tiles;
-        if (out.radius) out.radius[i] = r;
+        // 12. outputs (slot-addressed)
+        out.orig[slot] = (uint32_t)i;
+        out.depth_bits[slot] = __float_as_uint(vz);
+        out.xy[slot] = make_float2(mx, my);
+        out.conic_o[slot] = make_float4(cA, cB, cC, op);
+        out.rgb[slot] = make_float4(col[0], col[1], col[2], 0.f);
+        out.rect[slot] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
+                                      (unsigned short)ymax);
+        out.touched[slot] = n_tiles;
+        if (out.radius) out.radius[slot] = r;
     }
 }
 
 PreOut pre_out_of(const Workspace &ws, bool with_radius) {
-    return PreOut{ws.depth_bits, ws.xy, ws.conic_o, ws.rgb, ws.rect, ws.touched, ws.tmask,
+    return PreOut{ws.wcount, ws.orig, ws.depth_bits, ws.xy, ws.conic_o, ws.rgb, ws.rect, ws.touched, ws.tmask,
                   with_radius ? ws.radius : nullptr, ws.counters};
 }
 
