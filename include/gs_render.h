@@ -196,7 +196,10 @@ int gs_render_views_host_async(gs_ctx *ctx, void *stream, int N, const float *me
                                int W, int H, const gs_opts *opts, float *h_out_rgb, float *h_out_T);
 
 /* Synchronises the last stream used by ctx and reports counts and the status
- * of the last frame (e.g. GS_ERR_CAPACITY with the required n_keys). */
+ * of the last call (e.g. GS_ERR_CAPACITY with the required n_keys). For a
+ * multi-view call the status covers every view (any view over capacity gives
+ * GS_ERR_CAPACITY and n_keys = the largest K of the call's views); the other
+ * counts are the last view's. */
 int gs_last_stats(gs_ctx *ctx, gs_stats *out);
 
 /* Sums of the per-stage device times (ms) of all frames rendered with

@@ -1275,8 +1275,28 @@ static void column_pass(const Workspace &ws, cudaStream_t st, int grid, int N, i
     }
 }
 
+// the view's capacity error and K into the context's per-call accumulator
+__global__ void k_sticky(const Counters *cnt, Sticky *sticky) {
+    pdl_wait();
+    if (cnt->err) atomicOr(&sticky->err, cnt->err);
+    atomicMax(&sticky->max_keys, (unsigned long long)cnt->n_keys);
+}
+
+static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, bool tight,
+                        float znear);
+
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &,
                    bool tight, float znear) {
+    int launches = binning_body(ws, st, N, max_keys, ntiles, gx, tight, znear);
+    if (ws.sticky) {
+        launch_pdl(k_sticky, 1, 1, 0, st, (const Counters *)ws.counters, ws.sticky);
+        launches++;
+    }
+    return launches;
+}
+
+static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, bool tight,
+                        float znear) {
     Counters *cnt = ws.counters;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

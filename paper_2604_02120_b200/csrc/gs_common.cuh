@@ -26,6 +26,14 @@ struct Counters {
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
 
+// errors of a multi-view call, accumulated over its views (each view's counters are
+// reused by later views of the call): reset at the call's start, read by gs_last_stats
+struct Sticky {
+    uint32_t err;
+    uint32_t pad;
+    unsigned long long max_keys;   // largest K of the call's views (the capacity a retry needs)
+};
+
 constexpr int MAX_TILES = 1 << 20;   // 16384 x 16384 px; one-level binning sorts ceil(tile bits / 8) passes
 
 // ---- device workspace owned by the context ---------------------------------
@@ -66,6 +74,7 @@ struct Workspace {
     uint32_t *row_total;       // [512] digit totals
     size_t max_chunks;
     Counters *counters;
+    Sticky *sticky;            // the context's (shared by every workspace)
     // scene staging for the host-pointer entry point
     float *stage;
     size_t stage_bytes;

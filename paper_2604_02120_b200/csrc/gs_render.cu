@@ -38,6 +38,7 @@ struct gs_ctx {
     gs::Workspace vws[2 * gs::MAX_VIEW_GROUP] = {};
     bool vws_alloc[2 * gs::MAX_VIEW_GROUP] = {};
     gs::Counters *last_counters = nullptr;   // counters of the last rendered view
+    gs::Sticky *sticky = nullptr;            // errors / largest K over the views of the last call
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
     // scene staging, double-buffered (the async entry point uploads call k+1's scene while
@@ -169,6 +170,7 @@ int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
         c->vws_alloc[v] = true;   // (partially allocated pointers are freed by gs_ctx_destroy)
         if (int rc = check_cuda(alloc_ws(w, (size_t)c->max_points, (size_t)c->max_keys, (size_t)c->max_tiles)))
             return rc;
+        w.sticky = c->sticky;
     }
     *out = &w;
     return GS_OK;
@@ -186,6 +188,7 @@ void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const 
 int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
                   const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
     const int e0 = mark(c, st, o);
+    cudaMemsetAsync(c->sticky, 0, sizeof(gs::Sticky), st);   // this call's error accumulator
     if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
     int y0 = 0, y1 = 0;
     gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, y0, y1);
@@ -323,6 +326,9 @@ int gs_ctx_create(gs_ctx **out, int device, int64_t max_points, int64_t max_keys
     c->max_h = max_h;
     c->max_tiles = gs::ceil_div_i(max_w, GS_TILE) * gs::ceil_div_i(max_h, GS_TILE);
     cudaError_t e = alloc_ws(c->ws, (size_t)max_points, (size_t)max_keys, (size_t)c->max_tiles);
+    if (e == cudaSuccess) e = alloc(c->sticky, 1);
+    if (e == cudaSuccess) e = cudaMemset(c->sticky, 0, sizeof(gs::Sticky));
+    c->ws.sticky = c->sticky;
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         gs_ctx_destroy(c);
@@ -337,6 +343,7 @@ int gs_ctx_destroy(gs_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     free_ws(c->ws);
+    if (c->sticky) cudaFree(c->sticky);
     for (void *p : {(void *)c->frame_rgb, (void *)c->frame_T})
         if (p) cudaFree(p);
     for (int v = 1; v < 2 * gs::MAX_VIEW_GROUP; v++)
@@ -462,6 +469,9 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
         }
     }
+    // the call's error accumulator: reset before any of its views bins (stream order: the
+    // binning chains wait for the preprocess, which follows this reset on its stream)
+    cudaMemsetAsync(c->sticky, 0, sizeof(gs::Sticky), conc ? c->pre_stream : st);
     int last_set = 0;
     for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
         const int n = std::min(G, n_views - v0);
@@ -728,11 +738,14 @@ int gs_last_stats(gs_ctx *c, gs_stats *out) {
     gs::Counters h;
     const gs::Counters *src = c->last_counters ? c->last_counters : c->ws.counters;
     if (check_cuda(cudaMemcpy(&h, src, sizeof(h), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
+    gs::Sticky sk{};
+    if (check_cuda(cudaMemcpy(&sk, c->sticky, sizeof(sk), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
     out->n_points = c->last_n;
     out->n_visible = h.n_visible;
-    out->n_keys = (int64_t)h.n_keys;
+    // K: the last view's, or the largest of the call's views if one of them overflowed
+    out->n_keys = (sk.err & 1u) ? (int64_t)std::max<unsigned long long>(sk.max_keys, h.n_keys) : (int64_t)h.n_keys;
     out->capacity_keys = c->max_keys;
-    out->status = (h.err & 1u) ? GS_ERR_CAPACITY : c->last_status;
+    out->status = ((h.err | sk.err) & 1u) ? GS_ERR_CAPACITY : c->last_status;
     out->launches = c->launches;
     out->pairs_evaluated = (int64_t)h.pairs_eval;
     out->pairs_kept = (int64_t)h.pairs_kept;

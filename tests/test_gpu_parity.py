@@ -558,3 +558,39 @@ def test_host_async_entry_point_matches_device_frames():
     for hr, ht in outs:
         assert torch.equal(hr, ref_r) and torch.equal(ht, ref_t)
     ctx.close()
+
+
+def test_capacity_error_in_any_view_of_an_orbit_is_reported():
+    """A multi-view call fails with GS_ERR_CAPACITY if any view overflows max_keys (the
+    views reuse their counters, so the error is accumulated per call), and reports the
+    largest K; an empty scene renders background through the orbit path."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device
+    scene = synth.unbounded_scene(20000, 112, sh_degree=1)
+    cams = synth.orbit_cameras(6, 160, 96, 1.0)
+    ks = []
+    for c in cams:   # K of each view, one at a time
+        ctx1 = Context(0, max_points=scene.n, max_keys=1 << 22, max_w=160, max_h=96)
+        _, K, _ = gpu_binning(ctx1, scene, c)
+        ks.append(K)
+    cap = sorted(ks)[-2]   # only the largest view overflows
+    assert cap < max(ks)
+    ctx = Context(0, max_points=scene.n, max_keys=cap, max_w=160, max_h=96)
+    ctx.gs_set_view_group(4, True)
+    st = scene_to_device(scene)
+    r = torch.empty((6, 3, 96, 160), device="cuda")
+    t = torch.empty((6, 96, 160), device="cuda")
+    order = sorted(range(6), key=lambda v: ks[v])        # the overflowing view is rendered first
+    cam_list = [camera(cams[v]) for v in reversed(order)]
+    with pytest.raises(GsError) as e:
+        ctx.gs_render_views(st, cam_list, 160, 96, opts(sh_degree=1, flags=1), r, t)
+    assert e.value.code == -3
+    assert ctx.gs_last_stats().n_keys == max(ks)
+    empty = synth.object_scene(0, 0, sh_degree=0)
+    ctx0 = Context(0, max_points=1, max_keys=1024, max_w=40, max_h=24)
+    r0 = torch.empty((3, 3, 24, 40), device="cuda")
+    t0 = torch.empty((3, 24, 40), device="cuda")
+    ctx0.gs_render_views(scene_to_device(empty), [camera(c) for c in synth.orbit_cameras(3, 40, 24, 1.0)], 40, 24,
+                         opts((0.1, 0.2, 0.3), sh_degree=0, flags=1), r0, t0)
+    torch.cuda.synchronize()
+    assert (t0 == 1.0).all() and (r0[:, 2] == np.float32(0.3)).all()
