@@ -57,14 +57,26 @@ class ClockSampler:
         self.path = None
 
     def start(self):
+        """Starts sampling every 100 ms and returns once the first sample is out (nvidia-smi
+        takes a moment to start), so that the timed region that follows is covered."""
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        self.skip = 0
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 10.0:
+            with open(self.path) as f:
+                n = sum(1 for _ in f)
+            if n > 0:
+                self.skip = n   # samples taken before the timed region are not counted
+                return
+            time.sleep(0.05)
 
     def stop(self):
         if self.proc is None:
@@ -76,7 +88,7 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for line in list(open(self.path))[self.skip:]:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -506,7 +518,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--views", type=int, default=64)
