@@ -121,8 +121,11 @@ inline void band_rows(int gy, int band, int n_bands, int &y0, int &y1) {
 
 // Chunk geometry of the single-pass scans / onesweep radix passes.
 constexpr int SORT_THREADS = 256;
-constexpr int SORT_ITEMS = 16;
-constexpr int SORT_CHUNK = SORT_THREADS * SORT_ITEMS;   // 4096 keys per chunk
+#ifndef GS_SORT_ITEMS
+#define GS_SORT_ITEMS 12
+#endif
+constexpr int SORT_ITEMS = GS_SORT_ITEMS;   // elements per thread of a radix / scan chunk
+constexpr int SORT_CHUNK = SORT_THREADS * SORT_ITEMS;   // 3072 keys per chunk (sweep: 12 items/thread beats 8, 10, 14, 16, 32)
 
 __host__ __device__ inline int ceil_div_i(long long a, long long b) { return (int)((a + b - 1) / b); }
 
