@@ -31,6 +31,9 @@
 namespace gs {
 
 constexpr int NWARP = SORT_THREADS / 32;
+#ifndef GS_GRID_MULT
+#define GS_GRID_MULT 8   // radix / scan grids: at most this many blocks per SM (grid-stride over chunks)
+#endif
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
@@ -1301,8 +1304,8 @@ static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys,
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid_n = std::max(1, std::min(nsm * 8, ceil_div_i(N, SORT_CHUNK)));
-    const int grid_k = std::max(1, std::min(nsm * 8, ceil_div_i(max_keys, SORT_CHUNK)));
+    const int grid_n = std::max(1, std::min(nsm * GS_GRID_MULT, ceil_div_i(N, SORT_CHUNK)));
+    const int grid_k = std::max(1, std::min(nsm * GS_GRID_MULT, ceil_div_i(max_keys, SORT_CHUNK)));
     const uint64_t mk = (uint64_t)max_keys;
     const int gy = ntiles / gx;
     if (!(gx <= 512 && gy <= 512)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);

@@ -120,7 +120,10 @@ inline void band_rows(int gy, int band, int n_bands, int &y0, int &y1) {
 }
 
 // Chunk geometry of the single-pass scans / onesweep radix passes.
-constexpr int SORT_THREADS = 256;
+#ifndef GS_SORT_THREADS
+#define GS_SORT_THREADS 256
+#endif
+constexpr int SORT_THREADS = GS_SORT_THREADS;
 #ifndef GS_SORT_ITEMS
 #define GS_SORT_ITEMS 12
 #endif
