@@ -331,7 +331,7 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
                              int sh_stride, float scale_mod, int W, int H, int imode);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
-                   uint32_t &epoch, bool tight, float znear);
+                   uint32_t &epoch, bool tight, float znear, bool concurrent);
 void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,

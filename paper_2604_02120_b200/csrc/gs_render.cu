@@ -178,10 +178,10 @@ int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
 
 // binning of one preprocessed view (its workspace) on st
 void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const gs_camera &cam, int W, int H,
-                     const gs_opts &o) {
+                     const gs_opts &o, bool concurrent = false) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     c->launches += gs::launch_binning(w, st, N, c->max_keys, gx * gy, gx, c->epoch, (o.flags & GS_FLAG_TIGHT) != 0,
-                                      cam.znear);
+                                      cam.znear, concurrent);
 }
 
 // preprocess + binning of one view into the context's workspace (counters zeroed first)
@@ -503,7 +503,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                 cudaStream_t bs = c->bstream[j];
                 cudaStreamWaitEvent(bs, c->ev_pre[set], 0);
                 const int b0 = mark(c, bs, o);
-                enqueue_binning(c, *w[j], bs, N, cams[v0 + j], W, H, o);
+                enqueue_binning(c, *w[j], bs, N, cams[v0 + j], W, H, o, true);
                 span(c, 1, b0, mark(c, bs, o));
                 cudaEventRecord(c->ev_binned[set][j], bs);
             }
