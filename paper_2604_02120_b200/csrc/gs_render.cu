@@ -64,6 +64,10 @@ struct gs_ctx {
 };
 
 static constexpr int kMaxEvents = 4096;
+#ifndef GS_CHAIN_STREAMS
+#define GS_CHAIN_STREAMS 16   // concurrent binning chains of a view group (<= MAX_VIEW_GROUP)
+#endif
+static_assert(GS_CHAIN_STREAMS >= 1 && GS_CHAIN_STREAMS <= gs::MAX_VIEW_GROUP, "chain streams");
 namespace gs {
 int g_pdl = 1;
 }
@@ -500,7 +504,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         if (conc) {
             cudaEventRecord(c->ev_pre[set], ps);
             for (int j = 0; j < n; j++) {
-                cudaStream_t bs = c->bstream[j];
+                cudaStream_t bs = c->bstream[j % GS_CHAIN_STREAMS];   // chains beyond it queue up
                 cudaStreamWaitEvent(bs, c->ev_pre[set], 0);
                 const int b0 = mark(c, bs, o);
                 enqueue_binning(c, *w[j], bs, N, cams[v0 + j], W, H, o, true);
