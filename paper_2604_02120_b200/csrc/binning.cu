@@ -37,6 +37,9 @@ constexpr int NWARP = SORT_THREADS / 32;
 #ifndef GS_GRID_MULT
 #define GS_GRID_MULT 8
 #endif
+#ifndef GS_SCATTER_MINB
+#define GS_SCATTER_MINB 3   // resident blocks per SM of the unpacked radix scatter (register cap)
+#endif
 #ifndef GS_GRID_MULT_CONCURRENT
 #define GS_GRID_MULT_CONCURRENT 4
 #endif
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(SCANROWS_WARPS * 32) k_rs_scanrows(const Count
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
 // earlier chunks) + (rank among this chunk's elements of the digit)
 template <class Loader, int DBITS>
-__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : 3)
+__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : GS_SCATTER_MINB)
     k_rs_scatter(Loader ld, uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, const Counters *cnt,
                  int which, uint64_t max_keys, int shift, const uint32_t *__restrict__ cmat, uint32_t ldm,
                  const uint32_t *__restrict__ row_total) {
