@@ -11,13 +11,14 @@ import torch  # noqa: E402
 from paper_2604_02120_b200 import GS_FLAG_OBOX, GS_FLAG_TIMING, Context, camera, opts, scene_to_device, synth  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--views", type=int, default=12)
+ap.add_argument("--views", type=int, default=32)
 ap.add_argument("--serial", action="store_true")
+ap.add_argument("--group", type=int, default=16)
 a = ap.parse_args()
 scene, cams, bg = synth.make_config("C5", views=64)
 cam = cams[0]
 ctx = Context(0, max_points=scene.n, max_keys=48 << 20, max_w=cam.W, max_h=cam.H)
-ctx.gs_set_view_group(4, not a.serial)
+ctx.gs_set_view_group(a.group, not a.serial)
 st = scene_to_device(scene)
 cs = [camera(c) for c in cams[:a.views]]
 rgb = torch.empty((a.views, 3, cam.H, cam.W), device="cuda")
