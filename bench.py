@@ -111,6 +111,10 @@ def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: GS_BENCH_DEVICE pins every rank to one device (exercising the N > 1 host
+    # path on a 1-GPU box with GS_BENCH_BACKEND=gloo); unset in real runs
+    if os.environ.get("GS_BENCH_DEVICE") is not None:
+        local = int(os.environ["GS_BENCH_DEVICE"])
     return ws, rank, local
 
 
@@ -163,11 +167,15 @@ def run_ours(args):
 
     from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
                                        Context, camera, opts, scene_to_device, scene_to_host, synth)
-    from paper_2604_02120_b200.orbit import gather_frames_pipelined, partition_views
+    from paper_2604_02120_b200.orbit import gather_frames_pipelined, partition_views, share_frames
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GS_BENCH_BACKEND", "nccl")   # gloo: test hook only (see _dist)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     scene, cams, bg = synth.make_config("C5", views=args.views)
     W, H = cams[0].W, cams[0].H
     mine = partition_views(args.views, ws, rank)
@@ -181,8 +189,15 @@ def run_ours(args):
     group = VIEW_GROUP if ws == 1 else max(1, min(VIEW_GROUP, per // 2))
     ctx.gs_set_view_group(group, True)
     st = scene_to_device(scene)
-    out_rgb = torch.empty((per, 3, H, W), device="cuda")
-    out_T = torch.empty((per, H, W), device="cuda")
+    fused = ws > 1 and args.gather == "fused"
+    if fused:   # every rank's blends write straight into rank 0's frame buffers (CUDA IPC / NVLink)
+        own = ((torch.empty((args.views, 3, H, W), device="cuda"), torch.empty((args.views, H, W), device="cuda"))
+               if rank == 0 else (None, None))
+        all_rgb, all_T = share_frames(own[0], own[1], rank, dist)
+        out_rgb, out_T = all_rgb[mine.start:mine.stop], all_T[mine.start:mine.stop]
+    else:
+        out_rgb = torch.empty((per, 3, H, W), device="cuda")
+        out_T = torch.empty((per, H, W), device="cuda")
     # GS_FLAG_STATIC_SCENE (a step's preprocess may overlap the previous step's last blends)
     # measured slower here (1210 vs 1233 fps: the overlap slows the blends); off by default
     static = 32 if os.environ.get("GS_BENCH_STATIC", "0") == "1" else 0
@@ -191,11 +206,13 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     gather_out = None
-    if ws > 1 and rank == 0:   # receive buffers of the frame gather, allocated once (untimed)
+    if ws > 1 and rank == 0 and not fused:   # receive buffers of the frame gather, allocated once (untimed)
         gather_out = (torch.empty((ws, per, 3, H, W), device="cuda"), torch.empty((ws, per, H, W), device="cuda"))
 
     def step(o):
         ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
+        if fused:
+            return   # the frames are already in rank 0's buffers when the blends complete
         # NCCL frame gather to rank 0, view group by view group as the groups finish
         gather_frames_pipelined(out_rgb, out_T, ws, rank, group,
                                 wait_group=lambda s, g: ctx.gs_stream_wait_group(s, g), dist=dist, out=gather_out)
@@ -499,6 +516,9 @@ def run_ours(args):
                 "config": {"workload": WORKLOAD, "views": args.views, "n_gaussians": N, "W": W, "H": H,
                            "sh_degree": scene.sh_degree, "blend": args.blend,
                            "intersection": INTERSECT[args.intersect][1],
+                           "frame_gather": ("none (1 GPU)" if ws == 1 else
+                                            "fused: blends write into rank 0's frames via CUDA IPC / NVLink"
+                                            if args.gather == "fused" else "NCCL gather per view group, overlapped"),
                            "parallelism": f"view-partition x{ws}" + (" + NCCL gather" if ws > 1 else ""),
                            "l2": "inputs larger than L2 (1.42 GB scene, 2.1 GB of frames per step)"},
                 "ms_per_frame": elapsed_ms / args.steps / per, "stage_ms_per_frame": {
@@ -511,7 +531,8 @@ def run_ours(args):
                                    "pairs_kept": n_kept}}
         print(json.dumps(line), flush=True)
     if ws > 1:
-        dist.barrier()
+        torch.cuda.synchronize()
+        dist.barrier()   # (fused gather: rank 0's frame buffers stay mapped until every rank is done)
         dist.destroy_process_group()
 
 
@@ -528,6 +549,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ab", action="store_true")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL gather per view group (default) or blends writing into rank 0's frames "
+                         "through CUDA IPC peer memory")
     ap.add_argument("--intersect", default="obox", choices=list(INTERSECT),
                     help="intersection mode of the headline (the others are timed alongside, N3)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N2 resolution sweep")

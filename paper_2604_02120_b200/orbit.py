@@ -122,3 +122,25 @@ def gather_bands(rgb, T, n_bands: int, rank: int, dist=None):
         out_rgb[:, r.start:r.stop] = lr[b][:, :len(r)]
         out_T[r.start:r.stop] = lt[b][:len(r)]
     return out_rgb, out_T
+
+
+def share_frames(frames_rgb, frames_T, rank: int, dist=None):
+    """Fused frame "gather" (SURVEY 8(e) fused variant): rank 0 owns the orbit's frame
+    buffers [n_views,3,H,W] / [n_views,H,W]; every other rank maps them through CUDA IPC
+    (peer memory over NVLink, peer access enabled lazily by the mapping) and its blend
+    writes its views' pixels straight into rank 0's buffers -- no separate collective
+    and no extra copy. Pass frames_rgb / frames_T on rank 0 (None elsewhere); returns the
+    tensors every rank renders into (on rank r, views of rank 0's memory). The handles are
+    exchanged with broadcast_object_list (gloo or NCCL); the caller keeps rank 0's
+    buffers alive and orders the writes against rank 0's reads with a barrier."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    if dist is None:
+        import torch.distributed as dist
+    payload = [None, None]
+    if rank == 0:
+        payload = [reduce_tensor(frames_rgb)[1], reduce_tensor(frames_T)[1]]
+    dist.broadcast_object_list(payload, src=0)
+    if rank == 0:
+        return frames_rgb, frames_T
+    from torch.multiprocessing.reductions import rebuild_cuda_tensor
+    return rebuild_cuda_tensor(*payload[0]), rebuild_cuda_tensor(*payload[1])
