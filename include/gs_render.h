@@ -157,9 +157,10 @@ int gs_render_views(gs_ctx *ctx, void *stream, int N, const float *means3D, cons
 
 /* End-to-end variant with HOST buffers (pinned memory recommended): copies the
  * scene host->device, renders n_views, copies the frames device->host and
- * synchronises `stream` before returning. Scene staging uses the context's own
- * device buffers (sized by max_points). The frame copies run on a context-owned
- * second stream, one view group behind the rendering (two staging slots). */
+ * synchronises `stream` before returning. The scene is staged in one of two
+ * context-owned device buffers (sized for the scene on first use) by a context
+ * upload stream; every frame is copied back on a context copy stream as soon as
+ * its blend is done (staging slot v % 2G, G the view group size). */
 int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
                          const float *scales, const float *rots, const float *opacity,
                          const float *shs_or_colors, const gs_camera *cams, int n_views,
