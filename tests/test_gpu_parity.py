@@ -633,3 +633,25 @@ def test_random_scenes_and_cameras_bit_exact(seed):
     _, _, ref = oracle.render(scene, cam, bg)
     m = compare(rgb, T, ref)
     assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+
+
+def test_wide_depth_range_takes_the_fourth_pass():
+    """Depths beyond znear * 2^16 (13107 at znear 0.2) make the near-plane-relative
+    depth keys wider than 27 bits: the 4th radix pass and the copy back must run and the
+    keys / values / ranges stay bit-exact against the oracle (huge splats far away)."""
+    rng = np.random.default_rng(114)
+    scene = synth.object_scene(3000, 114, sh_degree=1)
+    far = rng.uniform(0.0, 1.0, scene.n) < 0.5
+    scene.means[far] *= np.float32(4000.0)            # far away: depths up to ~1e4 .. 4e4
+    scene.means[far, 2] += np.float32(30000.0)
+    scene.scales[far] *= np.float32(3000.0)            # still a few pixels wide on screen
+    cam = synth.look_at((0.0, 0.0, -4.0), (0, 0, 0), 128, 96, 0.9)
+    ctx = make_ctx(scene, cam)
+    pre = oracle.preprocess(scene, cam)
+    assert (pre["depth"][pre["touched"] > 0] > 0.2 * 65536).any()   # the wide case is exercised
+    code, K, gb = gpu_binning(ctx, scene, cam)
+    assert code == 0
+    ref = oracle.binning(pre, cam.W, cam.H)
+    assert K == ref["K"]
+    assert np.array_equal(gb["keys"], ref["keys"]) and np.array_equal(gb["vals"], ref["vals"])
+    assert np.array_equal(gb["ranges"], ref["ranges"])
