@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_p
 // define their own chunks (ColLoader).
 struct LinearChunks {
     __device__ void epilogue(uint32_t, uint32_t) const {}   // per scattered element (g = slot, v = value)
+    bool keys_if_wide = false;   // the last depth pass: its keys are only read by the 4th (wide) pass
     static constexpr bool PACKED = false;       // key = digit | value << PACK_SHIFT, no separate values
     static constexpr int PACK_SHIFT = 0;
     static constexpr bool EXPANDS = false;      // keys via key(i) from global memory
@@ -593,6 +594,7 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : GS_SCATTER_
     const uint32_t nchunks = ld.nchunks(n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int d0 = threadIdx.x * DPT;
+    if (kout && ld.keys_if_wide && !cnt->wide_depth) kout = nullptr;   // nobody reads these keys
     // exclusive scan over all NDIG digits; v[i] belongs to digit d0 + i
     auto block_excl_scan = [&](const uint32_t (&v)[DPT], uint32_t (&out)[DPT]) {
         uint32_t t = 0;
@@ -972,6 +974,7 @@ struct ColLoader {
     int gx;
     static constexpr bool EXPANDS = true;
     static constexpr int SCRATCH_WORDS = 0;
+    bool keys_if_wide = false;
     __device__ void epilogue(uint32_t, uint32_t) const {}
     __device__ uint32_t nchunks(uint32_t) const { return cnt->err ? 0u : cnt->n_cchunks; }
     __device__ void chunk(uint32_t c, uint32_t, uint32_t &cbase, uint32_t &cvalid) const {
@@ -1337,6 +1340,7 @@ static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys,
             ld.g_rect_out = ws.rect_r;
             ld.g_tmask = tm;
             ld.g_tmask_out = tm ? ws.tmask_r : nullptr;
+            ld.keys_if_wide = true;
         }
         launches += radix_pass(ws, st, grid_n, ld, ws.sk[p & 1], ws.sv[p & 1], CNT_VISIBLE, mk, 9 * p, 9);
     }
