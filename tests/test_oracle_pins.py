@@ -506,3 +506,57 @@ def test_obox_lists_are_an_alpha_exact_ordered_subset(name):
             a = float(pre["opacity"][i]) * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
             assert a.max() < (1.0 / 255.0) * math.exp(-0.004), (t, i, a.max())
     assert n_dropped > 0
+
+
+# ---- the decision-margin mask (R-21): pins against constructed decisions -------
+def _one_tile(xy, conic, opac, rgb):
+    """Splats + a one-tile (16x16) binning listing every splat in order."""
+    n = len(opac)
+    pre = dict(xy=np.asarray(xy, np.float32).reshape(n, 2), conic=np.asarray(conic, np.float32).reshape(n, 3),
+               opacity=np.asarray(opac, np.float32), rgb=np.asarray(rgb, np.float32).reshape(n, 3),
+               touched=np.ones(n, np.uint32))
+    b = dict(vals=np.arange(n, dtype=np.uint32), ranges=np.array([[0, n]], np.uint32), K=n)
+    return pre, b
+
+
+def test_margin_mask_flags_an_alpha_skip_on_the_threshold_and_bounds_its_flip():
+    """A splat placed so that pixel (0,0) sits within 1e-5 of ln(1/255) in ln alpha: that
+    pixel is flagged (and no decision 0.5 px away is), and the frame change caused by
+    flipping the decision (opacity scaled by exp(+-3e-4), larger than the documented GPU
+    error) stays within the reported flip bound."""
+    s2, o = 16.0, 0.5                                   # isotropic, sigma^2 = 16
+    ln_amin = math.log(float(np.float32(1.0 / 255.0)))
+    d2 = 2 * s2 * (math.log(o) - ln_amin - 1e-5)        # ln alpha(0,0) = ln_amin + 1e-5
+    mx = math.sqrt(d2)
+    pre, b = _one_tile([[mx, 0.0]], [[1 / s2, 0.0, 1 / s2]], [o], [[1.0, 1.0, 1.0]])
+    out = oracle.blend(pre, b, 16, 16)
+    assert out["flag"][0, 0]
+    assert out["flag"].sum() <= 2                       # only pixels on the threshold circle
+    for f in (math.exp(-3e-4), math.exp(3e-4)):        # both sides of the decision
+        pre2 = dict(pre, opacity=(pre["opacity"] * np.float32(f)).astype(np.float32))
+        o2 = oracle.blend(pre2, b, 16, 16)
+        assert abs(o2["rgb"][0, 0, 0] - out["rgb"][0, 0, 0]) <= out["bound"][0, 0] + 1e-12
+
+
+def test_margin_mask_is_empty_when_no_decision_is_near_a_threshold():
+    """A wide, half-transparent splat (alpha in [0.2, 0.5] on the whole tile, T far above
+    1e-4): no pixel is flagged and the flip bounds are zero."""
+    pre, b = _one_tile([[7.5, 7.5]], [[1e-3, 0.0, 1e-3]], [0.5], [[0.3, 0.6, 0.9]])
+    out = oracle.blend(pre, b, 16, 16)
+    assert not out["flag"].any() and (out["bound"] == 0).all()
+    assert (out["T"] > 0.4).all()
+
+
+def test_margin_mask_flags_a_termination_on_the_threshold():
+    """Identical flat splats with alpha a stacked so that T after k steps is within a hair
+    of 1e-4 at every pixel: the stop decision is ambiguous there, so every pixel is
+    flagged; with the stack one step shorter (T far above 1e-4 at the end) nothing is."""
+    k = 4
+    a = 1.0 - (1e-4 * (1 + 1e-7)) ** (1.0 / k)          # T_k = 1e-4 (1 + 1e-7)
+    n = k + 2
+    conic = [[1e-9, 0.0, 1e-9]] * n                     # flat: alpha ~ opacity on the tile
+    pre, b = _one_tile([[7.5, 7.5]] * n, conic, [a] * n, [[0.5, 0.5, 0.5]] * n)
+    out = oracle.blend(pre, b, 16, 16)
+    assert out["flag"].all()
+    pre3, b3 = _one_tile([[7.5, 7.5]] * 2, conic[:2], [a] * 2, [[0.5, 0.5, 0.5]] * 2)
+    assert not oracle.blend(pre3, b3, 16, 16)["flag"].any()
