@@ -40,6 +40,12 @@ constexpr int NWARP = SORT_THREADS / 32;
 #ifndef GS_SCATTER_MINB
 #define GS_SCATTER_MINB 3   // resident blocks per SM of the unpacked radix scatter (register cap)
 #endif
+#ifndef GS_SCATTER_MINB_PK
+#define GS_SCATTER_MINB_PK 5   // the packed (column) scatter
+#endif
+#ifndef GS_COUNT_NH
+#define GS_COUNT_NH 4          // privatised shared histograms of the count kernel
+#endif
 #ifndef GS_GRID_MULT_CONCURRENT
 #define GS_GRID_MULT_CONCURRENT 4
 #endif
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
     static_assert(NDIG == 256 || NDIG == 512, "8- or 9-bit digits");
     constexpr int DPT = NDIG / SORT_THREADS;   // digits per thread
     extern __shared__ uint32_t dyn[];          // expanding loaders: the chunk's keys + loader scratch
-    constexpr int NH = 4;                      // privatised histograms (warp % NH)
+    constexpr int NH = GS_COUNT_NH;            // privatised histograms (warp % NH)
     __shared__ uint32_t s_h[NH][NDIG];
     __shared__ uint32_t s_w[NWARP];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
@@ -573,7 +579,7 @@ __global__ void __launch_bounds__(SCANROWS_WARPS * 32) k_rs_scanrows(const Count
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
 // earlier chunks) + (rank among this chunk's elements of the digit)
 template <class Loader, int DBITS>
-__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? 5 : GS_SCATTER_MINB)
+__global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? GS_SCATTER_MINB_PK : GS_SCATTER_MINB)
     k_rs_scatter(Loader ld, uint32_t *__restrict__ kout, uint32_t *__restrict__ vout, const Counters *cnt,
                  int which, uint64_t max_keys, int shift, const uint32_t *__restrict__ cmat, uint32_t ldm,
                  const uint32_t *__restrict__ row_total) {
