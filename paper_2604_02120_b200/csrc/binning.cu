@@ -43,6 +43,10 @@ constexpr int NWARP = SORT_THREADS / 32;
 #ifndef GS_SCATTER_MINB_PK
 #define GS_SCATTER_MINB_PK 5   // the packed (column) scatter
 #endif
+#ifndef GS_COUNT_ILP
+#define GS_COUNT_ILP 4   // Gaussians / row entries per thread per round in the run-count loops
+#endif
+constexpr int COUNT_ILP = GS_COUNT_ILP;
 #ifndef GS_COUNT_NH
 #define GS_COUNT_NH 4          // privatised shared histograms of the count kernel
 #endif
@@ -924,21 +928,35 @@ __device__ __forceinline__ void row_count_runs(const RowLoader &ld, uint32_t c, 
     const uint32_t r_lo = ld.chunk_first[c];
     const uint32_t r_hi = c + 1 < nchunks ? min(nv - 1, ld.chunk_first[c + 1]) : nv - 1;
     const uint32_t cend = cbase + cvalid;
-    for (uint32_t r = r_lo + threadIdx.x; r <= r_hi; r += SORT_THREADS) {
-        const uint32_t o = ld.roff[r], o1 = r + 1 < nv ? ld.roff[r + 1] : n_rent;
-        const uint32_t q0 = o < cbase ? cbase - o : 0u;
-        const uint32_t len = min(o1, cend) - (o + q0);
-        if (len == 0) continue;
-        const uint32_t y0 = ld.rect_r[r].y;
-        const uint32_t rows = ld.tight ? ld.rowmask_r[r] : 0xFFFFFFFFu;
-        if (rows == 0xFFFFFFFFu) {
-            atomicAdd(&s_diff[y0 + q0], 1);
-            atomicAdd(&s_diff[y0 + q0 + len], -1);
-        } else {
-            for (uint32_t q = q0; q < q0 + len; q++) {
-                const uint32_t ty = y0 + (uint32_t)__fns(rows, 0, (int)q + 1);
-                atomicAdd(&s_diff[ty], 1);
-                atomicAdd(&s_diff[ty + 1], -1);
+    // COUNT_ILP Gaussians per thread per round: their loads are issued together
+    for (uint32_t r0 = r_lo + threadIdx.x; r0 <= r_hi; r0 += COUNT_ILP * SORT_THREADS) {
+        uint32_t o[COUNT_ILP], o1[COUNT_ILP], y0[COUNT_ILP], rows[COUNT_ILP];
+#pragma unroll
+        for (int u = 0; u < COUNT_ILP; u++) {
+            const uint32_t r = r0 + (uint32_t)u * SORT_THREADS;
+            o[u] = o1[u] = y0[u] = 0;
+            rows[u] = 0xFFFFFFFFu;
+            if (r <= r_hi) {
+                o[u] = ld.roff[r];
+                o1[u] = r + 1 < nv ? ld.roff[r + 1] : n_rent;
+                y0[u] = ld.rect_r[r].y;
+                if (ld.tight) rows[u] = ld.rowmask_r[r];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < COUNT_ILP; u++) {
+            const uint32_t q0 = o[u] < cbase ? cbase - o[u] : 0u;
+            const uint32_t len = min(o1[u], cend) - (o[u] + q0);
+            if (o1[u] <= o[u] + q0 || len == 0) continue;
+            if (rows[u] == 0xFFFFFFFFu) {
+                atomicAdd(&s_diff[y0[u] + q0], 1);
+                atomicAdd(&s_diff[y0[u] + q0 + len], -1);
+            } else {
+                for (uint32_t q = q0; q < q0 + len; q++) {
+                    const uint32_t ty = y0[u] + (uint32_t)__fns(rows[u], 0, (int)q + 1);
+                    atomicAdd(&s_diff[ty], 1);
+                    atomicAdd(&s_diff[ty + 1], -1);
+                }
             }
         }
     }
@@ -994,13 +1012,27 @@ struct ColLoader {
     static constexpr bool RUN_COUNTS = true;
     __device__ void count_runs(uint32_t c, uint32_t cbase, uint32_t cvalid, int *s_diff) const {
         const uint32_t e_lo = cdesc[c].w, e_hi = cdesc_last[c], cend = cbase + cvalid;
-        for (uint32_t e = e_lo + threadIdx.x; e <= e_hi; e += SORT_THREADS) {
-            const uint32_t o = poff[e], k = e_key[e];
-            const uint32_t q0 = o < cbase ? cbase - o : 0u;
-            const uint32_t len = min(o + (k >> 18), cend) - (o + q0);
-            const uint32_t x = ((k >> 9) & 0x1FFu) + q0;
-            atomicAdd(&s_diff[x], 1);
-            atomicAdd(&s_diff[x + len], -1);
+        for (uint32_t e0 = e_lo + threadIdx.x; e0 <= e_hi; e0 += COUNT_ILP * SORT_THREADS) {
+            uint32_t o[COUNT_ILP], k[COUNT_ILP];
+#pragma unroll
+            for (int u = 0; u < COUNT_ILP; u++) {
+                const uint32_t e = e0 + (uint32_t)u * SORT_THREADS;
+                o[u] = cend;   // (no run)
+                k[u] = 0;
+                if (e <= e_hi) {
+                    o[u] = poff[e];
+                    k[u] = e_key[e];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < COUNT_ILP; u++) {
+                if (e0 + (uint32_t)u * SORT_THREADS > e_hi) continue;
+                const uint32_t q0 = o[u] < cbase ? cbase - o[u] : 0u;
+                const uint32_t len = min(o[u] + (k[u] >> 18), cend) - (o[u] + q0);
+                const uint32_t x = ((k[u] >> 9) & 0x1FFu) + q0;
+                atomicAdd(&s_diff[x], 1);
+                atomicAdd(&s_diff[x + len], -1);
+            }
         }
     }
     __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
