@@ -187,9 +187,10 @@ def vp(xb, yb):
     return v
 
 
-def render(scene, cam, bg=(0.0, 0.0, 0.0), threads=None, mask=True, delta_a=DELTA_A, obox=False):
+def render(scene, cam, bg=(0.0, 0.0, 0.0), threads=None, mask=True, delta_a=DELTA_A, obox=False,
+           scale_modifier=1.0):
     """Whole path: preprocess -> binning -> blend."""
-    pre = preprocess(scene, cam, obox=obox)
+    pre = preprocess(scene, cam, scale_modifier=scale_modifier, obox=obox)
     b = binning(pre, cam.W, cam.H)
     out = blend(pre, b, cam.W, cam.H, bg, threads=threads, mask=mask, delta_a=delta_a)
     return pre, b, out

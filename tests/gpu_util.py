@@ -13,7 +13,14 @@ def make_ctx(scene, cam, max_keys=None):
     return Context(0, max_points=max(scene.n, 1), max_keys=max_keys or (1 << 24), max_w=cam.W, max_h=cam.H)
 
 
-def gpu_preprocess(ctx, scene, cam, st=None, flags=0):
+def _sh_opts(scene, **kw):
+    """opts() for a scene whose SH record may be longer than its degree needs (stride =
+    record length) or hold plain colours (degree -1, shs [N,3])."""
+    stride = scene.shs.shape[1] if scene.shs.ndim == 3 else 1
+    return opts(sh_degree=scene.sh_degree, sh_stride=stride, **kw)
+
+
+def gpu_preprocess(ctx, scene, cam, st=None, flags=0, scale_modifier=1.0):
     import torch
     st = st or scene_to_device(scene)
     n = scene.n
@@ -23,14 +30,15 @@ def gpu_preprocess(ctx, scene, cam, st=None, flags=0):
                 rect=torch.empty((n, 4), dtype=torch.int32, device=dev),
                 radius=torch.empty(n, dtype=torch.int32, device=dev),
                 touched=torch.empty(n, dtype=torch.int32, device=dev))
-    ctx.gs_debug_preprocess(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree, flags=flags), outs)
+    ctx.gs_debug_preprocess(st, camera(cam), cam.W, cam.H,
+                            _sh_opts(scene, flags=flags, scale_modifier=scale_modifier), outs)
     torch.cuda.synchronize()
     out = {k: v.cpu().numpy() for k, v in outs.items()}
     out["touched"] = out["touched"].view(np.uint32)
     return out
 
 
-def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0):
+def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0, scale_modifier=1.0):
     import torch
     st = st or scene_to_device(scene)
     cap = capacity or (1 << 22)
@@ -38,21 +46,21 @@ def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0):
     vals = torch.empty(cap, dtype=torch.int32, device="cuda")
     ntiles = ((cam.W + 15) // 16) * ((cam.H + 15) // 16)
     ranges = torch.empty((ntiles, 2), dtype=torch.int32, device="cuda")
-    code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H, opts(sh_degree=scene.sh_degree, flags=flags), keys,
-                                   vals, ranges)
+    code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H,
+                                   _sh_opts(scene, flags=flags, scale_modifier=scale_modifier), keys, vals, ranges)
     if code != 0:
         return code, K, None
     return code, K, dict(keys=keys[:K].cpu().numpy().view(np.uint64), vals=vals[:K].cpu().numpy().view(np.uint32),
                          ranges=ranges.cpu().numpy().view(np.uint32))
 
 
-def gpu_render(ctx, scene, cam, bg, blend=0, st=None, flags=0):
+def gpu_render(ctx, scene, cam, bg, blend=0, st=None, flags=0, scale_modifier=1.0):
     import torch
     st = st or scene_to_device(scene)
     out_rgb = torch.full((3, cam.H, cam.W), float("nan"), device="cuda")
     out_T = torch.full((cam.H, cam.W), float("nan"), device="cuda")
     ctx.gs_render(st, camera(cam), cam.W, cam.H,
-                  opts(bg, sh_degree=scene.sh_degree, blend=blend, flags=1 | flags), out_rgb, out_T)
+                  _sh_opts(scene, bg=bg, blend=blend, flags=1 | flags, scale_modifier=scale_modifier), out_rgb, out_T)
     torch.cuda.synchronize()
     return out_rgb.cpu().numpy().astype(np.float64), out_T.cpu().numpy().astype(np.float64)
 

@@ -655,3 +655,47 @@ def test_wide_depth_range_takes_the_fourth_pass():
     assert K == ref["K"]
     assert np.array_equal(gb["keys"], ref["keys"]) and np.array_equal(gb["vals"], ref["vals"])
     assert np.array_equal(gb["ranges"], ref["ranges"])
+
+
+@pytest.mark.parametrize("variant", ["scale_0.6", "scale_1.7", "stride16_deg1", "stride9_deg0", "plain_rgb"])
+def test_scale_modifier_sh_stride_and_plain_colours(variant):
+    """gs_opts.scale_modifier (step 4: g_k = sm * s_k), an SH record longer than the
+    evaluated degree (sh_stride > (D+1)^2: degree 1 or 0 of a degree-3 / degree-2
+    record) and plain colours (sh_degree -1, shs [N,3]): preprocess outputs and
+    keys / values / ranges bit-exact, frame within the bar, both intersection modes."""
+    from paper_2604_02120_b200 import GS_FLAG_OBOX
+    scene = synth.object_scene(4000, 301, sh_degree=3)
+    cam = synth.look_at((0.4, -0.6, -3.3), (0, 0, 0), 133, 71, 0.9)
+    bg = np.array([0.3, 0.1, 0.6], np.float32)
+    sm = 1.0
+    if variant.startswith("scale_"):
+        sm = float(variant.split("_")[1])
+    elif variant == "stride16_deg1":
+        scene.sh_degree = 1
+    elif variant == "stride9_deg0":
+        scene = synth.object_scene(4000, 302, sh_degree=2)
+        scene.sh_degree = 0
+    else:
+        scene.shs = np.ascontiguousarray(np.clip(scene.shs[:, 0, :] * 0.28 + 0.5, 0.0, 1.0), np.float32)
+        scene.sh_degree = -1
+    for obox in (False, True):
+        flags = GS_FLAG_OBOX if obox else 0
+        ctx = make_ctx(scene, cam)
+        got = gpu_preprocess(ctx, scene, cam, flags=flags, scale_modifier=sm)
+        pre = oracle.preprocess(scene, cam, scale_modifier=sm, obox=obox)
+        assert pre["n_visible"] > 1000
+        vis = pre["touched"] > 0
+        assert np.array_equal(got["touched"], pre["touched"])
+        for k in BIT_EXACT_KEYS:
+            a = got[k].view(np.uint32) if got[k].dtype == np.float32 else got[k].astype(np.int64)
+            b = pre[k].view(np.uint32) if pre[k].dtype == np.float32 else pre[k].astype(np.int64)
+            assert np.array_equal(a[vis], b[vis]), k
+        code, K, gb = gpu_binning(ctx, scene, cam, flags=flags, scale_modifier=sm)
+        assert code == 0
+        ref_b = oracle.binning(pre, cam.W, cam.H)
+        assert K == ref_b["K"] and np.array_equal(gb["keys"], ref_b["keys"])
+        assert np.array_equal(gb["vals"], ref_b["vals"]) and np.array_equal(gb["ranges"], ref_b["ranges"])
+        rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=flags, scale_modifier=sm)
+        _, _, ref = oracle.render(scene, cam, bg, obox=obox, scale_modifier=sm)
+        m = compare(rgb, T, ref)
+        assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
