@@ -43,6 +43,14 @@ constexpr int NWARP = SORT_THREADS / 32;
 #ifndef GS_SCATTER_MINB_PK
 #define GS_SCATTER_MINB_PK 5   // the packed (column) scatter
 #endif
+#ifndef GS_SCAN_MINB
+#define GS_SCAN_MINB 6   // minimum resident blocks of the scan kernels (0: not specified; 6: 40 registers, +0.8 % orbit fps)
+#endif
+#if GS_SCAN_MINB > 0
+#define GS_SCAN_BOUNDS __launch_bounds__(SORT_THREADS, GS_SCAN_MINB)
+#else
+#define GS_SCAN_BOUNDS __launch_bounds__(SORT_THREADS)
+#endif
 #ifndef GS_COUNT_ILP
 #define GS_COUNT_ILP 4   // Gaussians / row entries per thread per round in the run-count loops
 #endif
@@ -156,7 +164,7 @@ struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ chunk he
 };
 
 template <class Op>
-__global__ void __launch_bounds__(SORT_THREADS) k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums) {
+__global__ void GS_SCAN_BOUNDS k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums) {
     pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, ui
 // single-block scan of the sums, one launch and one dependency fewer); the block of
 // the last chunk also reports the total (op.finish).
 template <class Op>
-__global__ void __launch_bounds__(SORT_THREADS) k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
+__global__ void GS_SCAN_BOUNDS k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
     pdl_wait();
     __shared__ uint32_t s_w[NWARP];
     __shared__ unsigned long long s_pre[NWARP], s_tot[NWARP], s_base;
