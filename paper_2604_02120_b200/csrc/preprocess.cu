@@ -19,7 +19,10 @@ __device__ __forceinline__ int rect_bound(float v, int g) {
     return (int)c;
 }
 
-constexpr int PRE_THREADS = 256;
+#ifndef GS_PRE_THREADS
+#define GS_PRE_THREADS 256
+#endif
+constexpr int PRE_THREADS = GS_PRE_THREADS;
 
 // Tile-exact intersection (GS_FLAG_TIGHT). A pixel p can keep the Gaussian only if
 // ln(o) - q/2 >= ln(1/255) - margin (Eq. 3 power, q = d^T Q d, d = p - mu up to sign),
