@@ -190,42 +190,6 @@ __global__ void GS_SCAN_BOUNDS k_scan_reduce(Op op, uint32_t n_points, uint32_t 
     }
 }
 
-// one block: exclusive scan of the chunk sums in place; op.finish(total)
-template <class Op>
-__global__ void __launch_bounds__(1024) k_scan_sums(Op op, uint32_t n_points, uint32_t *sums) {
-    pdl_wait();
-    __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_carry;
-    const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
-    const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (uint32_t base = 0; base < nchunks; base += 1024) {
-        const uint32_t c = base + threadIdx.x;
-        const unsigned long long v = c < nchunks ? sums[c] : 0;
-        unsigned long long x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_w[warp] = x;
-        __syncthreads();
-        unsigned long long wb = 0, tot = 0;
-        for (int w = 0; w < 32; w++) {
-            if (w < warp) wb += s_w[w];
-            tot += s_w[w];
-        }
-        const unsigned long long ex = s_carry + wb + x - v;
-        if (c < nchunks) sums[c] = (uint32_t)(ex < 0xFFFFFFFFull ? ex : 0xFFFFFFFFull);
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) op.finish(s_carry);
-}
-
 // Each block computes its chunk's exclusive prefix itself, as the 64-bit sum of the
 // chunk sums before it (at most a few thousand L2-resident words: no separate
 // single-block scan of the sums, one launch and one dependency fewer); the block of
