@@ -699,3 +699,50 @@ def test_scale_modifier_sh_stride_and_plain_colours(variant):
         _, _, ref = oracle.render(scene, cam, bg, obox=obox, scale_modifier=sm)
         m = compare(rgb, T, ref)
         assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+
+
+@pytest.mark.parametrize("obox", [False, True], ids=["vanilla", "obox"])
+def test_capacity_boundary_is_exact(obox):
+    """max_keys == K renders (keys / values / ranges bit-exact, frame within the bar);
+    max_keys == K - 1 is a capacity error that reports the exact K, for gs_render and
+    for a view group (gs_render_views)."""
+    import torch
+    from paper_2604_02120_b200 import GS_FLAG_OBOX, camera, opts, scene_to_device
+    scene, cams, bg = synth.make_config("C2", n_override=60000, views=3)
+    cam = cams[0]
+    flags = GS_FLAG_OBOX if obox else 0
+    pre = oracle.preprocess(scene, cam, obox=obox)
+    K = oracle.binning(pre, cam.W, cam.H)["K"]
+    st = scene_to_device(scene)
+    ctx = make_ctx(scene, cam, max_keys=K)
+    code, Kg, gb = gpu_binning(ctx, scene, cam, capacity=K, st=st, flags=flags)
+    assert code == 0 and Kg == K
+    ref_b = oracle.binning(pre, cam.W, cam.H)
+    assert np.array_equal(gb["keys"], ref_b["keys"]) and np.array_equal(gb["vals"], ref_b["vals"])
+    rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=flags)
+    _, _, ref = oracle.render(scene, cam, bg, obox=obox)
+    m = compare(rgb, T, ref)
+    assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+    ctx.close()
+    ctx = make_ctx(scene, cam, max_keys=K - 1)
+    with pytest.raises(GsError) as e:
+        gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=flags)
+    assert e.value.code == -3 and ctx.gs_last_stats().n_keys == K
+    # the same view inside a group of 3: only its K exceeds the capacity when it is the largest
+    Ks = [oracle.binning(oracle.preprocess(scene, c, obox=obox), c.W, c.H)["K"] for c in cams]
+    ctx.close()
+    ctx = make_ctx(scene, cam, max_keys=max(Ks))
+    ctx.gs_set_view_group(3, True)
+    grgb = torch.empty((3, 3, cam.H, cam.W), device="cuda")
+    gT = torch.empty((3, cam.H, cam.W), device="cuda")
+    o = opts(bg, sh_degree=scene.sh_degree, flags=1 | flags)
+    ctx.gs_render_views(st, [camera(c) for c in cams], cam.W, cam.H, o, grgb, gT)
+    torch.cuda.synchronize()
+    ctx.close()
+    ctx = make_ctx(scene, cam, max_keys=max(Ks) - 1)
+    ctx.gs_set_view_group(3, True)
+    with pytest.raises(GsError) as e:
+        ctx.gs_render_views(st, [camera(c) for c in cams], cam.W, cam.H, o, grgb, gT)
+        torch.cuda.synchronize()
+    assert e.value.code == -3 and ctx.gs_last_stats().n_keys == max(Ks)
+    ctx.close()
