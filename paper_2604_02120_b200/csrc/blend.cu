@@ -52,6 +52,9 @@ namespace gs {
 #ifndef GS_BLEND_CH
 #define GS_BLEND_CH 16
 #endif
+#ifndef GS_BLEND_NAMED_WAIT
+#define GS_BLEND_NAMED_WAIT 1   // 1: compositor warps 1-7 wait in a named barrier behind warp 0's mbarrier poll (0: every warp polls)
+#endif
 #ifndef GS_BLEND_NB
 #define GS_BLEND_NB 32
 #endif
@@ -411,8 +414,18 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         for (uint32_t k = 0;; k++) {
             const int s = k % STAGES;
             const int c_slot = k % RING;
+#if GS_BLEND_NAMED_WAIT
+            // one warp polls the barriers, the other compositor warps sleep in a named
+            // barrier (no issue slots spent spinning); tc_fence_after orders their TMEM loads
+            if (warp == 0) {
+                mbar_wait(&sm.slot_ready[c_slot], (k / RING) & 1u);
+                mbar_wait(&sm.full[s], (k / STAGES) & 1u);
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+#else
             mbar_wait(&sm.slot_ready[c_slot], (k / RING) & 1u);
             mbar_wait(&sm.full[s], (k / STAGES) & 1u);
+#endif
             if (warp == 0) TRACE_EV(7, k);
             if (warp == 7) TRACE_EV(9, k);
             tc_fence_after();

@@ -29,7 +29,8 @@ for r in rows[2:]:
     wr *= scale.get(units[col["dram__bytes_write.sum"]], 1)
     res[name] = {
         "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-        "duration_us": num(r, "gpu__time_duration.sum"),
+        "duration_us": num(r, "gpu__time_duration.sum") * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(
+            units[col["gpu__time_duration.sum"]], 1.0),
         "tensor_pipe_pct": num(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
         "issue_active_pct": num(r, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "fma_pipe_pct": num(r, "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
