@@ -20,6 +20,8 @@
 //     alpha = min(0.99, 2^m), alpha-skip below 1/255, T' = T(1-alpha), stop when
 //     T' < 1e-4 (not composited), C += alpha T c (Eq. 1; readings R-1..R-4).
 //     A warp skips a Gaussian with one vote when none of its 32 pixels keeps it.
+//     Per batch, warp 0 polls the batch's mbarriers and warps 1-7 wait for it in a
+//     named barrier, so the waiting costs no issue slots (GS_BLEND_NAMED_WAIT).
 //   The compositor loop is a serial dependency chain per pixel, so the kernel is
 //   latency-bound: occupancy (CTAs per SM) is what sets its speed, and the pipe-
 //   line shape (one helper warp each for gathers and rows+MMA, 2 TMEM stages,
