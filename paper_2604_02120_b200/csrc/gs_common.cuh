@@ -100,7 +100,10 @@ struct PreOut {
     int32_t *radius;           // nullptr: not written (debug output only)
     Counters *counters;        // zeroed by the preprocess
 };
-constexpr int MAX_VIEW_GROUP = 16;  // views per preprocess launch (gs_set_view_group; default 4)
+#ifndef GS_MAX_VIEW_GROUP
+#define GS_MAX_VIEW_GROUP 16
+#endif
+constexpr int MAX_VIEW_GROUP = GS_MAX_VIEW_GROUP;  // views per preprocess launch (gs_set_view_group; default 4)
 struct PreViews {
     gs_camera cam[MAX_VIEW_GROUP];
     PreOut out[MAX_VIEW_GROUP];
