@@ -20,7 +20,8 @@
  *                      readings R-1..R-5, in float64.  GEMM-GS reaches this
  *                      result exactly in real arithmetic (Eq. 6 is an identity,
  *                      P:269-301), so the oracle is the plain definition.
- *                      It also emits the decision-margin mask (R-21).
+ *                      It also emits the decision-margin mask (R-21), a test
+ *                      device: which decisions lie within the documented GPU error.
  *   orc_vg / orc_vp -- Eq. (6) coefficient and monomial vectors,
  *                      float64, used only by the algebra pins.
  *
@@ -340,8 +341,9 @@ typedef struct {
     const uint32_t *vals, *ranges;
     int W, H, gx, gy;
     double bg[3];
-    double delta_a;      /* documented GPU bound on |d ln alpha| (R-21)       */
-    double impact_tau;   /* a flip whose impact bound is below this is benign */
+    double delta0;       /* documented GPU bound on |d ln alpha| (R-21):       */
+    double eps_rel;      /*   delta = delta0 + eps_rel * S per pair, S below    */
+    double budget;       /* flag a pixel when its summed flip impacts exceed it */
     double cmax;         /* max |colour| over the scene, and bg               */
     /* outputs */
     double *out_rgb, *out_T, *flip_bound;
@@ -357,14 +359,16 @@ static void blend_tile(blend_job *J, int t) {
     const double ln_amin = log(a_min);
     const double t_min = 1e-4, ln_tmin = log(1e-4);
     const int tx = t % J->gx, ty = t / J->gx;
+    /* tile reference pixel of the GEMM form (Eq. 4; reading R-6), for the mask only */
+    const double xc = TILE * tx + 7.5, yc = TILE * ty + 7.5;
     const uint32_t start = J->ranges[2 * t], end = J->ranges[2 * t + 1];
     for (int py = ty * TILE; py < ty * TILE + TILE; py++) {
         for (int px = tx * TILE; px < tx * TILE + TILE; px++) {
             if (px >= J->W || py >= J->H) continue;     /* R-19: in-frame pixels only */
             double T = 1.0, C[3] = {0.0, 0.0, 0.0};
-            double S = 0.0;          /* sum of alpha/(1-alpha) over composited steps */
+            double Serr = 0.0;       /* sum of delta alpha/(1-alpha) over composited steps */
             double bound = 0.0;
-            int flagged = 0;
+            const double xb = xc - (double)px, yb = yc - (double)py;
             for (uint32_t e = start; e < end; e++) {
                 const uint32_t i = J->vals[e];
                 /* Eq. (2)-(3): x_g = [x_g - x_p, y_g - y_p], power = -1/2 x^T Sigma^-1 x */
@@ -376,28 +380,32 @@ static void blend_tile(blend_job *J, int t) {
                 const double a_raw = o * exp(power);
                 const double alpha = a_raw < 0.99 ? a_raw : 0.99;           /* R-4 */
                 J->evaluated++;
+                /* decision margin (R-21): the GPU sums the Eq. (6) terms v_k p_k about the tile
+                 * centre in fp32 / TF32 hi-lo, so its |d ln alpha| scales with their magnitude S */
+                const double xh = (double)J->xy[2 * i] - xc, yh = (double)J->xy[2 * i + 1] - yc;
+                const double Smag = 0.5 * fabs(A) * xb * xb + 0.5 * fabs(Cc) * yb * yb + fabs(B * xb * yb) +
+                                    fabs(A * xh + B * yh) * fabs(xb) + fabs(Cc * yh + B * xh) * fabs(yb) +
+                                    0.5 * fabs(A) * xh * xh + 0.5 * fabs(Cc) * yh * yh + fabs(B * xh * yh) +
+                                    fabs(log(o));
+                const double delta = J->delta0 + J->eps_rel * Smag;
                 /* margin mask (i): the alpha-skip decision */
                 const double ln_a = log(o) + power;
-                if (fabs(ln_a - ln_amin) < 2.0 * J->delta_a) {
-                    double imp = T * a_min * (1.0 + 2.0 * J->cmax) * exp(2.0 * J->delta_a);
-                    if (imp > J->impact_tau) { flagged = 1; bound += imp; }
-                }
+                if (fabs(ln_a - ln_amin) < 2.0 * delta)
+                    bound += T * a_min * (1.0 + 2.0 * J->cmax) * exp(2.0 * delta);
                 if (alpha < a_min) continue;                                /* R-1 */
                 J->live++;
                 const double tT = T * (1.0 - alpha);
                 /* margin mask (ii): the early-termination decision */
-                const double clamped_both = (a_raw * exp(-2.0 * J->delta_a) >= 0.99);
-                const double err = J->delta_a * (S + (clamped_both ? 0.0 : alpha / (1.0 - alpha))) +
+                const double clamped_both = (a_raw * exp(-2.0 * delta) >= 0.99);
+                const double err = Serr + (clamped_both ? 0.0 : delta * alpha / (1.0 - alpha)) +
                                    1e-6 * (double)(e - start + 1);
-                if (fabs(log(tT) - ln_tmin) < 2.0 * err) {
-                    double imp = T * (1.0 + 2.0 * J->cmax);
-                    if (imp > J->impact_tau) { flagged = 1; bound += imp; }
-                }
+                if (fabs(log(tT) - ln_tmin) < 2.0 * err) bound += T * (1.0 + 2.0 * J->cmax);
                 if (tT < t_min) break;                                      /* R-2 */
                 for (int ch = 0; ch < 3; ch++) C[ch] += (double)J->rgb[3 * i + ch] * alpha * T; /* R-3 */
                 T = tT;
-                if (!clamped_both) S += alpha / (1.0 - alpha);
+                if (!clamped_both) Serr += delta * alpha / (1.0 - alpha);
             }
+            const int flagged = bound > J->budget;
             const size_t pix = (size_t)py * (size_t)J->W + (size_t)px;
             const size_t plane = (size_t)J->W * (size_t)J->H;
             for (int ch = 0; ch < 3; ch++) J->out_rgb[ch * plane + pix] = C[ch] + T * J->bg[ch];
@@ -416,10 +424,14 @@ static void *blend_worker(void *arg) {
 }
 
 /* out_rgb: [3][H][W] planar, out_T: [H][W]; flag / flip_bound may be NULL.
+ * Decision-margin mask (R-21, test device): a decision is ambiguous when it lies within
+ * 2 delta of its threshold, delta = delta0 + eps_rel * S the documented bound on the GPU's
+ * |d ln alpha| for that pair; flip_bound = the summed first-order impacts of a pixel's
+ * ambiguous decisions, flag = flip_bound > budget.
  * stats[0] = evaluated pairs, stats[1] = pairs with alpha >= 1/255. */
 void orc_blend(const float *xy, const float *conic, const float *opacity, const float *rgb,
                const uint32_t *vals, const uint32_t *ranges, int W, int H, const float *bg,
-               double delta_a, double impact_tau, double cmax, int nthreads,
+               double delta0, double eps_rel, double budget, double cmax, int nthreads,
                double *out_rgb, double *out_T, uint8_t *flag, double *flip_bound,
                int64_t *stats) {
     if (nthreads < 1) nthreads = 1;
@@ -431,7 +443,7 @@ void orc_blend(const float *xy, const float *conic, const float *opacity, const 
         J->vals = vals; J->ranges = ranges; J->W = W; J->H = H;
         J->gx = ceil_div(W, TILE); J->gy = ceil_div(H, TILE);
         for (int ch = 0; ch < 3; ch++) J->bg[ch] = bg[ch];
-        J->delta_a = delta_a; J->impact_tau = impact_tau; J->cmax = cmax;
+        J->delta0 = delta0; J->eps_rel = eps_rel; J->budget = budget; J->cmax = cmax;
         J->out_rgb = out_rgb; J->out_T = out_T; J->flag = flag; J->flip_bound = flip_bound;
         J->nthreads = nthreads; J->tid = k;
         if (nthreads > 1) pthread_create(&th[k], NULL, blend_worker, J);

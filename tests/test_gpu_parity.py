@@ -12,8 +12,8 @@ import pytest
 import oracle
 from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GsError, synth
 
-from gpu_util import (MAX_ABS, MIN_PSNR, compare, gpu_binning, gpu_blend_from, gpu_preprocess, gpu_render,
-                      make_ctx)
+from gpu_util import (MAX_ABS, MIN_PSNR, check_frame, exponent_errors, gpu_binning, gpu_blend_from, gpu_preprocess,
+                      gpu_render, make_ctx)
 
 pytestmark = pytest.mark.gpu
 
@@ -117,11 +117,7 @@ def test_blend_parity_on_oracle_binning(case, blend):
     ctx = make_ctx(scene, cam)
     pre, b, ref = oracle.render(scene, cam, bg)
     rgb, T = gpu_blend_from(ctx, pre, b, cam.W, cam.H, bg, blend)
-    m = compare(rgb, T, ref)
-    assert m["max_unflagged"] <= MAX_ABS, m
-    assert m["psnr"] >= MIN_PSNR, m
-    assert m["over_within_bound"], m
-    assert m["T_max"] <= MAX_ABS, m
+    check_frame(f"blend_only/{case}/{['tc', 'direct', 'mma'][blend]}", rgb, T, ref)
 
 
 @pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA], ids=["tc", "direct", "mma"])
@@ -132,62 +128,28 @@ def test_render_parity_end_to_end(case, blend):
     rgb, T = gpu_render(ctx, scene, cam, bg, blend)
     assert np.isfinite(rgb).all() and np.isfinite(T).all()
     _, _, ref = oracle.render(scene, cam, bg)
-    m = compare(rgb, T, ref)
-    print(case, blend, m)
-    assert m["max_unflagged"] <= MAX_ABS, m
-    assert m["psnr"] >= MIN_PSNR, m
-    assert m["over_within_bound"], m
+    check_frame(f"end_to_end/{case}/{['tc', 'direct', 'mma'][blend]}", rgb, T, ref)
 
 
-def test_exponent_precision_bound():
-    """|d ln alpha| of the tensor-core exponent (TF32 hi/lo, reading R-11) stays
-    below the delta_a the margin mask assumes, on every pair the oracle keeps."""
-    import torch
-    scene, cam, bg = _cfg("C2")
+@pytest.mark.parametrize("case", list(CASES))
+def test_exponent_precision_bound(case):
+    """|d ln alpha| of the tensor-core exponent (TF32 hi/lo, reading R-11) stays below the
+    bound the margin mask assumes, delta = DELTA_0 + EPS_REL * S (S = magnitude of the
+    Eq. (6) terms about the tile centre), on every pair the oracle keeps: every tile of the
+    small cases, 96 sampled tiles of the large ones; the adversarial case has needles with
+    anisotropy up to 300 (SURVEY C-11)."""
+    scene, cam, bg = CASES[case]()
     ctx = make_ctx(scene, cam)
     pre = oracle.preprocess(scene, cam)
     b = oracle.binning(pre, cam.W, cam.H)
-    gx = (cam.W + 15) // 16
-    # a sample of tiles keeps the dump small
-    rng = np.random.default_rng(0)
-    ranges = np.zeros_like(b["ranges"])
-    sel = rng.choice(len(ranges), 64, replace=False)
-    ranges[sel] = b["ranges"][sel]
-    K = b["K"]
-    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    out_m = torch.full((K, 256), float("nan"), device="cuda")
-    ctx.gs_debug_exponents(scene.n, t(pre["xy"]), t(pre["conic"]), t(pre["opacity"]), t(b["vals"].view(np.int32)),
-                           K, t(ranges.view(np.int32)), cam.W, cam.H, out_m)
-    m = out_m.cpu().numpy()
-    worst, n_pairs = 0.0, 0
-    lanes = np.arange(256)
-    w, l = lanes // 32, lanes % 32
-    px_in = 8 * (w % 2) + l % 8
-    py_in = 4 * (w // 2) + l // 8
-    for tsel in sel:
-        s, e = b["ranges"][tsel]
-        if e == s:
-            continue
-        tx, ty = tsel % gx, tsel // gx
-        px = 16 * tx + px_in
-        py = 16 * ty + py_in
-        idx = b["vals"][s:e]
-        xy = pre["xy"][idx].astype(np.float64)
-        co = pre["conic"][idx].astype(np.float64)
-        o = pre["opacity"][idx].astype(np.float64)
-        dx = xy[:, 0:1] - px[None, :]
-        dy = xy[:, 1:2] - py[None, :]
-        power = -0.5 * (co[:, 0:1] * dx * dx + co[:, 2:3] * dy * dy) - co[:, 1:2] * dx * dy
-        ln_a = np.log(o)[:, None] + power
-        keep = ln_a >= np.log(1 / 255.0)
-        got = m[s:e] * np.log(2.0)
-        d = np.abs(got - ln_a)[keep]
-        n_pairs += d.size
-        if d.size:
-            worst = max(worst, float(d.max()))
-    print(f"max |d ln alpha| = {worst:.3e} over {n_pairs} kept pairs")
-    assert n_pairs > 10000
-    assert worst <= oracle.DELTA_A
+    nt = len(b["ranges"])
+    tiles = np.arange(nt) if nt <= 200 else np.random.default_rng(0).choice(nt, 96, replace=False)
+    err, S = exponent_errors(ctx, scene.n, pre, b, cam.W, cam.H, tiles)
+    bound = oracle.DELTA_0 + oracle.EPS_REL * S
+    print(f"{case}: max |d ln alpha| = {err.max():.3e}, max err/bound = {(err / bound).max():.3f} "
+          f"over {err.size} kept pairs")
+    assert err.size > 1000
+    assert (err <= bound).all(), (float(err.max()), float((err / bound).max()))
 
 
 def test_determinism_and_tc_vs_direct():
@@ -278,11 +240,8 @@ def test_full_size_c5_view_sampled_parity(obox):
     mask = np.zeros((cam.H, cam.W), bool)
     for t in sel:
         mask[16 * (t // gx):16 * (t // gx) + 16, 16 * (t % gx):16 * (t % gx) + 16] = True
-    err = np.abs(rgb - ref["rgb"])[:, mask]
-    ok = ~ref["flag"][mask]
-    assert err[:, ok].max() <= MAX_ABS
-    mse = float((err ** 2).mean())
-    assert 10 * np.log10(1 / max(mse, 1e-30)) >= MIN_PSNR
+    sub = {k: ref[k][..., mask] for k in ("rgb", "T", "flag", "bound")}
+    check_frame(f"C5_full/{'obox' if obox else 'vanilla'}/48_tiles", rgb[:, mask], T[mask], sub)
 
 
 # ---------------------------------------------------------------------------
@@ -631,8 +590,7 @@ def test_random_scenes_and_cameras_bit_exact(seed):
         assert np.array_equal(gb["ranges"], ref_b["ranges"])
     rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=GS_FLAG_OBOX)
     _, _, ref = oracle.render(scene, cam, bg)
-    m = compare(rgb, T, ref)
-    assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+    check_frame(f"random/{seed}", rgb, T, ref)
 
 
 def test_wide_depth_range_takes_the_fourth_pass():
@@ -697,8 +655,7 @@ def test_scale_modifier_sh_stride_and_plain_colours(variant):
         assert np.array_equal(gb["vals"], ref_b["vals"]) and np.array_equal(gb["ranges"], ref_b["ranges"])
         rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, flags=flags, scale_modifier=sm)
         _, _, ref = oracle.render(scene, cam, bg, obox=obox, scale_modifier=sm)
-        m = compare(rgb, T, ref)
-        assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+        check_frame(f"inputs/{variant}/{'obox' if obox else 'vanilla'}", rgb, T, ref)
 
 
 @pytest.mark.parametrize("obox", [False, True], ids=["vanilla", "obox"])
@@ -721,8 +678,7 @@ def test_capacity_boundary_is_exact(obox):
     assert np.array_equal(gb["keys"], ref_b["keys"]) and np.array_equal(gb["vals"], ref_b["vals"])
     rgb, T = gpu_render(ctx, scene, cam, bg, GS_BLEND_TC, st=st, flags=flags)
     _, _, ref = oracle.render(scene, cam, bg, obox=obox)
-    m = compare(rgb, T, ref)
-    assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+    check_frame(f"capacity_boundary/{'obox' if obox else 'vanilla'}", rgb, T, ref)
     ctx.close()
     ctx = make_ctx(scene, cam, max_keys=K - 1)
     with pytest.raises(GsError) as e:
@@ -784,5 +740,5 @@ def test_degenerate_image_and_scene_sizes(wh, n):
         for blend in (GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA):
             rgb, T = gpu_render(ctx, scene, cam, bg, blend, flags=flags)
             _, _, ref = oracle.render(scene, cam, bg, obox=obox)
-            m = compare(rgb, T, ref)
-            assert m["max_unflagged"] <= MAX_ABS and m["psnr"] >= MIN_PSNR and m["over_within_bound"], m
+            check_frame(f"degenerate/{W}x{H}/n{n}/{'obox' if obox else 'vanilla'}/{['tc', 'direct', 'mma'][blend]}",
+                        rgb, T, ref)

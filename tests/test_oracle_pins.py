@@ -560,3 +560,132 @@ def test_margin_mask_flags_a_termination_on_the_threshold():
     assert out["flag"].all()
     pre3, b3 = _one_tile([[7.5, 7.5]] * 2, conic[:2], [a] * 2, [[0.5, 0.5, 0.5]] * 2)
     assert not oracle.blend(pre3, b3, 16, 16)["flag"].any()
+
+
+# ---- compositing readings R-2 / R-4 and the Jacobian clamp of R-14: closed forms ------
+# Each of these fails under the plausible misreading it names (tests/test_oracle_mutations.py
+# rebuilds the oracle with each misreading and checks that some pin fails).
+
+def _flat(o_list, rgb_list):
+    """Splats with a zero conic on one 16x16 tile: power = 0 at every pixel, so alpha = o
+    exactly (Eq. 2-3 with Sigma^-1 = 0), and the list order is the given order."""
+    n = len(o_list)
+    return _one_tile([[7.5, 7.5]] * n, [[0.0, 0.0, 0.0]] * n, o_list, rgb_list)
+
+
+def test_alpha_cap_closed_form():
+    """R-4 (BASELINE.json north_star: alpha capped at 0.99; vanilla): one splat with
+    o = 0.999 covering pixel (8, 8) exactly -> alpha = min(0.99, 0.999) = 0.99, so
+    out = 0.99 c + 0.01 bg and T = 0.01 (PAPER.md P:169 / P:376 state no cap: without it
+    T would be 1e-3). A splat with o = 0.5 is below the cap and composites at 0.5."""
+    c = np.float32([0.8, 0.3, 0.1]).astype(np.float64)
+    bg = np.float32([0.2, 0.4, 0.6]).astype(np.float64)
+    pre, b = _one_tile([[8.0, 8.0]], [[0.05, 0.0, 0.05]], [0.999], [c])
+    out = oracle.blend(pre, b, 16, 16, bg, threads=1)
+    np.testing.assert_allclose(out["rgb"][:, 8, 8], 0.99 * c + 0.01 * bg, rtol=0, atol=1e-12)
+    assert abs(out["T"][8, 8] - 0.01) < 1e-12
+    o3, oT = oracle.blend_pixel([0], pre, 8.0, 8.0, bg)
+    np.testing.assert_allclose(o3, 0.99 * c + 0.01 * bg, rtol=0, atol=1e-12)
+    assert abs(oT - 0.01) < 1e-12
+    pre5, b5 = _flat([0.5], [c])
+    o5 = oracle.blend(pre5, b5, 16, 16, bg, threads=1)
+    a = float(np.float32(0.5))
+    np.testing.assert_allclose(o5["rgb"][:, 3, 11], a * c + (1 - a) * bg, rtol=0, atol=1e-12)
+
+
+def test_early_termination_closed_form():
+    """R-2 (BASELINE.json north_star "early termination at T < 1e-4"; vanilla): a stack of
+    six flat splats with alpha = o = 0.95 gives T_j = (1 - o)^j: T_3 = 1.25e-4 >= 1e-4, and
+    the 4th splat would leave T_4 = 6.25e-6 < 1e-4, so compositing stops there WITHOUT
+    compositing the 4th splat: out = sum_{j<3} c_j o T_j + T_3 bg, T = T_3. Three
+    misreadings give other values: compositing the stopper first (T = T_4 and its colour
+    added), the paper's literal "T <= 0 -> stop" (all six composited, T = T_6), and a
+    1e-6 threshold (the 4th composited, T = T_4)."""
+    o = float(np.float32(0.95))
+    cols = np.float32([[0.9, 0.1, 0.2], [0.1, 0.8, 0.3], [0.2, 0.2, 0.9],
+                       [0.7, 0.6, 0.5], [0.3, 0.9, 0.9], [1.0, 0.0, 1.0]]).astype(np.float64)
+    bg = np.float32([0.05, 0.1, 0.15]).astype(np.float64)
+    pre, b = _flat([0.95] * 6, cols)
+    out = oracle.blend(pre, b, 16, 16, bg, threads=1)
+    T = [(1.0 - o) ** j for j in range(7)]
+    assert T[3] >= 1e-4 > T[4]
+    want = sum(cols[j] * o * T[j] for j in range(3)) + T[3] * bg
+    for py, px in ((0, 0), (7, 9), (15, 15)):
+        np.testing.assert_allclose(out["rgb"][:, py, px], want, rtol=0, atol=1e-13)
+        assert abs(out["T"][py, px] - T[3]) < 1e-15
+    o3, oT = oracle.blend_pixel(np.arange(6), pre, 3.0, 4.0, bg)
+    np.testing.assert_allclose(o3, want, rtol=0, atol=1e-13)
+    assert abs(oT - T[3]) < 1e-15
+    # the same stack one splat shorter than the stop never reaches it: T = T_3 exactly too,
+    # and with the stopper moved to the end of a shorter list the skip rule still holds
+    pre3, b3 = _flat([0.95] * 3, cols[:3])
+    o3b = oracle.blend(pre3, b3, 16, 16, bg, threads=1)
+    np.testing.assert_allclose(o3b["rgb"][:, 5, 5], want, rtol=0, atol=1e-13)
+
+
+def test_jacobian_clamp_closed_form():
+    """R-14 (vanilla EWA): the Jacobian of the projection is evaluated at the view-space
+    point with x/z and y/z clamped to +-1.3 tan(fov/2) (a clamp, not a cull). Two Gaussians
+    outside that cone (x/z = 1.0 and y/z = -1.2, limit 1.3 * 0.64 = 0.832) but reaching the
+    image: cov2D = J Sigma J^T + 0.3 I with the clamped J, computed here by hand in float64
+    from the textbook Jacobian of (f x/z + c_x, f y/z + c_y). The unclamped Jacobian and a
+    1.0 tan(fov/2) clamp both miss by > 10 %."""
+    from scipy.spatial.transform import Rotation
+    f, z, W = 50.0, 10.0, 64
+    cam = _axis_camera(W=W, H=W, f=f, D=z)       # world z = 0 is at depth 10; R = I
+    tanf = float(np.float32(W / (2 * f)))
+    q = np.array([[0.9, 0.2, -0.3, 0.25], [0.8, -0.1, 0.4, 0.3]], np.float64)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    scales = np.array([[2.0, 0.6, 1.2], [0.7, 1.9, 1.1]])
+    means = np.array([[1.0 * z, 0.1, 0.0], [0.2, -1.2 * z, 0.0]])
+    sc = _scene(means, scales, q.astype(np.float32), [0.9, 0.9], _sh_zero(2, 0), 0)
+    pre = oracle.preprocess(sc, cam)
+    assert (pre["touched"] > 0).all()
+
+    def cov2d(i, lim):
+        m = means[i].astype(np.float32).astype(np.float64)
+        v = m + np.array([0.0, 0.0, z])                           # view space (R = I, t = (0,0,z))
+        u = np.clip(v[:2] / v[2], -lim, lim)
+        J = np.array([[f / v[2], 0.0, -f * u[0] / v[2]], [0.0, f / v[2], -f * u[1] / v[2]]])
+        Rq = Rotation.from_quat(np.roll(q[i].astype(np.float32).astype(np.float64), -1)).as_matrix()
+        s = scales[i].astype(np.float32).astype(np.float64)
+        return J @ (Rq @ np.diag(s * s) @ Rq.T) @ J.T + 0.3 * np.eye(2)
+
+    for i in range(2):
+        A, B, C = pre["conic"][i].astype(np.float64)
+        got = np.linalg.inv(np.array([[A, B], [B, C]]))
+        want = cov2d(i, 1.3 * tanf)
+        assert np.abs(got - want).max() <= 1e-5 * np.abs(want).max(), (i, got, want)
+        for wrong in (cov2d(i, np.inf), cov2d(i, 1.0 * tanf)):
+            assert np.abs(wrong - want).max() > 0.1 * np.abs(want).max()
+
+
+def test_single_anisotropic_gaussian_matches_scipy_density():
+    """Eq. (2)-(3) with a full 2x2 conic (cross term B != 0): alpha(p) = o * N(p; mu, Sigma) /
+    N(mu; mu, Sigma), the bivariate normal density of scipy.stats evaluated from the 2D
+    covariance Sigma = (conic)^-1, on every pixel of a tile (alpha capped at 0.99, skipped
+    below 1/255): out = alpha c + (1 - alpha) bg and T = 1 - alpha."""
+    from scipy.stats import multivariate_normal
+    cov = np.array([[9.0, -5.5], [-5.5, 6.0]])
+    inv = np.linalg.inv(cov)
+    conic = np.float32([inv[0, 0], inv[0, 1], inv[1, 1]])
+    mu = np.float32([6.7, 9.2])
+    o = np.float32(0.93)
+    c = np.float32([0.7, 0.2, 0.5]).astype(np.float64)
+    bg = np.float32([0.1, 0.1, 0.3]).astype(np.float64)
+    pre, b = _one_tile([mu], [conic], [o], [c])
+    out = oracle.blend(pre, b, 16, 16, bg, threads=1)
+    A, B, C = conic.astype(np.float64)
+    sig = np.linalg.inv(np.array([[A, B], [B, C]]))      # the covariance the fp32 conic encodes
+    rv = multivariate_normal(mean=mu.astype(np.float64), cov=sig)
+    yy, xx = np.mgrid[0:16, 0:16]
+    dens = rv.pdf(np.stack([xx, yy], -1).astype(np.float64)) / rv.pdf(mu.astype(np.float64))
+    alpha = np.minimum(0.99, float(o) * dens)
+    a = np.where(alpha >= np.float32(1 / 255), alpha, 0.0)
+    assert (a > 0).sum() > 50 and (a == 0).sum() > 10     # both the kept and skipped regions
+    for ch in range(3):
+        np.testing.assert_allclose(out["rgb"][ch], a * c[ch] + (1 - a) * bg[ch], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(out["T"], 1 - a, rtol=0, atol=1e-12)
+    # the mirrored cross term gives a visibly different image
+    pre_m, _ = _one_tile([mu], [[conic[0], -conic[1], conic[2]]], [o], [c])
+    assert np.abs(oracle.blend(pre_m, b, 16, 16, bg, threads=1)["T"] - out["T"]).max() > 0.05
