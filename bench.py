@@ -174,15 +174,18 @@ def run_ours(args):
 
     from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
                                        Context, camera, opts, scene_to_device, scene_to_host, synth)
-    from paper_2604_02120_b200.orbit import gather_frames_pipelined, partition_views, share_frames
+    from paper_2604_02120_b200.orbit import gather_frames_pipelined, gather_plan, partition_views, share_frames
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
+    backend = None
     if ws > 1:
         backend = os.environ.get("GS_BENCH_BACKEND", "nccl")   # gloo: test hook only (see _dist)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        if dist.get_world_size() != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but the process group has {dist.get_world_size()} ranks")
     scene, cams, bg = synth.make_config("C5", views=args.views)
     W, H = cams[0].W, cams[0].H
     mine = partition_views(args.views, ws, rank)
@@ -191,9 +194,10 @@ def run_ours(args):
     blend = GS_BLEND_DIRECT if args.blend == "direct" else GS_BLEND_TC
     base_flags = INTERSECT[args.intersect][0]
     ctx = Context(local, max_points=scene.n, max_keys=args.max_keys, max_w=W, max_h=H)
-    # view group: 16 on one GPU; with N > 1 at most half a rank's views, so that the NCCL
-    # gather of the first group overlaps the rendering of the next (orbit.gather_frames_pipelined)
-    group = VIEW_GROUP if ws == 1 else max(1, min(VIEW_GROUP, per // 2))
+    # view group: the rank's whole block up to 16 views (one scene read per group), the NCCL
+    # gather in chunks of a quarter block that start as soon as their views are blended
+    # (gs_stream_wait_view), so only the last chunk's transfer trails the rendering
+    group, chunk = gather_plan(per, VIEW_GROUP)
     ctx.gs_set_view_group(group, True)
     st = scene_to_device(scene)
     fused = ws > 1 and args.gather == "fused"
@@ -220,9 +224,9 @@ def run_ours(args):
         ctx.gs_render_views(st, my_cams, W, H, o, out_rgb, out_T, stream)
         if fused:
             return   # the frames are already in rank 0's buffers when the blends complete
-        # NCCL frame gather to rank 0, view group by view group as the groups finish
-        gather_frames_pipelined(out_rgb, out_T, ws, rank, group,
-                                wait_group=lambda s, g: ctx.gs_stream_wait_group(s, g), dist=dist, out=gather_out)
+        # NCCL frame gather to rank 0, chunk by chunk as the views finish
+        gather_frames_pipelined(out_rgb, out_T, ws, rank, chunk,
+                                wait_views=lambda s, v: ctx.gs_stream_wait_view(s, v), dist=dist, out=gather_out)
 
     for _ in range(args.warmup):
         step(o_plain)
@@ -285,22 +289,28 @@ def run_ours(args):
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs") or 6650.0
     smax = peaks.get("sm_max_mhz") or 1965.0
-    fp32_peak = 148 * 128 * 2 * smax * 1e6 / 1e12        # TFLOP/s, FP32 FMA on the CUDA cores
+    clk_mhz = clk.get("sm_mhz") or smax
+    # issue roof of the blend: 148 SMs x 4 schedulers x 32 lanes per clock,
+    # at the median SM clock measured during the timed region
+    issue_peak = 148 * 128 * clk_mhz * 1e6 / 1e12        # T lane-slots/s
     N = scene.n
     M = scene.shs.shape[1]
-    # algorithmic bytes: preprocess reads the means of every
-    # Gaussian and the rest of the inputs of the projected ones ONCE PER VIEW GROUP
-    # (n_vis, the per-view count, is a lower bound of the group's union), writes 60 B
-    # per Gaussian per view
-    pre_bytes = (N * 12 + n_vis * (12 + 16 + 4 + 12 * M)) / group + N * 60
+    # algorithmic bytes: per view group the preprocess reads the 44 B of means,
+    # scales, rotation and opacity of every Gaussian and the SH record (12 M B) of the ones
+    # some view of the group projects (n_vis, the per-view count, is a lower bound of the
+    # group's union); per view it writes the warp's slot count (4 B per 32 Gaussians) and
+    # 60 B per visible Gaussian (index, depth, mean, conic+opacity, colour, rect, tiles)
+    pre_bytes = (N * 44 + n_vis * 12 * M) / group + N / 8 + n_vis * 60
     # binning: compaction (read touched+depth, write 8 B/vis), 3 depth passes (16 B/vis
     # each + a histogram read) with the rect gather (16 B/vis), duplication (8 B/key
     # written), tile sort 2 passes (16 B/key each + histogram read), ranges (4 B/key)
     bin_bytes = N * 8 + n_vis * 8 + 3 * 16 * n_vis + 4 * n_vis + 16 * n_vis + n_keys * 8 + \
         2 * 16 * n_keys + 4 * n_keys + 4 * n_keys
-    # blend: 13 flop per evaluated (Gaussian, pixel) exponent (Eq. 6 dot product + skip
-    # test) and 12 flop per kept pair (alpha, clamp, T update, stop test, colour)
-    blend_flop = 13.0 * n_eval + 12.0 * n_kept
+    # blend: SURVEY 8(d)'s issue roof -- 4 lane-slots per (Gaussian, pixel) pair the MMA
+    # evaluates (the warp-level exit and the warp-uniform alpha-skip leave ~4 issue slots of
+    # compositing per MMA pair; the Eq. 6 dot product itself runs on the tensor pipe)
+    BLEND_SLOTS_PER_PAIR = 4.0
+    blend_slots = BLEND_SLOTS_PER_PAIR * n_eval
     stages = {
         "preprocess": {"ms": pre_ms, "bound": "hbm", "achieved": pre_bytes / (pre_ms * 1e-3) / 1e9,
                        "peak": hbm, "unit": "GB/s", "view_group": group,
@@ -308,8 +318,9 @@ def run_ours(args):
         "binning": {"ms": bin_ms, "bound": "hbm", "achieved": bin_bytes / (bin_ms * 1e-3) / 1e9, "peak": hbm,
                     "unit": "GB/s", "kernels": "compaction, 3 depth passes, row entries + row pass, pair offsets, "
                     "column pass with tile ranges (two-level binning)", "timing": "chains serialised (extra orbit)"},
-        "blend": {"ms": blend_ms, "bound": "alu", "achieved": blend_flop / (blend_ms * 1e-3) / 1e12,
-                  "peak": fp32_peak, "unit": "TFLOP/s", "pairs_evaluated": n_eval, "pairs_kept": n_kept,
+        "blend": {"ms": blend_ms, "bound": "alu", "achieved": blend_slots / (blend_ms * 1e-3) / 1e12,
+                  "peak": issue_peak, "unit": "T lane-slots/s", "pairs_evaluated": n_eval, "pairs_kept": n_kept,
+                  "slots_per_pair": BLEND_SLOTS_PER_PAIR,
                   "timing": "live, CUDA events around each launch in the timed region"},
     }
     for v in stages.values():
@@ -324,8 +335,11 @@ def run_ours(args):
         pass
     bl = ncu.get("k_blend_tc", {})
     roof = {"kernel": "k_blend_tc", "bound": "alu", "achieved": stages["blend"]["achieved"],
-            "peak": stages["blend"]["peak"], "unit": "TFLOP/s", "frac": stages["blend"]["frac"],
-            "traffic": bl.get("dram_bytes_per_launch"), "peak_note": "FP32 CUDA-core peak 148x128x2 flop x max clock",
+            "peak": stages["blend"]["peak"], "unit": "T lane-slots/s", "frac": stages["blend"]["frac"],
+            "traffic": bl.get("dram_bytes_per_launch"),
+            "peak_note": ("issue roof: 148 SMs x 128 lanes x median SM clock of the timed region "
+                          f"({clk_mhz:.0f} MHz); achieved = 4 lane-slots (SURVEY 8(d)) x the (Gaussian, pixel) "
+                          "pairs the MMA evaluates per frame / live blend time"),
             "tensor_pipe_pct": bl.get("tensor_pipe_pct"), "issue_active_pct": bl.get("issue_active_pct"),
             "ncu_source": bl.get("source")}
 
@@ -346,13 +360,18 @@ def run_ours(args):
             torch.cuda.synchronize()
             dms, dfr = ctx.gs_stage_times()
             return dms[2] / max(dfr, 1), per / (e0.elapsed_time(e1) / 1e3)
-        d_ms, d_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_DIRECT, flags=GS_FLAG_TIMING))
-        ab = {"blend_tc_ms": blend_ms, "blend_direct_ms": d_ms, "fps_direct": d_fps,
-              "speedup_tc_over_direct": d_ms / blend_ms, "mma_sync": {}}
+        # every arm on the headline's lists (same intersection flag), the tcgen05 arm re-timed
+        # in the same way beside them
+        t_ms, t_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_TC,
+                                      flags=GS_FLAG_TIMING | base_flags))
+        d_ms, d_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_DIRECT,
+                                      flags=GS_FLAG_TIMING | base_flags))
+        ab = {"intersection": INTERSECT[args.intersect][1], "blend_tc_ms": t_ms, "fps_tc": t_fps,
+              "blend_direct_ms": d_ms, "fps_direct": d_fps, "speedup_tc_over_direct": d_ms / t_ms, "mma_sync": {}}
         for b in (32, 64, 128, 256):
             m_ms, m_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA, batch=b,
-                                          flags=GS_FLAG_TIMING))
-            ab["mma_sync"][f"b{b}"] = {"blend_ms": m_ms, "fps": m_fps, "speedup_tc_over_mma": m_ms / blend_ms}
+                                          flags=GS_FLAG_TIMING | base_flags))
+            ab["mma_sync"][f"b{b}"] = {"blend_ms": m_ms, "fps": m_fps, "speedup_tc_over_mma": m_ms / t_ms}
 
     # --- N3: the other intersection modes (bit-identical frames, fewer pairs), one timed orbit each ---
     n3 = {}
@@ -532,6 +551,9 @@ def run_ours(args):
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
                 "roofline": roof, "stages": stages, "clocks": clk,
+                "comm": ({"backend": backend, "world_size": dist.get_world_size(),
+                          "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
+                          "view_group": group, "gather_chunk_views": chunk} if ws > 1 else None),
                 "gpu_launches": int(launches), "e2e": e2e, "cpu_baseline": cpu, "ab_blend": ab, "intersection_modes": n3, "row_split_one_view": row_split, "other_configs": per_config,
                 "resolution_sweep": res_sweep,
                 "work_per_frame": {"n_visible": n_vis, "n_keys": n_keys, "pairs_evaluated": n_eval,
@@ -565,6 +587,19 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the C2-C4b config shapes")
     ap.add_argument("--sweep-views", type=int, default=8)
     args = ap.parse_args()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and ws_env is None:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    if ws_env is not None and int(ws_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -85,7 +85,10 @@ enum {
                            * arrays (they are resident and unchanged, as in an orbit or serving
                            * loop), so the call's preprocess and binning may start before the
                            * caller's earlier work on `stream` (e.g. the previous call's last
-                           * blends) has finished; frames are still written in stream order. */
+                           * blends) has finished; frames are still written in stream order.
+                           * Safe with interleaved single-view calls: the view-group calls use
+                           * their own workspaces and error accumulator, never the ones of
+                           * gs_render / gs_debug_* (which run in the caller's stream order). */
     GS_FLAG_OBOX = 16u    /* opacity-aware box (cheaper): the vanilla rect clipped to the
                            * bounding box of the ellipse where alpha >= 1/255 can hold (margin
                            * 5e-3 in ln alpha), and Gaussians with 255*opacity < 1 culled; no
@@ -119,7 +122,9 @@ typedef struct {
     int64_t capacity_keys; /* max_keys of the context                                       */
     int status;            /* gs_status of the last frame (device-side checks included)     */
     int64_t launches;      /* kernels launched by this context since creation              */
-    int64_t pairs_evaluated;  /* GS_FLAG_STATS: (Gaussian, pixel) exponents computed, last frame */
+    int64_t pairs_evaluated;  /* GS_FLAG_STATS: (Gaussian, pixel) exponents the tensor-core MMA
+                               * computed in the last frame (256 x the Gaussians of every batch
+                               * built; k_blend_tc only) */
     int64_t pairs_kept;       /* GS_FLAG_STATS: of those, alpha >= 1/255 on a live pixel       */
 } gs_stats;
 
@@ -170,8 +175,11 @@ int gs_render_views_host(gs_ctx *ctx, void *stream, int N, const float *means3D,
  * 1 = one preprocess launch per view) and whether the group's per-view binning
  * chains run concurrently on context-owned streams (concurrent != 0, default) or
  * back to back on the caller's stream. Output does not depend on either. The
- * first multi-view call with group g allocates g-1 extra workspaces (as
- * gs_ctx_create: about 36 B x max_points + 16 B x max_keys each). With
+ * first multi-view call with group g allocates g workspaces per slot set (two
+ * sets in the concurrent mode; as gs_ctx_create: about 36 B x max_points + 16 B x
+ * max_keys each), separate from the context's single-view workspace. If an
+ * allocation fails the call returns GS_ERR_CUDA with nothing half-allocated
+ * (a later call retries) and `stream` still orders after any work it enqueued. With
  * GS_FLAG_TIMING and concurrent chains the per-stage times overlap.
  * GS_ERR_INVALID_ARG for g outside 1..16. */
 int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
@@ -183,6 +191,14 @@ int gs_set_view_group(gs_ctx *ctx, int g, int concurrent);
  * NCCL frame gather of the multi-GPU orbit -- start on early groups while later
  * ones still render. GS_ERR_INVALID_ARG if g is not a group of that call. */
 int gs_stream_wait_group(gs_ctx *ctx, void *stream, int g);
+
+/* Makes `stream` wait (device-side) until views [0, v] of the last gs_render_views
+ * call are complete (the blends run in view order, so view v's completion implies
+ * every earlier view's). Decouples the gather granularity from the view group:
+ * a rank can read the scene once per group of 8-16 views and still hand its
+ * frames to the NCCL gather two at a time. GS_ERR_INVALID_ARG if v is not a view
+ * of that call. */
+int gs_stream_wait_view(gs_ctx *ctx, void *stream, int v);
 
 /* Asynchronous form of gs_render_views_host (same arguments): returns once the
  * work is enqueued; `stream` reaches completion only after every frame is in

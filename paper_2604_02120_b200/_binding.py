@@ -39,7 +39,7 @@ EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "g
            "gs_last_stats", "gs_status_string", "gs_device_arch", "gs_debug_preprocess",
            "gs_debug_binning", "gs_debug_blend", "gs_debug_exponents", "gs_stage_times",
            "gs_debug_set_trace", "gs_set_view_group", "gs_debug_timeline", "gs_stream_wait_group",
-           "gs_render_views_host_async")
+           "gs_render_views_host_async", "gs_stream_wait_view")
 
 
 class GsError(RuntimeError):
@@ -99,6 +99,7 @@ def load():
         "gs_debug_set_trace": [P, P],
         "gs_set_view_group": [P, I, I],
         "gs_stream_wait_group": [P, P, I],
+        "gs_stream_wait_view": [P, P, I],
         "gs_debug_timeline": [P, ctypes.POINTER(ctypes.c_double), I, ctypes.POINTER(I)],
     }
     for name, args in sig.items():
@@ -218,6 +219,11 @@ class Context:
         n = ctypes.c_int(0)
         _check(self.lib.gs_debug_timeline(self.h, buf, max_spans, ctypes.byref(n)), "gs_debug_timeline")
         return [(int(buf[3 * i]), buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+    def gs_stream_wait_view(self, stream, v):
+        """Device-side wait of `stream` (torch.cuda.Stream) until views [0, v] of the last
+        gs_render_views call are complete."""
+        _check(self.lib.gs_stream_wait_view(self.h, _stream(stream), int(v)), "gs_stream_wait_view")
 
     def gs_stream_wait_group(self, stream, g):
         """Device-side wait of `stream` (torch.cuda.Stream) for view group g of the last

@@ -266,7 +266,6 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         // indices run PF batches ahead in registers; the next tile's first PF
         // index vectors are fetched in three steps during the current tile.
         uint32_t b_idx = 0;
-        unsigned long long n_eval = 0;
         int tile = 0;
         if (lane == 0) tile = tile0 + (int)atomicAdd(tile_queue, 1u);   // tiles [tile0, ntiles)
         tile = __shfl_sync(0xffffffffu, tile, 0);
@@ -325,7 +324,6 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         for (;;) {
             if (tile >= ntiles) {
                 for (int t = 0; t < NBLD; t++) push(make_int4(-1, 0, 0, 0), 0u);   // one per builder
-                if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
                 break;
             }
             head_step();
@@ -345,7 +343,6 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             }
             const uint32_t cnt = min((uint32_t)NB, rg.y - b);
             push(make_int4(tile, (int)seq, (int)cnt, (int)b), idx[0]);
-            if (STATS && lane == 0) n_eval += (unsigned long long)cnt * GS_TILE_PIX;
 #pragma unroll
             for (int j = 0; j + 1 < PF; j++) idx[j] = idx[j + 1];
             idx[PF - 1] = (b + PF * NB + lane < rg.y) ? vals[b + PF * NB + lane] : 0u;
@@ -353,6 +350,9 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         }
     } else if (warp >= WARP_BUILD0 && warp < WARP_BUILD0 + NBLD) {
         // =================== builders: M_g rows (Eq. 6-7) ===================
+        // STATS: the exponents the MMA computes, (Gaussian, pixel) pairs of the batches built
+        // (batches of a tile found terminated before their build are dropped, not counted)
+        unsigned long long n_eval = 0;
         for (uint32_t kb = warp - WARP_BUILD0;; kb += NBLD) {
             const int r = kb % RAW, s = kb % STAGES, slot = kb % RING;
             mbar_wait(&sm.raw_full[r], (kb / RAW) & 1u);
@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             if (hd.z > 0) {
                 if (lane < NB) build_row(sm, s, slot, hd, sm.raw[r][lane], lane, gx);
                 fence_proxy_async_smem();
+                if (STATS) n_eval += (unsigned long long)hd.z * GS_TILE_PIX;
             }
             if (lane == 0) sm.hdr[slot] = hd;
             __syncwarp();
@@ -399,7 +400,10 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 }
                 __syncwarp();
             }
-            if (hd.x < 0) break;
+            if (hd.x < 0) {
+                if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
+                break;
+            }
         }
     } else {
         // =================== compositors ===================

@@ -31,14 +31,19 @@ struct gs_ctx {
     std::vector<Span> spans;
     double stage_ms[3] = {0, 0, 0};
     int64_t timed_frames = 0;
-    // view groups (gs_render_views): per-view preprocess outputs + counters of views 1..G-1
+    // view groups (gs_render_views): per-view preprocess outputs + counters of every view slot
     int view_group = 4;
     // slot s*MAX_VIEW_GROUP + j = view j of a group in slot set s (two sets: the preprocess of
-    // group g+1 runs while group g bins and blends); slot 0 is the context's own workspace
+    // group g+1 runs while group g bins and blends). None of them is the context's own
+    // workspace `ws`, which only the single-view calls (gs_render, gs_debug_*) use on the
+    // caller's stream: a view group's preprocess may start before the caller's earlier work
+    // (GS_FLAG_STATIC_SCENE, the host entry points), so the two must share no buffer.
     gs::Workspace vws[2 * gs::MAX_VIEW_GROUP] = {};
     bool vws_alloc[2 * gs::MAX_VIEW_GROUP] = {};
     gs::Counters *last_counters = nullptr;   // counters of the last rendered view
-    gs::Sticky *sticky = nullptr;            // errors / largest K over the views of the last call
+    gs::Sticky *sticky = nullptr;            // errors / largest K over the views of the last single-view call
+    gs::Sticky *vsticky = nullptr;           // the same for the view-group calls (their own accumulator)
+    gs::Sticky *last_sticky = nullptr;       // the accumulator of the last call (gs_last_stats)
     // gs_render_views_host: device -> host frame copies overlap the next view group
     cudaStream_t copy_stream = nullptr;
     // scene staging, double-buffered (the async entry point uploads call k+1's scene while
@@ -61,6 +66,9 @@ struct gs_ctx {
     // starts on group g while later groups still render)
     std::vector<cudaEvent_t> ev_group;
     int n_groups = 0;
+    // one event per view of the last gs_render_views call, after its blend (gs_stream_wait_view)
+    std::vector<cudaEvent_t> ev_view;
+    int n_views_last = 0;
 };
 
 static constexpr int kMaxEvents = 4096;
@@ -165,16 +173,24 @@ void span(gs_ctx *c, int stage, int e0, int e1) {
 // get a full workspace of their own (~1 GB at C5), so the views' binning chains can run
 // concurrently on their own streams
 int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
-    if (v == 0) {
-        *out = &c->ws;
-        return GS_OK;
-    }
     gs::Workspace &w = c->vws[v];
     if (!c->vws_alloc[v]) {
-        c->vws_alloc[v] = true;   // (partially allocated pointers are freed by gs_ctx_destroy)
-        if (int rc = check_cuda(alloc_ws(w, (size_t)c->max_points, (size_t)c->max_keys, (size_t)c->max_tiles)))
+        if (!c->vsticky) {
+            cudaError_t e = alloc(c->vsticky, 1);
+            if (e == cudaSuccess) e = cudaMemset(c->vsticky, 0, sizeof(gs::Sticky));
+            if (e != cudaSuccess) {
+                if (c->vsticky) cudaFree(c->vsticky);
+                c->vsticky = nullptr;
+                return check_cuda(e);
+            }
+        }
+        if (int rc = check_cuda(alloc_ws(w, (size_t)c->max_points, (size_t)c->max_keys, (size_t)c->max_tiles))) {
+            free_ws(w);   // a partial allocation is released; the slot stays unallocated (a retry re-allocates)
+            cudaGetLastError();
             return rc;
-        w.sticky = c->sticky;
+        }
+        w.sticky = c->vsticky;
+        c->vws_alloc[v] = true;
     }
     *out = &w;
     return GS_OK;
@@ -193,6 +209,7 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
                   const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
     const int e0 = mark(c, st, o);
     cudaMemsetAsync(c->sticky, 0, sizeof(gs::Sticky), st);   // this call's error accumulator
+    c->last_sticky = c->sticky;
     if (N == 0) cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);   // else k_preprocess zeroes them
     int y0 = 0, y1 = 0;
     gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, y0, y1);
@@ -350,8 +367,9 @@ int gs_ctx_destroy(gs_ctx *c) {
     if (c->sticky) cudaFree(c->sticky);
     for (void *p : {(void *)c->frame_rgb, (void *)c->frame_T})
         if (p) cudaFree(p);
-    for (int v = 1; v < 2 * gs::MAX_VIEW_GROUP; v++)
+    for (int v = 0; v < 2 * gs::MAX_VIEW_GROUP; v++)
         if (c->vws_alloc[v]) free_ws(c->vws[v]);
+    if (c->vsticky) cudaFree(c->vsticky);
     for (int k = 0; k < 2; k++) {
         for (int v = 0; v < gs::MAX_VIEW_GROUP; v++)
             if (c->ev_binned[k][v]) cudaEventDestroy(c->ev_binned[k][v]);
@@ -362,12 +380,10 @@ int gs_ctx_destroy(gs_ctx *c) {
         if (c->bstream[v]) cudaStreamDestroy(c->bstream[v]);
     if (c->ev_start) cudaEventDestroy(c->ev_start);
     for (auto e : c->ev_group) cudaEventDestroy(e);
+    for (auto e : c->ev_view) cudaEventDestroy(e);
     if (c->blend_stream) cudaStreamDestroy(c->blend_stream);
     if (c->pre_stream) cudaStreamDestroy(c->pre_stream);
     for (auto &e : c->ev) cudaEventDestroy(e);
-    for (int k = 0; k < 2; k++) {
-        (void)k;
-    }
     for (int k = 0; k < 2 * gs::MAX_VIEW_GROUP; k++) {
         if (c->view_done[k]) cudaEventDestroy(c->view_done[k]);
         if (c->copies_done[k]) cudaEventDestroy(c->copies_done[k]);
@@ -418,6 +434,16 @@ static int record_group(gs_ctx *c, cudaStream_t s, int g) {
     }
     c->n_groups = g + 1;
     return check_cuda(cudaEventRecord(c->ev_group[g], s));
+}
+
+static int record_view(gs_ctx *c, cudaStream_t s, int v) {
+    while ((int)c->ev_view.size() <= v) {
+        cudaEvent_t e = nullptr;
+        if (int rc = check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return rc;
+        c->ev_view.push_back(e);
+    }
+    c->n_views_last = v + 1;
+    return check_cuda(cudaEventRecord(c->ev_view[v], s));
 }
 
 static int ensure_streams(gs_ctx *c) {
@@ -473,9 +499,32 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             cudaStreamWaitEvent(c->blend_stream, c->ev_start, 0);
         }
     }
+    // an error return after work was enqueued on the context streams joins them with the
+    // caller's stream first, so `stream` never completes before work of this call
+    auto fail = [&](int rc) {
+        if (conc) {
+            for (int k = 0; k < 2; k++) {
+                cudaEventRecord(c->ev_blended[k], c->blend_stream);
+                cudaStreamWaitEvent(st, c->ev_blended[k], 0);
+            }
+            cudaEventRecord(c->ev_pre[0], c->pre_stream);
+            cudaStreamWaitEvent(st, c->ev_pre[0], 0);
+            for (int j = 0; j < GS_CHAIN_STREAMS; j++) {
+                cudaEventRecord(c->ev_binned[0][j], c->bstream[j]);
+                cudaStreamWaitEvent(st, c->ev_binned[0][j], 0);
+            }
+        }
+        return rc;
+    };
+    // the first slot's workspace (and the view accumulator) must exist before its reset
+    {
+        gs::Workspace *w0 = nullptr;
+        if (int rc = view_ws(c, 0, &w0)) return fail(rc);
+    }
     // the call's error accumulator: reset before any of its views bins (stream order: the
     // binning chains wait for the preprocess, which follows this reset on its stream)
-    cudaMemsetAsync(c->sticky, 0, sizeof(gs::Sticky), conc ? c->pre_stream : st);
+    cudaMemsetAsync(c->vsticky, 0, sizeof(gs::Sticky), conc ? c->pre_stream : st);
+    c->last_sticky = c->vsticky;
     int last_set = 0;
     for (int v0 = 0, g = 0; v0 < n_views; v0 += G, g++) {
         const int n = std::min(G, n_views - v0);
@@ -486,7 +535,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
         gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, pv.band_y0, pv.band_y1);
         gs::Workspace *w[gs::MAX_VIEW_GROUP];
         for (int j = 0; j < n; j++) {
-            if (int rc = view_ws(c, set * gs::MAX_VIEW_GROUP + j, &w[j])) return rc;
+            if (int rc = view_ws(c, set * gs::MAX_VIEW_GROUP + j, &w[j])) return fail(rc);
             pv.cam[j] = cams[v0 + j];
             pv.out[j] = gs::pre_out_of(*w[j], false);
         }
@@ -520,12 +569,13 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                               o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
                 const int e2 = mark(c, bl, o);
                 if (hk && hk->post_blend) hk->post_blend(hk->user, bl, v0 + j);
+                if (int rc = record_view(c, bl, v0 + j)) return fail(rc);
                 span(c, 2, e1, e2);
                 if (e2 >= 0) c->timed_frames++;
                 c->last_counters = w[j]->counters;
             }
             cudaEventRecord(c->ev_blended[set], bl);
-            if (int rc = record_group(c, bl, g)) return rc;
+            if (int rc = record_group(c, bl, g)) return fail(rc);
             continue;
         }
         for (int j = 0; j < n; j++) {
@@ -536,13 +586,14 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                           rgb_of[v0 + j], T_of[v0 + j], nullptr);
             const int e2 = mark(c, st, o);
             if (hk && hk->post_blend) hk->post_blend(hk->user, st, v0 + j);
+            if (int rc = record_view(c, st, v0 + j)) return fail(rc);
             span(c, 1, e_prev, e1);
             span(c, 2, e1, e2);
             e_prev = e2;
             if (e2 >= 0) c->timed_frames++;
             c->last_counters = w[j]->counters;
         }
-        if (int rc = record_group(c, st, g)) return rc;
+        if (int rc = record_group(c, st, g)) return fail(rc);
     }
     if (conc) {   // the frames are complete in the caller's stream order
         cudaStreamWaitEvent(st, c->ev_blended[last_set], 0);
@@ -607,22 +658,46 @@ static int render_views_host_impl(gs_ctx *c, void *stream, int N, const float *m
     }
     if (total * sizeof(float) > c->stage_cap) {
         if (check_cuda(cudaDeviceSynchronize())) return GS_ERR_CUDA;   // staging in use by earlier calls
+        // (re)allocation: on failure nothing stays half-allocated (stage_cap 0, null buffers),
+        // so the next call retries instead of using a null staging buffer
         for (int k = 0; k < 2; k++) {
             if (c->stage[k]) cudaFree(c->stage[k]);
             c->stage[k] = nullptr;
-            if (check_cuda(cudaMalloc(&c->stage[k], total * sizeof(float)))) return GS_ERR_CUDA;
+        }
+        c->stage_cap = 0;
+        for (int k = 0; k < 2; k++) {
+            if (cudaMalloc(&c->stage[k], total * sizeof(float)) != cudaSuccess) {
+                cudaGetLastError();
+                for (int j = 0; j < 2; j++) {
+                    if (c->stage[j]) cudaFree(c->stage[j]);
+                    c->stage[j] = nullptr;
+                }
+                return GS_ERR_CUDA;
+            }
         }
         c->stage_cap = total * sizeof(float);
     }
-    if (!c->frame_rgb) {   // 2G staging frames (G <= MAX_VIEW_GROUP), a copy stream and its events
+    if (!c->copy_stream) {   // 2G staging frames (G <= MAX_VIEW_GROUP), a copy stream and its events
         const size_t fr = 2 * gs::MAX_VIEW_GROUP * (size_t)c->max_w * c->max_h;
-        if (check_cuda(cudaMalloc(&c->frame_rgb, 3 * fr * sizeof(float)))) return GS_ERR_CUDA;
-        if (check_cuda(cudaMalloc(&c->frame_T, fr * sizeof(float)))) return GS_ERR_CUDA;
-        if (check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking))) return GS_ERR_CUDA;
-        for (int k = 0; k < 2 * gs::MAX_VIEW_GROUP; k++) {
-            cudaEventCreateWithFlags(&c->view_done[k], cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&c->copies_done[k], cudaEventDisableTiming);
+        float *frgb = nullptr, *fT = nullptr;
+        cudaStream_t cs = nullptr;
+        cudaError_t e = cudaMalloc(&frgb, 3 * fr * sizeof(float));
+        if (e == cudaSuccess) e = cudaMalloc(&fT, fr * sizeof(float));
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+        for (int k = 0; k < 2 * gs::MAX_VIEW_GROUP && e == cudaSuccess; k++) {
+            if (!c->view_done[k]) e = cudaEventCreateWithFlags(&c->view_done[k], cudaEventDisableTiming);
+            if (e == cudaSuccess && !c->copies_done[k])
+                e = cudaEventCreateWithFlags(&c->copies_done[k], cudaEventDisableTiming);
         }
+        if (e != cudaSuccess) {   // all or nothing: a retry starts from scratch
+            if (frgb) cudaFree(frgb);
+            if (fT) cudaFree(fT);
+            if (cs) cudaStreamDestroy(cs);
+            return check_cuda(e);
+        }
+        c->frame_rgb = frgb;
+        c->frame_T = fT;
+        c->copy_stream = cs;
     }
     const int b = c->stage_idx;
     c->stage_idx ^= 1;
@@ -728,6 +803,12 @@ int gs_stream_wait_group(gs_ctx *c, void *stream, int g) {
     return check_cuda(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), c->ev_group[g], 0));
 }
 
+int gs_stream_wait_view(gs_ctx *c, void *stream, int v) {
+    if (!c || v < 0 || v >= c->n_views_last) return GS_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    return check_cuda(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), c->ev_view[v], 0));
+}
+
 int gs_set_view_group(gs_ctx *c, int g, int concurrent) {
     if (!c || g < 1 || g > gs::MAX_VIEW_GROUP) return GS_ERR_INVALID_ARG;
     c->view_group = g;
@@ -743,7 +824,8 @@ int gs_last_stats(gs_ctx *c, gs_stats *out) {
     const gs::Counters *src = c->last_counters ? c->last_counters : c->ws.counters;
     if (check_cuda(cudaMemcpy(&h, src, sizeof(h), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
     gs::Sticky sk{};
-    if (check_cuda(cudaMemcpy(&sk, c->sticky, sizeof(sk), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
+    const gs::Sticky *sks = c->last_sticky ? c->last_sticky : c->sticky;
+    if (check_cuda(cudaMemcpy(&sk, sks, sizeof(sk), cudaMemcpyDeviceToHost))) return GS_ERR_CUDA;
     out->n_points = c->last_n;
     out->n_visible = h.n_visible;
     // K: the last view's, or the largest of the call's views if one of them overflowed
@@ -782,6 +864,7 @@ int gs_debug_preprocess(gs_ctx *c, void *stream, int N, const float *means3D, co
                           o->scale_modifier, *cam, W, H, gs::intersect_mode(o->flags), true, 0,
                           gs::ceil_div_i(H, GS_TILE));
     c->last_counters = c->ws.counters;
+    c->last_sticky = c->sticky;
     if (N > 0) {
         cudaMemsetAsync(depth, 0, sizeof(float) * N, st);
         cudaMemsetAsync(xy, 0, sizeof(float) * 2 * N, st);
@@ -829,6 +912,7 @@ static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, c
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
+    c->last_sticky = c->sticky;
     if (N > 0) {
         k_pack_splats<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, xy, conic, opacity, rgb, c->ws.xy, c->ws.conic_o,
                                                               c->ws.rgb);

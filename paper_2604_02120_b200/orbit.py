@@ -36,18 +36,19 @@ def gather_frames(rgb, T, world: int, rank: int, dist=None):
     return torch.cat(lr, 0), torch.cat(lt, 0)
 
 
-def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_group=None, dist=None, out=None):
-    """gather_frames, one view group at a time, overlapped with the rendering.
+def gather_frames_pipelined(rgb, T, world: int, rank: int, chunk: int, wait_views=None, dist=None, out=None):
+    """gather_frames, a chunk of views at a time, overlapped with the rendering.
 
-    rgb [per,3,H,W] / T [per,H,W] are this rank's frames, rendered in view groups of
-    `group` by gs_render_views. For each group g, `wait_group(stream, g)` (the C-ABI's
-    gs_stream_wait_group) makes a side stream wait until that group has finished
-    blending, and an asynchronous NCCL gather of the group's frames is issued on it,
-    so the transfer of group g overlaps the rendering of groups g+1, ... The current
-    stream waits for every gather before returning. `out`: optional preallocated
-    (rgb_all [world,per,3,H,W], T_all [world,per,H,W]) receive buffers on rank 0.
-    Returns (rgb_all [world*per,3,H,W], T_all [world*per,H,W]) on rank 0 (view order:
-    ranks own contiguous view blocks), (None, None) elsewhere."""
+    rgb [per,3,H,W] / T [per,H,W] are this rank's frames, rendered in view order by
+    gs_render_views. For each chunk [v0, v1) of `chunk` views, `wait_views(stream, v1 - 1)`
+    (the C-ABI's gs_stream_wait_view) makes a side stream wait until those views have
+    finished blending, and an asynchronous NCCL gather of the chunk's frames is issued on
+    it, so the transfer of chunk k overlaps the rendering of the later views; the chunk is
+    independent of the view group the scene is read in. The current stream waits for every
+    gather before returning. `out`: optional preallocated (rgb_all [world,per,3,H,W],
+    T_all [world,per,H,W]) receive buffers on rank 0. Returns (rgb_all [world*per,3,H,W],
+    T_all [world*per,H,W]) on rank 0 (view order: ranks own contiguous view blocks),
+    (None, None) elsewhere."""
     import contextlib
 
     import torch
@@ -56,6 +57,7 @@ def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_grou
     if dist is None:
         import torch.distributed as dist
     per = rgb.shape[0]
+    chunk = max(1, int(chunk))
     if rank == 0:
         if out is None:
             out = (torch.empty((world,) + tuple(rgb.shape), dtype=rgb.dtype, device=rgb.device),
@@ -63,10 +65,10 @@ def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_grou
         all_rgb, all_T = out
     side = torch.cuda.Stream(device=rgb.device) if rgb.is_cuda else None
     works = []
-    for g0 in range(0, per, group):
-        sl = slice(g0, min(per, g0 + group))
-        if wait_group is not None and side is not None:
-            wait_group(side, g0 // group)
+    for v0 in range(0, per, chunk):
+        sl = slice(v0, min(per, v0 + chunk))
+        if wait_views is not None and side is not None:
+            wait_views(side, sl.stop - 1)
         with (torch.cuda.stream(side) if side is not None else contextlib.nullcontext()):
             lr = [all_rgb[r, sl] for r in range(world)] if rank == 0 else None
             lt = [all_T[r, sl] for r in range(world)] if rank == 0 else None
@@ -79,6 +81,15 @@ def gather_frames_pipelined(rgb, T, world: int, rank: int, group: int, wait_grou
     if rank != 0:
         return None, None
     return all_rgb.view((world * per,) + tuple(rgb.shape[1:])), all_T.view((world * per,) + tuple(T.shape[1:]))
+
+
+def gather_plan(per: int, max_group: int = 16):
+    """(view group, gather chunk) for a rank that renders `per` views: the whole block in
+    one preprocess launch when it fits a view group (the scene is read once per rank and
+    step), the gather in chunks of a quarter of the block (at least 1 view), so that only
+    the last chunk's transfer trails the rendering."""
+    group = max(1, min(max_group, per))
+    return group, max(1, per // 4)
 
 
 def band_pixel_rows(H: int, band: int, n_bands: int) -> range:

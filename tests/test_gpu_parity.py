@@ -413,6 +413,18 @@ def test_stream_wait_group_orders_frame_consumers():
     assert torch.equal(copies, r) and not torch.isnan(r).any()
     with pytest.raises(GsError):
         ctx.gs_stream_wait_group(side, 3)
+    # gs_stream_wait_view: the same per view (the gather chunks of the multi-GPU orbit)
+    r.fill_(float("nan"))
+    copies.fill_(0.0)
+    ctx.gs_render_views(st, [camera(c) for c in cams], 256, 160, o, r, t)
+    for v in range(7):
+        ctx.gs_stream_wait_view(side, v)
+        with torch.cuda.stream(side):
+            copies[v].copy_(r[v])
+    torch.cuda.synchronize()
+    assert torch.equal(copies, r) and not torch.isnan(r).any()
+    with pytest.raises(GsError):
+        ctx.gs_stream_wait_view(side, 7)
     ctx.close()
 
 
@@ -742,3 +754,82 @@ def test_degenerate_image_and_scene_sizes(wh, n):
             _, _, ref = oracle.render(scene, cam, bg, obox=obox)
             check_frame(f"degenerate/{W}x{H}/n{n}/{'obox' if obox else 'vanilla'}/{['tc', 'direct', 'mma'][blend]}",
                         rgb, T, ref)
+
+
+def test_single_view_calls_interleaved_with_static_scene_view_groups():
+    """gs_render (the context's own workspace, caller's stream) enqueued back to back with
+    gs_render_views under GS_FLAG_STATIC_SCENE (whose preprocess does not wait for the
+    caller's earlier work): the two share no buffer, so every frame equals its reference."""
+    import torch
+    from paper_2604_02120_b200 import GS_FLAG_STATIC_SCENE, Context, camera, opts, scene_to_device
+    scene = synth.unbounded_scene(200000, 115, sh_degree=3)
+    cams = synth.orbit_cameras(6, 640, 360, 1.0)
+    ctx = Context(0, max_points=scene.n, max_keys=1 << 23, max_w=640, max_h=360)
+    ctx.gs_set_view_group(4, True)
+    st = scene_to_device(scene)
+    o = opts((0.1, 0.2, 0.3), sh_degree=3)
+    ref_r, ref_t = [], []
+    for c in cams:
+        r = torch.empty((3, 360, 640), device="cuda")
+        t = torch.empty((360, 640), device="cuda")
+        ctx.gs_render(st, camera(c), 640, 360, o, r, t)
+        torch.cuda.synchronize()
+        ref_r.append(r.cpu())
+        ref_t.append(t.cpu())
+    o_s = opts((0.1, 0.2, 0.3), sh_degree=3, flags=GS_FLAG_STATIC_SCENE)
+    outs = []
+    for it in range(3):
+        r1 = torch.full((3, 360, 640), float("nan"), device="cuda")
+        t1 = torch.full((360, 640), float("nan"), device="cuda")
+        rv = torch.full((5, 3, 360, 640), float("nan"), device="cuda")
+        tv = torch.full((5, 360, 640), float("nan"), device="cuda")
+        ctx.gs_render(st, camera(cams[0]), 640, 360, o, r1, t1)
+        ctx.gs_render_views(st, [camera(c) for c in cams[1:]], 640, 360, o_s, rv, tv)
+        outs.append((r1, t1, rv, tv))
+    torch.cuda.synchronize()
+    for r1, t1, rv, tv in outs:
+        assert torch.equal(r1.cpu(), ref_r[0]) and torch.equal(t1.cpu(), ref_t[0])
+        for v in range(5):
+            assert torch.equal(rv[v].cpu(), ref_r[v + 1]) and torch.equal(tv[v].cpu(), ref_t[v + 1])
+    ctx.close()
+
+
+def test_workspace_allocation_failure_leaves_the_context_usable():
+    """A view group whose per-view workspaces do not fit in HBM fails with GS_ERR_CUDA
+    (no crash, nothing half-allocated); the context then still renders correct frames."""
+    import torch
+    from paper_2604_02120_b200 import GS_ERR_CUDA, Context, camera, opts, scene_to_device
+    scene = synth.object_scene(20000, 116, sh_degree=1)
+    cams = synth.orbit_cameras(3, 160, 96, 1.0)
+    free, _ = torch.cuda.mem_get_info()
+    # a max_keys whose workspace (16 B per key) takes about a fifth of the free memory:
+    # 16 views x 2 slot sets cannot all be allocated
+    max_keys = min((1 << 32) - 1, int(free * 0.2 / 17))
+    ctx = Context(0, max_points=scene.n, max_keys=max_keys, max_w=160, max_h=96)
+    st = scene_to_device(scene)
+    o = opts((0.0, 0.0, 0.0), sh_degree=1)
+    ref = []
+    for c in cams:
+        r = torch.empty((3, 96, 160), device="cuda")
+        t = torch.empty((96, 160), device="cuda")
+        ctx.gs_render(st, camera(c), 160, 96, o, r, t)
+        ref.append(r.cpu())
+    ctx.gs_set_view_group(16, True)
+    rv = torch.empty((3 * 8, 3, 96, 160), device="cuda")
+    tv = torch.empty((3 * 8, 96, 160), device="cuda")
+    with pytest.raises(GsError) as e:
+        ctx.gs_render_views(st, [camera(c) for c in cams] * 8, 160, 96, o, rv, tv)
+    assert e.value.code == GS_ERR_CUDA
+    torch.cuda.synchronize()
+    ctx.gs_set_view_group(2, False)        # the slots of set 0 that did get allocated
+    rv.fill_(float("nan"))
+    ctx.gs_render_views(st, [camera(c) for c in cams], 160, 96, o, rv[:3], tv[:3])
+    torch.cuda.synchronize()
+    for v in range(3):
+        assert torch.equal(rv[v].cpu(), ref[v])
+    r = torch.empty((3, 96, 160), device="cuda")
+    t = torch.empty((96, 160), device="cuda")
+    ctx.gs_render(st, camera(cams[1]), 160, 96, o, r, t)
+    torch.cuda.synchronize()
+    assert torch.equal(r.cpu(), ref[1])
+    ctx.close()

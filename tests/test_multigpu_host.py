@@ -8,7 +8,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2604_02120_b200.orbit import (band_pixel_rows, gather_bands, gather_frames, gather_frames_pipelined,
-                                         partition_views)
+                                         gather_plan, partition_views)
 
 
 def test_partition_covers_views_once():
@@ -17,6 +17,13 @@ def test_partition_covers_views_once():
         assert seen == list(range(64))
     with pytest.raises(ValueError):
         partition_views(64, 3, 0)
+
+
+def test_gather_plan():
+    """One preprocess launch per rank and step while the block fits a view group (16),
+    gather chunks of a quarter block: N = 1, 2, 4, 8 ranks of the 64-view orbit."""
+    assert [gather_plan(64 // n) for n in (1, 2, 4, 8)] == [(16, 16), (16, 8), (16, 4), (8, 2)]
+    assert gather_plan(1) == (1, 1) and gather_plan(3) == (3, 1)
 
 
 def _free_port():
@@ -49,7 +56,7 @@ def _worker(rank, world, port, q):
     if rank == 0:
         assert torch.equal(brgb, yy.expand(3, Hv, Wv)) and torch.equal(bT, -yy)
     a, b = gather_frames(rgb, T, world, rank)
-    # the group-pipelined gather (views in groups of 3: a ragged last group)
+    # the chunk-pipelined gather (chunks of 3 views: a ragged last chunk)
     c, d = gather_frames_pipelined(rgb, T, world, rank, 3)
     if rank == 0:
         assert torch.equal(a, c) and torch.equal(b, d)
