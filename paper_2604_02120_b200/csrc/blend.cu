@@ -31,6 +31,8 @@
 // x_bar = x_c - x_p (Eq. 4; reading R-7).
 #include <algorithm>
 
+#include <cuda.h>   // CUtensorMap (the TMA descriptors of the frame stores)
+
 #include "gs_common.cuh"
 
 namespace gs {
@@ -90,12 +92,16 @@ static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0 && GS_BLEND_
 // Header: {tile, seq, count, list offset}; count 0 = end-of-tile marker,
 // count -1 = batch of an already terminated tile (skipped), tile -1 = terminal.
 
-struct RawRec {        // one gathered Gaussian (cp.async destinations)
-    float2 m;          // projected mean
-    float2 pad;
-    float4 co;         // (A, B, C, opacity)
-    float4 col;        // (r, g, b, 0)
-};
+#ifndef GS_BLEND_BULK
+#define GS_BLEND_BULK 1   // 1: one cp.async.bulk (TMA engine, UBLKCP) per 48-B record; 0: three cp.async (LDGSTS)
+#endif
+using RawRec = Splat;   // one gathered Gaussian: the preprocess's 48-B record, copied as is
+#ifndef GS_BLEND_TMA_STORE
+#define GS_BLEND_TMA_STORE 1   // 1: frames leave through a TMA tensor store per tile (UTMASTG); 0: per-thread stores
+#endif
+#if GS_BLEND_TMA_STORE && !GS_BLEND_NAMED_WAIT
+#error "the TMA store epilogue relies on the per-batch named barrier of the compositors"
+#endif
 
 struct __align__(1024) SmemTC {
     uint8_t A[2][128 * 64];       // M_p halves: 128 rows x 16 tf32, interleaved core matrices
@@ -111,6 +117,9 @@ struct __align__(1024) SmemTC {
     uint64_t raw_empty[RAW];      // builder -> producer
     uint32_t tmem_base;
     uint32_t warp_done_seq[NCW];
+#if GS_BLEND_TMA_STORE
+    float outb[2][4][GS_TILE_PIX];   // finished tile (R, G, B, T planes, row-major 16 x 16), double-buffered
+#endif
 };
 
 // byte offset of (row r, 16-byte K-chunk c) in a K-major no-swizzle operand
@@ -139,25 +148,6 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[32]) { tmem_ld32(taddr, v); }
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[16]) { tmem_ld16(taddr, v); }
-
-struct Rec {
-    float2 m;     // projected mean
-    float4 co;    // (A, B, C, opacity)
-    float4 col;   // (r, g, b, 0)
-};
-
-__device__ __forceinline__ void gather(Rec &r, const float2 *__restrict__ xy, const float4 *__restrict__ conic_o,
-                                       const float4 *__restrict__ rgb, uint32_t gi, bool ok) {
-    if (ok) {
-        r.m = __ldg(xy + gi);
-        r.co = __ldg(conic_o + gi);
-        r.col = __ldg(rgb + gi);
-    } else {
-        r.m = make_float2(0.f, 0.f);
-        r.co = make_float4(0.f, 0.f, 0.f, 1.f);
-        r.col = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-}
 
 __device__ __forceinline__ bool tile_done(const SmemTC &sm, int lane, uint32_t seq) {
     const uint32_t dseq = lane < NCW ? *((volatile const uint32_t *)&sm.warp_done_seq[lane]) : seq;
@@ -209,11 +199,11 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
 
 template <bool DUMP, bool STATS, bool TRACE>
 __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
-    k_blend_tc(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
-               const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
+    k_blend_tc(const Splat *__restrict__ splat, const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
                int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
-               unsigned long long *stat_kept, long long *trace) {
+               unsigned long long *stat_kept, long long *trace, const __grid_constant__ CUtensorMap tm_rgb,
+               const __grid_constant__ CUtensorMap tm_T, int tma_out) {
     extern __shared__ uint8_t smem_raw[];
     SmemTC &sm = *reinterpret_cast<SmemTC *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -226,7 +216,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         }
         for (int r = 0; r < RING; r++) mbar_init(&sm.slot_ready[r], 1);
         for (int r = 0; r < RAW; r++) {
-            mbar_init(&sm.raw_full[r], 33);      // 32 cp.async completions (noinc) + header
+            mbar_init(&sm.raw_full[r], GS_BLEND_BULK ? 1 : 33);   // header arrive (+ expect_tx) | 32 cp.async + header
             mbar_init(&sm.raw_empty[r], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -305,12 +295,24 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             TRACE_EV(0, b_idx);
             mbar_wait(&sm.raw_empty[r], ((b_idx / RAW) & 1u) ^ 1u);
             TRACE_EV(1, b_idx);
+#if GS_BLEND_BULK
+            // the header arrives with the batch's byte count; each lane's bulk copy of its
+            // 48-B record completes its share of the transaction bytes (the phase completes
+            // when all have landed)
+            if (lane == 0) {
+                sm.raw_hdr[r] = hd;
+                mbar_arrive_expect_tx(&sm.raw_full[r], hd.z > 0 ? (uint32_t)hd.z * (uint32_t)sizeof(Splat) : 0u);
+            }
+            __syncwarp();
+            if (lane < hd.z) bulk_g2s(&sm.raw[r][lane], splat + gi, (uint32_t)sizeof(Splat), &sm.raw_full[r]);
+#else
             if (lane < hd.z) {
                 RawRec &d = sm.raw[r][lane];
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&d.m)), "l"(xy + gi) : "memory");
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.co)), "l"(conic_o + gi)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.m)), "l"(&splat[gi].m)
                              : "memory");
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.col)), "l"(rgb + gi)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.co)), "l"(&splat[gi].co)
+                             : "memory");
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&d.col)), "l"(&splat[gi].col)
                              : "memory");
             }
             if (lane == 0) {
@@ -319,6 +321,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.raw_full[r]))
                          : "memory");
+#endif
             b_idx++;
         };
         for (;;) {
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         // pixel has stopped (R-2), so "live" is a single compare and no bool is carried.
         float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
         bool wdone = false;
-        uint32_t n_kept = 0;
+        uint32_t n_kept = 0, n_tiles = 0;
         for (uint32_t k = 0;; k++) {
             const int s = k % STAGES;
             const int c_slot = k % RING;
@@ -446,6 +449,32 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                     }
                     break;
                 }
+#if GS_BLEND_TMA_STORE
+                if (!DUMP && tma_out) {
+                    // a9 through the TMA engine: the tile's four planes go to shared memory,
+                    // then ONE thread stores them with two tensor copies (3-D RGB box, 2-D T
+                    // box) that clip the frame edge themselves. Double-buffered: the store of
+                    // the tile before last must have read its buffer (wait_group.read 1), which
+                    // thread 0 checked right after issuing the previous tile's store, before
+                    // it joined this tile's batch barriers.
+                    float *ob = &sm.outb[n_tiles & 1][0][0];
+                    const int pi = y * GS_TILE + x;
+                    ob[pi] = C0 + T * bg0;
+                    ob[GS_TILE_PIX + pi] = C1 + T * bg1;
+                    ob[2 * GS_TILE_PIX + pi] = C2 + T * bg2;
+                    ob[3 * GS_TILE_PIX + pi] = T;
+                    fence_proxy_async_smem();
+                    asm volatile("bar.sync 2, 256;" ::: "memory");
+                    if (threadIdx.x == 0) {
+                        const int x0 = GS_TILE * (hd.x % gx), y0 = GS_TILE * (hd.x / gx);
+                        tma_store_3d(&tm_rgb, ob, x0, y0, 0);
+                        tma_store_2d(&tm_T, ob + 3 * GS_TILE_PIX, x0, y0);
+                        bulk_commit_group();
+                        bulk_wait_group_read1();
+                    }
+                    n_tiles++;
+                } else
+#endif
                 if (!DUMP) {
                     const int px = GS_TILE * (hd.x % gx) + x, py = GS_TILE * (hd.x / gx) + y;
                     if (px < W && py < H) {
@@ -506,6 +535,9 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             if (lane == 0) mbar_arrive(&sm.empty[s]);
         }
     }
+#if GS_BLEND_TMA_STORE
+    if (threadIdx.x == 0 && tma_out) bulk_wait_group_all();   // the last stores complete before the CTA exits
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == WARP_TMEM) {
@@ -516,8 +548,45 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
 
 long long *g_blend_trace = nullptr;   // set by gs_debug_set_trace (debug only)
 
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
+// TMA descriptors of a frame: RGB planes as a 3-D tensor {W, H, 3} with 16 x 16 x 3 boxes,
+// T as a 2-D tensor {W, H} with 16 x 16 boxes (row pitch W floats). cuTensorMapEncodeTiled
+// comes from the driver through the runtime's entry-point query (no libcuda link). False
+// when the layout does not allow a tensor map (row pitch or base not 16-B aligned): the
+// kernel then stores per thread.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool frame_tensor_maps(float *out_rgb, float *out_T, int W, int H, CUtensorMap &m_rgb, CUtensorMap &m_T) {
+    static EncodeTiledFn encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<EncodeTiledFn>(fn);
+        else
+            cudaGetLastError();
+    }
+    if (!encode || !out_rgb || !out_T || (W & 3) || (reinterpret_cast<uintptr_t>(out_rgb) & 15) ||
+        (reinterpret_cast<uintptr_t>(out_T) & 15))
+        return false;
+    const cuuint64_t dims3[3] = {(cuuint64_t)W, (cuuint64_t)H, 3};
+    const cuuint64_t str3[2] = {(cuuint64_t)W * 4, (cuuint64_t)W * H * 4};
+    const cuuint32_t box3[3] = {GS_TILE, GS_TILE, 3}, es3[3] = {1, 1, 1};
+    const cuuint64_t dims2[2] = {(cuuint64_t)W, (cuuint64_t)H};
+    const cuuint64_t str2[1] = {(cuuint64_t)W * 4};
+    const cuuint32_t box2[2] = {GS_TILE, GS_TILE}, es2[2] = {1, 1};
+    return encode(&m_rgb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out_rgb, dims3, str3, box3, es3,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           encode(&m_T, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out_T, dims2, str2, box2, es2,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats) {
     const size_t smem = sizeof(SmemTC) + 1024;
@@ -532,15 +601,17 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
     const int grid = std::max(1, std::min(GS_BLEND_MINB * num_sms, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
-#define ARGS xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
+    CUtensorMap m_rgb{}, m_T{};
+    const int tma = (GS_BLEND_TMA_STORE && !dump_m && frame_tensor_maps(out_rgb, out_T, W, H, m_rgb, m_T)) ? 1 : 0;
+#define ARGS splat, vals, ranges, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
-        launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
+        launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
     else if (stats)
-        launch_pdl(k_blend_tc<false, true, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
+        launch_pdl(k_blend_tc<false, true, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
     else if (g_blend_trace)
-        launch_pdl(k_blend_tc<false, false, true>, grid, TC_THREADS, smem, st, ARGS, g_blend_trace);
+        launch_pdl(k_blend_tc<false, false, true>, grid, TC_THREADS, smem, st, ARGS, g_blend_trace, m_rgb, m_T, tma);
     else
-        launch_pdl(k_blend_tc<false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr);
+        launch_pdl(k_blend_tc<false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
 #undef ARGS
 }
 
@@ -548,8 +619,7 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, con
 // CUDA-core direct blend (Alg. 1 with Eq. 3 per pixel): one 256-thread CTA per
 // tile, batches of 256 Gaussians staged in shared memory.
 // ===========================================================================
-__global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o,
-                                                      const float4 *__restrict__ rgb, const uint32_t *__restrict__ vals,
+__global__ void __launch_bounds__(256) k_blend_direct(const Splat *__restrict__ splat, const uint32_t *__restrict__ vals,
                                                       const uint2 *__restrict__ ranges, int tile0, int gx, int W, int H,
                                                       float bg0, float bg1, float bg2, float *__restrict__ out_rgb,
                                                       float *__restrict__ out_T) {
@@ -571,11 +641,11 @@ __global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__
         const uint32_t cnt = min(256u, rg.y - b0);
         if ((uint32_t)p < cnt) {
             const uint32_t gi = vals[b0 + p];
-            const float2 m = xy[gi];
-            const float4 co = conic_o[gi];
+            const float2 m = splat[gi].m;
+            const float4 co = splat[gi].co;
             s_g[p] = make_float4(m.x, m.y, co.x, co.y);
             s_g2[p] = make_float2(co.z, lg2_approx(co.w));
-            s_c[p] = rgb[gi];
+            s_c[p] = splat[gi].col;
         }
         __syncthreads();
         for (uint32_t j = 0; j < cnt && !done; j++) {
@@ -603,11 +673,10 @@ __global__ void __launch_bounds__(256) k_blend_direct(const float2 *__restrict__
     }
 }
 
-void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
+void launch_blend_direct(cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *) {
     if (ntiles - tile0 <= 0) return;
-    launch_pdl(k_blend_direct, ntiles - tile0, 256, 0, st, xy, conic_o, rgb, vals, ranges, tile0, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
+    launch_pdl(k_blend_direct, ntiles - tile0, 256, 0, st, splat, vals, ranges, tile0, gx, W, H, bg[0], bg[1], bg[2], out_rgb,
                                            out_T);
 }
 
@@ -669,8 +738,7 @@ __device__ __forceinline__ uint32_t mp_word(int x, int y, int k) {
 #endif
 template <int BATCH>
 __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
-    k_blend_mma(const float2 *__restrict__ xy, const float4 *__restrict__ conic_o, const float4 *__restrict__ rgb,
-                const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
+    k_blend_mma(const Splat *__restrict__ splat, const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
                 int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                 uint32_t *tile_queue) {
     extern __shared__ uint8_t smem_raw[];
@@ -712,9 +780,9 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
         auto fetch = [&](uint32_t b) {
             if (threadIdx.x < BATCH && b + threadIdx.x < rg.y) {
                 const uint32_t gi = vals[b + threadIdx.x];
-                pm = xy[gi];
-                pco = conic_o[gi];
-                pcol = rgb[gi];
+                pm = splat[gi].m;
+                pco = splat[gi].co;
+                pcol = splat[gi].col;
             }
         };
         fetch(rg.x);
@@ -824,8 +892,7 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
 }
 
 template <int BATCH>
-static void launch_mma_b(cudaStream_t st, int grid, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
+static void launch_mma_b(cudaStream_t st, int grid, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, uint32_t *queue) {
     const size_t smem = sizeof(SmemMMA<BATCH>) + 128;
     static bool attr = false;
@@ -833,21 +900,20 @@ static void launch_mma_b(cudaStream_t st, int grid, const float2 *xy, const floa
         cudaFuncSetAttribute(k_blend_mma<BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    launch_pdl(k_blend_mma<BATCH>, grid, MMA_THREADS, smem, st, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H,
+    launch_pdl(k_blend_mma<BATCH>, grid, MMA_THREADS, smem, st, splat, vals, ranges, tile0, ntiles, gx, W, H,
                bg[0], bg[1], bg[2], out_rgb, out_T, queue);
 }
 
-void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
+void launch_blend_mma(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
                       int W, int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch) {
     if (ntiles - tile0 <= 0) return;
     const int grid = std::max(1, std::min(GS_MMA_MINB * num_sms, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     switch (batch) {
-        case 32: launch_mma_b<32>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        case 64: launch_mma_b<64>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        case 128: launch_mma_b<128>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
-        default: launch_mma_b<256>(st, grid, xy, conic_o, rgb, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 32: launch_mma_b<32>(st, grid, splat, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 64: launch_mma_b<64>(st, grid, splat, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        case 128: launch_mma_b<128>(st, grid, splat, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
+        default: launch_mma_b<256>(st, grid, splat, vals, ranges, tile0, ntiles, gx, W, H, bg, out_rgb, out_T, queue); break;
     }
 }
 

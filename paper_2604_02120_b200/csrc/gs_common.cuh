@@ -36,6 +36,20 @@ struct Sticky {
 
 constexpr int MAX_TILES = 1 << 20;   // 16384 x 16384 px; one-level binning sorts ceil(tile bits / 8) passes
 
+// ---- the blend's per-Gaussian record ----------------------------------------
+// One 48-byte record per visible Gaussian (slot-addressed), written by the preprocess:
+// everything the blend reads of a Gaussian in one contiguous, 16-B aligned block, so
+// the tcgen05 blend's producer fetches it with ONE bulk copy (cp.async.bulk, the TMA
+// engine's 1-D form) straight into its shared-memory ring, and the other blends with
+// three vector loads from two 32-B sectors (the SoA form touched three).
+struct __align__(16) Splat {
+    float2 m;      // projected mean (pixels)
+    float2 aux;    // (0, 0): padding to the 16-B granule of the bulk copy
+    float4 co;     // (A, B, C, opacity): conic of Eq. 3 and opacity
+    float4 col;    // (r, g, b, 0): SH colour
+};
+static_assert(sizeof(Splat) == 48, "48-byte splat record");
+
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
     // per Gaussian SLOT (max_points): the preprocess packs the visible Gaussians of each
@@ -45,9 +59,7 @@ struct Workspace {
     uint32_t *wcount;          // [N/32+1] visible Gaussians per warp of 32
     uint32_t *orig;            // [N] Gaussian index of each used slot (debug outputs)
     uint32_t *depth_bits;      // [N] raw IEEE bits of the camera depth
-    float2 *xy;                // [N] projected mean (pixels)
-    float4 *conic_o;           // [N] (A, B, C, opacity)
-    float4 *rgb;               // [N] (r, g, b, 0)
+    Splat *splat;              // [N] what the blend reads: mean, conic + opacity, colour (48 B AoS)
     ushort4 *rect;             // [N] (xmin, ymin, xmax, ymax) tiles, half-open
     uint32_t *touched;         // [N] tiles touched (0 = culled); with GS_FLAG_TIGHT: tiles kept
     unsigned long long *tmask; // [N] GS_FLAG_TIGHT: kept tiles of the rect (bit ty*w+tx), ~0 = all
@@ -91,9 +103,7 @@ struct PreOut {
     uint32_t *wcount;
     uint32_t *orig;
     uint32_t *depth_bits;
-    float2 *xy;
-    float4 *conic_o;
-    float4 *rgb;
+    Splat *splat;
     ushort4 *rect;
     uint32_t *touched;
     unsigned long long *tmask;
@@ -183,6 +193,36 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t cnt) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
 }
+// arrive (count 1) and raise the phase's expected transaction bytes by `bytes`
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 1-D bulk copy global -> shared by the TMA engine (SASS UBLKCP): `bytes` (multiple of 16,
+// both addresses 16-B aligned) land in dst, then complete `bytes` transaction bytes on bar
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// TMA tensor stores shared -> global (SASS UTMASTG), tracked by the issuing thread's bulk
+// async-groups; the source must be made visible to the async proxy first
+// (fence_proxy_async_smem + a barrier). Out-of-range box elements are not written.
+__device__ __forceinline__ void tma_store_3d(const void *tmap, const void *src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tmap),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const void *tmap, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all but the most recent group have finished READING their shared-memory source
+__device__ __forceinline__ void bulk_wait_group_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+// every group has completed (its global writes performed)
+__device__ __forceinline__ void bulk_wait_group_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // Waits for the phase with the given parity. The suspend-time hint lets a
 // waiting warp sleep in hardware until the phase completes instead of
 // spinning (spinning warps took a third of the blend's issue slots).
@@ -335,15 +375,12 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
                              int sh_stride, float scale_mod, int W, int H, int imode);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
                    uint32_t &epoch, bool tight, float znear, bool concurrent);
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                     const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats);
 extern long long *g_blend_trace;
-void launch_blend_mma(const Workspace &ws, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                      const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
+void launch_blend_mma(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
                       int W, int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch);
-void launch_blend_direct(cudaStream_t st, const float2 *xy, const float4 *conic_o, const float4 *rgb,
-                         const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
+void launch_blend_direct(cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W, int H,
                          const float bg[3], float *out_rgb, float *out_T, const Counters *counters);
 }  // namespace gs

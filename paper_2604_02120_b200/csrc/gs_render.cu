@@ -105,7 +105,7 @@ cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
 #define A(ptr, n) \
     if (e == cudaSuccess) e = alloc(ptr, n)
     A(w.wcount, N / 32 + 1); A(w.orig, N);
-    A(w.depth_bits, N); A(w.xy, N); A(w.conic_o, N); A(w.rgb, N); A(w.rect, N); A(w.touched, N);
+    A(w.depth_bits, N); A(w.splat, N); A(w.rect, N); A(w.touched, N);
     A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
     A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
     A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
@@ -113,11 +113,14 @@ cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
     A(w.counters, 1);
 #undef A
     if (e == cudaSuccess) e = cudaMemset(w.counters, 0, sizeof(gs::Counters));
+    // the compaction loads every slot's depth unconditionally (both loads in flight at
+    // once) and discards those of unused slots: defined contents keep initcheck clean
+    if (e == cudaSuccess) e = cudaMemset(w.depth_bits, 0, sizeof(uint32_t) * N);
     return e;
 }
 
 void free_ws(gs::Workspace &w) {
-    void *ptrs[] = {w.wcount, w.orig, w.tmask, w.tmask_r, w.depth_bits, w.xy, w.conic_o, w.rgb, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
+    void *ptrs[] = {w.wcount, w.orig, w.tmask, w.tmask_r, w.depth_bits, w.splat, w.rect, w.touched, w.radius, w.sk[0], w.sk[1],
                     w.sv[0], w.sv[1], w.off, w.rect_r, w.kt[0], w.kt[1], w.kv[0], w.kv[1], w.chunk_first,
                     w.ranges, w.sums, w.cmat, w.row_total, w.cdesc, w.cdesc_last, w.tile_cnt, w.rowinfo,
                     w.counters, w.stage};
@@ -225,21 +228,20 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
     return e2;
 }
 
-void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const float2 *xy, const float4 *conic_o,
-                   const float4 *rgb, const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o,
+void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const gs::Splat *splat, const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o,
                    float *out_rgb, float *out_T, float *dump) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     int y0 = 0, y1 = gy;   // the row band's tiles only (a split frame's other bands are untouched)
     gs::band_rows(gy, o.band, o.n_bands, y0, y1);
     const int t0 = y0 * gx, t1 = y1 * gx;
     if (o.blend == GS_BLEND_DIRECT && !dump)
-        gs::launch_blend_direct(st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_direct(st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                                 w.counters);
     else if (o.blend == GS_BLEND_MMA && !dump)
-        gs::launch_blend_mma(w, st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_mma(w, st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                              c->num_sms, o.batch);
     else
-        gs::launch_blend_tc(w, st, xy, conic_o, rgb, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_tc(w, st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                             dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
     c->launches += 1;
 }
@@ -261,12 +263,15 @@ int finish(gs_ctx *c, cudaStream_t st, const gs_opts &o, int64_t N) {
 
 // ---- small packing kernels for the debug / split entry points ------------
 __global__ void k_pack_splats(int N, const float *xy, const float *conic, const float *opacity, const float *rgb,
-                              float2 *oxy, float4 *oco, float4 *orgb) {
+                              gs::Splat *out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    oxy[i] = make_float2(xy[2 * i], xy[2 * i + 1]);
-    oco[i] = make_float4(conic[3 * i], conic[3 * i + 1], conic[3 * i + 2], opacity[i]);
-    if (rgb) orgb[i] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
+    gs::Splat s;
+    s.m = make_float2(xy[2 * i], xy[2 * i + 1]);
+    s.aux = make_float2(0.f, 0.f);
+    s.co = make_float4(conic[3 * i], conic[3 * i + 1], conic[3 * i + 2], opacity[i]);
+    s.col = rgb ? make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    out[i] = s;
 }
 
 // debug preprocess: scatter the slot-addressed outputs back to Gaussian order (the
@@ -277,11 +282,12 @@ __global__ void k_unpack_pre(int N, gs::Workspace ws, float *depth, float *xy, f
     if (s >= N || (uint32_t)(s & 31) >= ws.wcount[s >> 5]) return;
     const uint32_t i = ws.orig[s];
     depth[i] = __uint_as_float(ws.depth_bits[s]);
-    xy[2 * i] = ws.xy[s].x;
-    xy[2 * i + 1] = ws.xy[s].y;
-    const float4 co = ws.conic_o[s];
+    const gs::Splat sp = ws.splat[s];
+    xy[2 * i] = sp.m.x;
+    xy[2 * i + 1] = sp.m.y;
+    const float4 co = sp.co;
     conic[3 * i] = co.x; conic[3 * i + 1] = co.y; conic[3 * i + 2] = co.z;
-    const float4 c = ws.rgb[s];
+    const float4 c = sp.col;
     rgb[3 * i] = c.x; rgb[3 * i + 1] = c.y; rgb[3 * i + 2] = c.z;
     const ushort4 r = ws.rect[s];
     rect[4 * i] = r.x; rect[4 * i + 1] = r.y; rect[4 * i + 2] = r.z; rect[4 * i + 3] = r.w;
@@ -409,7 +415,7 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int e2 = enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
-    enqueue_blend(c, c->ws, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb,
+    enqueue_blend(c, c->ws, st, c->ws.splat, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb,
                   out_T, nullptr);
     const int e3 = mark(c, st, *o);
     span(c, 2, e2, e3);
@@ -565,7 +571,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                 cudaStreamWaitEvent(bl, c->ev_binned[set][j], 0);
                 if (hk && hk->pre_blend) hk->pre_blend(hk->user, bl, v0 + j);
                 const int e1 = mark(c, bl, o);
-                enqueue_blend(c, *w[j], bl, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H,
+                enqueue_blend(c, *w[j], bl, w[j]->splat, w[j]->kv[0], w[j]->ranges, W, H,
                               o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
                 const int e2 = mark(c, bl, o);
                 if (hk && hk->post_blend) hk->post_blend(hk->user, bl, v0 + j);
@@ -582,7 +588,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
             if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, v0 + j);
             const int e1 = mark(c, st, o);
-            enqueue_blend(c, *w[j], st, w[j]->xy, w[j]->conic_o, w[j]->rgb, w[j]->kv[0], w[j]->ranges, W, H, o,
+            enqueue_blend(c, *w[j], st, w[j]->splat, w[j]->kv[0], w[j]->ranges, W, H, o,
                           rgb_of[v0 + j], T_of[v0 + j], nullptr);
             const int e2 = mark(c, st, o);
             if (hk && hk->post_blend) hk->post_blend(hk->user, st, v0 + j);
@@ -914,12 +920,11 @@ static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, c
     cudaMemsetAsync(c->ws.counters, 0, sizeof(gs::Counters), st);
     c->last_sticky = c->sticky;
     if (N > 0) {
-        k_pack_splats<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, xy, conic, opacity, rgb, c->ws.xy, c->ws.conic_o,
-                                                              c->ws.rgb);
+        k_pack_splats<<<gs::ceil_div_i(N, 256), 256, 0, st>>>(N, xy, conic, opacity, rgb, c->ws.splat);
         c->launches++;
     }
     c->last_counters = c->ws.counters;
-    enqueue_blend(c, c->ws, st, c->ws.xy, c->ws.conic_o, c->ws.rgb, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
+    enqueue_blend(c, c->ws, st, c->ws.splat, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
                   *o, out_rgb, out_T, dump);
     return finish(c, st, *o, N);
 }

@@ -338,9 +338,12 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         // 12. outputs (slot-addressed)
         out.orig[slot] = (uint32_t)i;
         out.depth_bits[slot] = __float_as_uint(vz);
-        out.xy[slot] = make_float2(mx, my);
-        out.conic_o[slot] = make_float4(cA, cB, cC, op);
-        out.rgb[slot] = make_float4(col[0], col[1], col[2], 0.f);
+        {   // the blend's 48-B record: three 16-B stores
+            float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
+            d[0] = make_float4(mx, my, 0.f, 0.f);
+            d[1] = make_float4(cA, cB, cC, op);
+            d[2] = make_float4(col[0], col[1], col[2], 0.f);
+        }
         out.rect[slot] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
                                       (unsigned short)ymax);
         out.touched[slot] = n_tiles;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
 }
 
 PreOut pre_out_of(const Workspace &ws, bool with_radius) {
-    return PreOut{ws.wcount, ws.orig, ws.depth_bits, ws.xy, ws.conic_o, ws.rgb, ws.rect, ws.touched, ws.tmask,
+    return PreOut{ws.wcount, ws.orig, ws.depth_bits, ws.splat, ws.rect, ws.touched, ws.tmask,
                   with_radius ? ws.radius : nullptr, ws.counters};
 }
 
