@@ -99,12 +99,13 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
 // ---------------------------------------------------------------------------
 // element counts (device-resident)
 // ---------------------------------------------------------------------------
-enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2, CNT_RENT = 3, CNT_VISIBLE_WIDE = 4 };
+enum : int { CNT_POINTS = 0, CNT_VISIBLE = 1, CNT_KEYS = 2, CNT_RENT = 3, CNT_VISIBLE_WIDE = 4, CNT_SPAIRS = 5 };
 __device__ __forceinline__ uint32_t count_of(const Counters *c, int which, uint32_t n_points, uint64_t max_keys) {
     if (which == CNT_POINTS) return n_points;
     if (which == CNT_VISIBLE) return c->n_visible;
     if (which == CNT_VISIBLE_WIDE) return c->wide_depth ? c->n_visible : 0u;   // 4th depth pass only if needed
     if (which == CNT_RENT) return c->err ? 0u : c->n_rent;   // > max_keys sets err
+    if (which == CNT_SPAIRS) return c->err ? 0u : c->n_spairs;   // K > max_keys sets err
     const uint64_t k = c->n_keys;
     return c->err ? 0u : (uint32_t)(k < max_keys ? k : max_keys);
 }
@@ -122,6 +123,7 @@ struct CompactOp {   // used slots -> (depth key, slot) of the visible Gaussians
     Counters *cnt;
     uint32_t dbase;   // bits(znear) if znear > 0, else 0 (raw bits, always 4 passes)
     static constexpr int WHICH = CNT_POINTS;
+    static constexpr bool SIDE = false;
     struct Aux {
         uint32_t depth;
     };
@@ -148,6 +150,7 @@ struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ chunk he
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
+    static constexpr bool SIDE = false;
     struct Aux {};
     __device__ uint32_t load(uint32_t r) const { return touched[sorted_idx[r]]; }
     __device__ uint32_t load(uint32_t r, Aux &) const { return touched[sorted_idx[r]]; }
@@ -164,27 +167,40 @@ struct OffsetsOp {   // tiles_touched in depth order -> pair offsets (+ chunk he
 };
 
 template <class Op>
-__global__ void GS_SCAN_BOUNDS k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums) {
+__global__ void GS_SCAN_BOUNDS k_scan_reduce(Op op, uint32_t n_points, uint32_t *sums, uint32_t *sums2) {
     pdl_wait();
-    __shared__ uint32_t s_w[NWARP];
+    __shared__ uint32_t s_w[NWARP], s_w2[NWARP];
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        uint32_t acc = 0;
+        uint32_t acc = 0, acc2 = 0;
 #pragma unroll
         for (int r = 0; r < SORT_ITEMS; r++) {
             const uint32_t e = c * SORT_CHUNK + elem_of(warp, r, lane);
-            if (e < n) acc += op.load(e);
+            if (e < n) {
+                acc += op.load(e);
+                if constexpr (Op::SIDE) acc2 += op.side(e);
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) s_w[warp] = acc;
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if constexpr (Op::SIDE) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+        }
+        if (lane == 0) {
+            s_w[warp] = acc;
+            s_w2[warp] = acc2;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < NWARP; w++) t += s_w[w];
+            uint32_t t = 0, t2 = 0;
+            for (int w = 0; w < NWARP; w++) {
+                t += s_w[w];
+                t2 += s_w2[w];
+            }
             sums[c] = t;
+            if constexpr (Op::SIDE) sums2[c] = t2;
         }
         __syncthreads();
     }
@@ -195,10 +211,10 @@ __global__ void GS_SCAN_BOUNDS k_scan_reduce(Op op, uint32_t n_points, uint32_t 
 // single-block scan of the sums, one launch and one dependency fewer); the block of
 // the last chunk also reports the total (op.finish).
 template <class Op>
-__global__ void GS_SCAN_BOUNDS k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums) {
+__global__ void GS_SCAN_BOUNDS k_scan_apply(Op op, uint32_t n_points, const uint32_t *sums, const uint32_t *sums2) {
     pdl_wait();
     __shared__ uint32_t s_w[NWARP];
-    __shared__ unsigned long long s_pre[NWARP], s_tot[NWARP], s_base;
+    __shared__ unsigned long long s_pre[NWARP], s_tot[NWARP], s_tot2[NWARP], s_base;
     const uint32_t n = count_of(op.cnt, Op::WHICH, n_points, 0);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -213,30 +229,39 @@ __global__ void GS_SCAN_BOUNDS k_scan_apply(Op op, uint32_t n_points, const uint
         // (the element loads above are in flight meanwhile)
         {   // prefix of the chunk sums before c (and, for the last chunk, the total)
             const bool last = c + 1 == nchunks;
-            unsigned long long acc = 0, tot = 0;
+            unsigned long long acc = 0, tot = 0, tot2 = 0;
             for (uint32_t k = threadIdx.x; k < (last ? nchunks : c); k += SORT_THREADS) {
                 const unsigned long long x = sums[k];
                 if (k < c) acc += x;
                 tot += x;
+                if constexpr (Op::SIDE) {
+                    if (last) tot2 += sums2[k];
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                if constexpr (Op::SIDE) tot2 += __shfl_xor_sync(0xffffffffu, tot2, o);
             }
             if (lane == 0) {
                 s_pre[warp] = acc;
                 s_tot[warp] = tot;
+                s_tot2[warp] = tot2;
             }
             __syncthreads();
             if (threadIdx.x == 0) {
-                unsigned long long p = 0, t = 0;
+                unsigned long long p = 0, t = 0, t2 = 0;
                 for (int w = 0; w < NWARP; w++) {
                     p += s_pre[w];
                     t += s_tot[w];
+                    t2 += s_tot2[w];
                 }
                 s_base = p;
-                if (last) op.finish(t);
+                if (last) {
+                    if constexpr (Op::SIDE) op.finish(t, t2);
+                    else op.finish(t);
+                }
             }
             __syncthreads();
         }
@@ -687,22 +712,23 @@ __global__ void __launch_bounds__(SORT_THREADS, Loader::PACKED ? GS_SCATTER_MINB
 // ---------------------------------------------------------------------------
 // tile ranges: boundary detection over the sorted tile ids
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ tiles, const Counters *cnt,
-                                                uint64_t max_keys, uint2 *ranges) {
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t *__restrict__ keys, const Counters *cnt,
+                                                uint64_t max_keys, uint2 *ranges, int which, uint32_t kmask) {
     pdl_wait();
-    const uint32_t n = count_of(cnt, CNT_KEYS, 0, max_keys);
+    const uint32_t n = count_of(cnt, which, 0, max_keys);
+    auto tiles_at = [&](uint32_t k) { return keys[k] & kmask; };
     const uint32_t stride = gridDim.x * blockDim.x * 4;
     for (uint32_t k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4; k0 < n; k0 += stride) {
         uint32_t t[6];
-        t[0] = k0 > 0 ? tiles[k0 - 1] : 0xFFFFFFFFu;
+        t[0] = k0 > 0 ? tiles_at(k0 - 1) : 0xFFFFFFFFu;
         if (k0 + 4 <= n) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(tiles + k0);
-            t[1] = v.x; t[2] = v.y; t[3] = v.z; t[4] = v.w;
+            const uint4 v = *reinterpret_cast<const uint4 *>(keys + k0);
+            t[1] = v.x & kmask; t[2] = v.y & kmask; t[3] = v.z & kmask; t[4] = v.w & kmask;
         } else {
 #pragma unroll
-            for (int j = 0; j < 4; j++) t[1 + j] = k0 + j < n ? tiles[k0 + j] : 0xFFFFFFFFu;
+            for (int j = 0; j < 4; j++) t[1 + j] = k0 + j < n ? tiles_at(k0 + j) : 0xFFFFFFFFu;
         }
-        t[5] = k0 + 4 < n ? tiles[k0 + 4] : 0xFFFFFFFFu;
+        t[5] = k0 + 4 < n ? tiles_at(k0 + 4) : 0xFFFFFFFFu;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const uint32_t k = k0 + j;
@@ -747,6 +773,7 @@ struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry off
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_VISIBLE;
+    static constexpr bool SIDE = false;
     struct Aux {};   // emit re-reads (L1-hot): nothing is held across the scan, for occupancy
     __device__ uint32_t nrows(const ushort4 &rc, unsigned long long m, uint32_t &rows) const {
         if (!tmask_r) {
@@ -944,6 +971,7 @@ struct PairOffsetsOp {   // row entries in (ty, depth) order -> pair offsets (ru
     Counters *cnt;
     uint64_t max_keys;
     static constexpr int WHICH = CNT_RENT;
+    static constexpr bool SIDE = false;
     struct Aux {};
     __device__ uint32_t load(uint32_t e) const { return e_key[e] >> 18; }
     __device__ uint32_t load(uint32_t e, Aux &) const { return e_key[e] >> 18; }
@@ -1204,6 +1232,216 @@ __global__ void __launch_bounds__(512) k_tile_ranges(const uint32_t *__restrict_
     if (t < (uint32_t)gx) ranges[ty * gx + t] = n ? make_uint2(start, start + n) : make_uint2(0u, 0u);
 }
 
+
+// ---------------------------------------------------------------------------
+// Supertile binning (the tcgen05 blend's lists). A supertile is a block of
+// ST_SIDE x ST_SIDE tiles. The depth-ordered Gaussians are expanded to
+// (supertile, Gaussian) pairs -- one per supertile their rect overlaps, in
+// row-major order -- and ONE stable radix pass on the supertile id groups them:
+// each supertile's list is
+// in (depth, index) order (up to 512 supertiles, 9 bits: e.g. 1080p has 30 x 17;
+// larger grids take the per-tile two-level path). Each pair carries the 16-bit mask of the supertile's
+// tiles the Gaussian's rect (GS_FLAG_TIGHT: its kept tiles) covers, so a tile's
+// list (the pairs of that tile, sorted by depth) is its supertile's list
+// filtered by one mask bit; the blend's producer warp filters it on the fly.
+// Versus per-tile lists this sorts S ~ 0.31 K pairs once (C5: 5.4M vs 17.1M) and
+// skips the row pass, the pair offsets and the column pass; the blend reads ~5x
+// more list entries than it keeps, but only up to its tiles' termination (~12 %
+// of the lists at C5).
+// key = supertile id | mask << 16, value = Gaussian slot.
+// ---------------------------------------------------------------------------
+constexpr uint32_t ST_SIDE = 4;
+
+__device__ __forceinline__ uint32_t st_count(const ushort4 &rc) {
+    const uint32_t sx0 = rc.x / ST_SIDE, sx1 = (rc.z - 1u) / ST_SIDE + 1u;
+    const uint32_t sy0 = rc.y / ST_SIDE, sy1 = (rc.w - 1u) / ST_SIDE + 1u;
+    return (sx1 - sx0) * (sy1 - sy0);
+}
+
+// q / w for q < 2^24, w >= 1: float reciprocal estimate, corrected to the exact quotient
+__device__ __forceinline__ uint32_t udiv_small(uint32_t q, uint32_t w) {
+    uint32_t d = (uint32_t)((float)q * __frcp_rn((float)w));
+    if (d * w > q) d--;
+    else if ((d + 1) * w <= q) d++;
+    return d;
+}
+
+// tiles of supertile (sx, sy) that the rect [x0, x1) x [y0, y1) covers (bit 4 (ty % 4) + tx % 4);
+// with a GS_FLAG_TIGHT tile mask tm (bit (ty - y0) w + tx - x0 of the rect; ~0 = every tile,
+// also for rects of more than 64 tiles) only the kept ones
+__device__ __forceinline__ uint32_t st_mask(uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1, uint32_t sx,
+                                            uint32_t sy, unsigned long long tm) {
+    const uint32_t bx = ST_SIDE * sx, by = ST_SIDE * sy;
+    const uint32_t xb = max(x0, bx), xe = min(x1, bx + ST_SIDE), yb = max(y0, by), ye = min(y1, by + ST_SIDE);
+    const uint32_t w = x1 - x0;
+    if (tm == ~0ull || w * (y1 - y0) > 64u) {
+        const uint32_t cols = ((1u << (xe - xb)) - 1u) << (xb - bx);
+        return cols * ((0x1111u >> (4u * (ST_SIDE - (ye - yb)))) << (4u * (yb - by)));
+    }
+    uint32_t m = 0;
+    for (uint32_t ty = yb; ty < ye; ty++) {
+        const uint32_t bits = (uint32_t)(tm >> ((ty - y0) * w + (xb - x0))) & ((1u << (xe - xb)) - 1u);
+        m |= bits << (4u * (ty - by) + (xb - bx));
+    }
+    return m;
+}
+
+struct StOffsetsOp {   // supertiles per depth-ordered Gaussian -> pair offsets (+ chunk heads); side sum: K
+    const ushort4 *rect_r;                 // rects in depth order (gathered by the last depth pass)
+    const uint32_t *sorted_idx, *touched;  // GS_FLAG_TIGHT: K counts the kept tiles (touched)
+    bool tight;
+    uint32_t *soff, *chunk_first;
+    Counters *cnt;
+    uint64_t max_keys;
+    static constexpr int WHICH = CNT_VISIBLE;
+    static constexpr bool SIDE = true;
+    struct Aux {};
+    __device__ uint32_t load(uint32_t r) const { return st_count(rect_r[r]); }
+    __device__ uint32_t load(uint32_t r, Aux &) const { return load(r); }
+    __device__ uint32_t side(uint32_t r) const {
+        if (tight) return touched[sorted_idx[r]];
+        const ushort4 rc = rect_r[r];
+        return (uint32_t)(rc.z - rc.x) * (uint32_t)(rc.w - rc.y);
+    }
+    __device__ void emit(uint32_t r, uint64_t o, uint32_t v, const Aux &) const {
+        soff[r] = (uint32_t)(o < 0xFFFFFFFFull ? o : 0xFFFFFFFFull);
+        for (uint64_t c = (o + SORT_CHUNK - 1) / SORT_CHUNK; c * SORT_CHUNK < o + v; c++)
+            if (c * SORT_CHUNK < max_keys) chunk_first[c] = r;
+    }
+    __device__ void finish(uint64_t s_total, uint64_t k_total) const {
+        cnt->n_spairs = (uint32_t)(s_total < 0xFFFFFFFFull ? s_total : 0xFFFFFFFFull);
+        cnt->n_keys = k_total;   // K = the (Gaussian, tile) pairs, S <= K
+        if (k_total > max_keys) atomicOr(&cnt->err, 1u);
+    }
+};
+
+// Supertile pairs cbase .. cbase+cvalid-1: pair p belongs to the depth-ordered Gaussian r
+// with soff[r] <= p < soff[r+1] and is the (p - soff[r])-th supertile of its rect (row-major).
+struct StLoader : LinearChunks {
+    const uint32_t *soff, *chunk_first, *sorted_idx;
+    const ushort4 *rect_r;
+    const unsigned long long *tmask_r;   // GS_FLAG_TIGHT only
+    const Counters *cnt;
+    int sgx;
+    bool tight;
+    static constexpr bool EXPANDS = true;
+    static constexpr bool RUN_COUNTS = true;
+    static constexpr int SCRATCH_WORDS = 0;
+    __device__ void window(uint32_t c, uint32_t &r_lo, uint32_t &r_hi) const {
+        const uint32_t nv = cnt->n_visible;
+        const uint32_t nch = (cnt->n_spairs + SORT_CHUNK - 1) / SORT_CHUNK;
+        r_lo = chunk_first[c];
+        r_hi = c + 1 < nch ? min(nv - 1, chunk_first[c + 1]) : nv - 1;
+    }
+    // digit counts from runs: the Gaussian's supertiles in the chunk window are runs of
+    // consecutive ids, one per supertile row
+    __device__ void count_runs(uint32_t c, uint32_t cbase, uint32_t cvalid, int *s_diff) const {
+        uint32_t r_lo, r_hi;
+        window(c, r_lo, r_hi);
+        const uint32_t nv = cnt->n_visible, S = cnt->n_spairs, cend = cbase + cvalid;
+        for (uint32_t r0 = r_lo + threadIdx.x; r0 <= r_hi; r0 += COUNT_ILP * SORT_THREADS) {
+            uint32_t o[COUNT_ILP], o1[COUNT_ILP];
+            ushort4 rc[COUNT_ILP];
+#pragma unroll
+            for (int u = 0; u < COUNT_ILP; u++) {
+                const uint32_t r = r0 + (uint32_t)u * SORT_THREADS;
+                o[u] = o1[u] = 0;
+                rc[u] = make_ushort4(0, 0, 1, 1);
+                if (r <= r_hi) {
+                    o[u] = soff[r];
+                    o1[u] = r + 1 < nv ? soff[r + 1] : S;
+                    rc[u] = rect_r[r];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < COUNT_ILP; u++) {
+                const uint32_t q0 = o[u] < cbase ? cbase - o[u] : 0u;
+                if (o1[u] <= o[u] + q0) continue;
+                const uint32_t end = min(o1[u], cend) - o[u];
+                const uint32_t sx0 = rc[u].x / ST_SIDE, sy0 = rc[u].y / ST_SIDE;
+                const uint32_t sw = (rc[u].z - 1u) / ST_SIDE + 1u - sx0;
+                if (q0 == 0 && end == o1[u] - o[u]) {   // the whole rect in this chunk: one run per row
+                    const uint32_t sy1 = (rc[u].w - 1u) / ST_SIDE + 1u;
+                    for (uint32_t sy = sy0; sy < sy1; sy++) {
+                        const uint32_t d = sy * (uint32_t)sgx + sx0;
+                        atomicAdd(&s_diff[d], 1);
+                        atomicAdd(&s_diff[d + sw], -1);
+                    }
+                    continue;
+                }
+                for (uint32_t q = q0; q < end;) {
+                    const uint32_t qy = udiv_small(q, sw), qx = q - qy * sw;
+                    const uint32_t run = min(end - q, sw - qx);
+                    const uint32_t d = (sy0 + qy) * (uint32_t)sgx + sx0 + qx;   // < 512
+                    atomicAdd(&s_diff[d], 1);
+                    atomicAdd(&s_diff[d + run], -1);
+                    q += run;
+                }
+            }
+        }
+    }
+    __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
+        uint32_t r_lo, r_hi;
+        window(c, r_lo, r_hi);
+        const uint32_t nv = cnt->n_visible, S = cnt->n_spairs;
+        const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+        const uint32_t cend = cbase + cvalid;
+        for (uint32_t g0 = r_lo + 32u * warp; g0 <= r_hi; g0 += 32u * NWARP) {
+            const uint32_t r = g0 + lane;
+            uint32_t len = 0, q0 = 0, slot0 = 0, rxy = 0, rzw = 0, idx = 0;
+            unsigned long long m = ~0ull;
+            if (r <= r_hi) {
+                const uint32_t o = soff[r], o1 = r + 1 < nv ? soff[r + 1] : S;
+                const ushort4 rc = rect_r[r];
+                idx = sorted_idx[r];
+                if (tight) m = tmask_r[r];
+                rxy = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
+                rzw = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+                q0 = o < cbase ? cbase - o : 0u;
+                len = min(o1, cend) - (o + q0);
+                slot0 = o + q0 - cbase;
+            }
+            const uint32_t wslot = __shfl_sync(0xffffffffu, slot0, 0);
+            warp_expand(len, [&](bool valid, int owner, uint32_t j, uint32_t t) {
+                const uint32_t oq0 = __shfl_sync(0xffffffffu, q0, owner);
+                const uint32_t oxy = __shfl_sync(0xffffffffu, rxy, owner);
+                const uint32_t ozw = __shfl_sync(0xffffffffu, rzw, owner);
+                const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
+                unsigned long long om = ~0ull;
+                if (tight)
+                    om = ((unsigned long long)__shfl_sync(0xffffffffu, (uint32_t)(m >> 32), owner) << 32) |
+                         __shfl_sync(0xffffffffu, (uint32_t)m, owner);
+                if (!valid) return;
+                const uint32_t x0 = oxy & 0xFFFFu, y0 = oxy >> 16, x1 = ozw & 0xFFFFu, y1 = ozw >> 16;
+                const uint32_t sx0 = x0 / ST_SIDE, sy0 = y0 / ST_SIDE, sw = (x1 - 1u) / ST_SIDE + 1u - sx0;
+                const uint32_t q = oq0 + j, qy = udiv_small(q, sw);
+                const uint32_t sx = sx0 + (q - qy * sw), sy = sy0 + qy;
+                sk[wslot + t] = (sy * (uint32_t)sgx + sx) | (st_mask(x0, y0, x1, y1, sx, sy, om) << 16);
+                if (sv) sv[wslot + t] = oidx;
+            });
+        }
+    }
+};
+
+// one pass: the supertile ranges are the exclusive scan of the pass's digit totals
+__global__ void __launch_bounds__(512) k_st_ranges(const uint32_t *__restrict__ row_total, int nst, uint2 *ranges) {
+    pdl_wait();
+    __shared__ uint32_t s_w[16];
+    const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+    const uint32_t n = t < (uint32_t)nst ? row_total[t] : 0u;
+    uint32_t x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t b = 0;
+    for (uint32_t w = 0; w < warp; w++) b += s_w[w];
+    const uint32_t start = b + x - n;
+    if (t < (uint32_t)nst) ranges[t] = make_uint2(start, start + n);
+}
 // ---------------------------------------------------------------------------
 template <class Loader, int NDIG = 256>
 static void launch_count(const Workspace &ws, cudaStream_t st, int grid, Loader ld, int which, uint64_t mk,
@@ -1262,8 +1500,10 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
 
 template <class Op>
 static int scan_pass(const Workspace &ws, cudaStream_t st, int grid, Op op, uint32_t n_points) {
-    launch_pdl(k_scan_reduce<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
-    launch_pdl(k_scan_apply<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums);
+    uint32_t *sums2 = ws.sums + ws.max_chunks;   // side sums (Op::SIDE)
+    launch_pdl(k_scan_reduce<Op>, grid, SORT_THREADS, 0, st, op, n_points, ws.sums, sums2);
+    launch_pdl(k_scan_apply<Op>, grid, SORT_THREADS, 0, st, op, n_points, (const uint32_t *)ws.sums,
+               (const uint32_t *)sums2);
     return 2;
 }
 
@@ -1308,12 +1548,16 @@ __global__ void k_sticky(const Counters *cnt, Sticky *sticky) {
 }
 
 static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, bool tight,
-                        float znear, int grid_mult);
+                        float znear, int grid_mult, bool supertile);
+
+int supertile_count(int gx, int gy) {
+    return ceil_div_i(gx, (int)ST_SIDE) * ceil_div_i(gy, (int)ST_SIDE);
+}
 
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, uint32_t &,
-                   bool tight, float znear, bool concurrent) {
+                   bool tight, float znear, bool concurrent, bool supertile) {
     int launches = binning_body(ws, st, N, max_keys, ntiles, gx, tight, znear,
-                                concurrent ? GS_GRID_MULT_CONCURRENT : GS_GRID_MULT);
+                                concurrent ? GS_GRID_MULT_CONCURRENT : GS_GRID_MULT, supertile);
     if (ws.sticky) {
         launch_pdl(k_sticky, 1, 1, 0, st, (const Counters *)ws.counters, ws.sticky);
         launches++;
@@ -1322,7 +1566,7 @@ int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int 
 }
 
 static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx, bool tight,
-                        float znear, int grid_mult) {
+                        float znear, int grid_mult, bool supertile) {
     Counters *cnt = ws.counters;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -1331,7 +1575,9 @@ static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys,
     const int grid_k = std::max(1, std::min(nsm * grid_mult, ceil_div_i(max_keys, SORT_CHUNK)));
     const uint64_t mk = (uint64_t)max_keys;
     const int gy = ntiles / gx;
-    if (!(gx <= 512 && gy <= 512)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
+    const int nst = supertile_count(gx, gy);
+    supertile = supertile && nst <= 512;   // (the caller decides with the same rule)
+    if (!supertile && !(gx <= 512 && gy <= 512)) cudaMemsetAsync(ws.ranges, 0, sizeof(uint2) * (size_t)ntiles, st);
     int launches = 0;   // (the two-level path writes every tile range: no memset node)
     // 1. compaction of the visible Gaussians (index order), keys relative to the near plane
     uint32_t dbase = 0;
@@ -1359,6 +1605,22 @@ static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys,
     launch_pdl(k_depth_wide_copy, nsm * 2, 256, 0, st, (const Counters *)cnt, (const uint32_t *)ws.sv[1], ws.sv[0],
                (const ushort4 *)ws.rect, ws.rect_r, tm, ws.tmask_r);
     launches++;
+    if (supertile) {
+        // 3. supertile pairs per depth-ordered Gaussian (K on the side), 4. one stable pass on
+        //    the supertile id with the expansion fused in (final lists in kt[0] / kv[0]),
+        // 5. supertile ranges from the pass's digit totals
+        int sbits = 1;
+        while ((1 << sbits) < nst) sbits++;
+        launches += scan_pass(ws, st, grid_n,
+                              StOffsetsOp{ws.rect_r, ws.sv[0], ws.touched, tight, ws.off, ws.chunk_first, cnt, mk},
+                              (uint32_t)N);
+        launches += radix_pass(ws, st, grid_k,
+                               StLoader{{}, ws.off, ws.chunk_first, ws.sv[0], ws.rect_r, ws.tmask_r, cnt,
+                                        ceil_div_i(gx, (int)ST_SIDE), tight},
+                               ws.kt[0], ws.kv[0], CNT_SPAIRS, mk, 0, sbits);
+        launch_pdl(k_st_ranges, 1, 512, 0, st, (const uint32_t *)ws.row_total, nst, ws.ranges);
+        return launches + 1;
+    }
     int tbx = 0, tby = 0;
     while ((1 << tbx) < gx) tbx++;
     while ((1 << tby) < gy) tby++;
@@ -1412,7 +1674,8 @@ static int binning_body(Workspace &ws, cudaStream_t st, int N, int64_t max_keys,
         }
     }
     // 5. tile ranges
-    launch_pdl(k_ranges, nsm * 4, 256, 0, st, ws.kt[0], cnt, mk, ws.ranges);
+    launch_pdl(k_ranges, nsm * 4, 256, 0, st, (const uint32_t *)ws.kt[0], (const Counters *)cnt, mk, ws.ranges,
+               (int)CNT_KEYS, 0xFFFFFFFFu);
     return launches + 1;
 }
 

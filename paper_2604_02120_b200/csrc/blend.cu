@@ -47,9 +47,6 @@ namespace gs {
 #ifndef GS_BLEND_RAW
 #define GS_BLEND_RAW 2   // raw-record ring depth (sweep: 1 / 2 / 3 / 4 -> blend 0.267 / 0.270 / 0.274 / 0.279 ms per view)
 #endif
-#ifndef GS_BLEND_PF
-#define GS_BLEND_PF 2
-#endif
 #ifndef GS_BLEND_MINB
 #define GS_BLEND_MINB 4      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
 #endif
@@ -73,8 +70,12 @@ constexpr int STAGES = GS_BLEND_STAGES; // M_g / TMEM ring depth
 constexpr int NCW = 8;                  // compositor warps: 256 pixels
 constexpr int NBLD = GS_BLEND_NBLD;     // builder warps (alternate batches)
 constexpr int RAW = GS_BLEND_RAW;       // raw-record ring (producer -> builders): gathers in flight
-constexpr int PF = GS_BLEND_PF;         // index lookahead of the producer (batches)
 constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
+#ifndef GS_BLEND_LPF
+#define GS_BLEND_LPF 4
+#endif
+constexpr int LPF = GS_BLEND_LPF;  // list rounds (32 entries) the producer reads ahead
+constexpr int LQ = 64;             // producer queue of kept entries (>= NB + 32)
 // warp roles: 0..NCW-1 compositors, NCW producer, NCW+1.. builders (each also issues
 // the MMAs of the batches it built, and builder 0 owns the TMEM allocation)
 constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_TMEM = NCW + 1;
@@ -93,7 +94,9 @@ static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0 && GS_BLEND_
 // count -1 = batch of an already terminated tile (skipped), tile -1 = terminal.
 
 #ifndef GS_BLEND_BULK
-#define GS_BLEND_BULK 1   // 1: one cp.async.bulk (TMA engine, UBLKCP) per 48-B record; 0: three cp.async (LDGSTS)
+#define GS_BLEND_BULK 0   // 1: one cp.async.bulk (TMA engine, UBLKCP) per 48-B record; 0: three cp.async (LDGSTS).
+                          // A/B (profiles/r2_sweep_bulk.txt, C5 orbit): bulk 1353 / 1360 fps, blend 0.284 / 0.287 ms;
+                          // cp.async 1390 / 1393 fps, 0.266 / 0.269 ms: 48-B bulk copies cost more than they save
 #endif
 using RawRec = Splat;   // one gathered Gaussian: the preprocess's 48-B record, copied as is
 #ifndef GS_BLEND_TMA_STORE
@@ -115,10 +118,12 @@ struct __align__(1024) SmemTC {
     uint64_t slot_ready[RING];    // colours/header written -> compositors
     uint64_t raw_full[RAW];       // producer -> builder
     uint64_t raw_empty[RAW];      // builder -> producer
+    uint32_t lq[LQ];              // producer: kept list entries waiting for a batch
     uint32_t tmem_base;
     uint32_t warp_done_seq[NCW];
 #if GS_BLEND_TMA_STORE
-    float outb[2][4][GS_TILE_PIX];   // finished tile (R, G, B, T planes, row-major 16 x 16), double-buffered
+    alignas(128) float outb[2][4][GS_TILE_PIX];   // finished tile (R, G, B, T planes, row-major 16 x 16), double-
+                                                  // buffered; a TMA source must be 128-B aligned
 #endif
 };
 
@@ -199,7 +204,7 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
 
 template <bool DUMP, bool STATS, bool TRACE>
 __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
-    k_blend_tc(const Splat *__restrict__ splat, const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
+    k_blend_tc(const Splat *__restrict__ splat, const TileLists lists, int tile0, int ntiles, int gx,
                int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
                unsigned long long *stat_kept, long long *trace, const __grid_constant__ CUtensorMap tm_rgb,
@@ -249,27 +254,51 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     pdl_wait();   // the setup above overlapped the binning's tail
 
     if (warp == WARP_PRODUCER) {
-        // =================== producer: asynchronous gathers ===================
-        // Lane j of batch b copies record j (mean, conic+opacity, colour) with
-        // cp.async straight into raw slot b % RAW; the slot's barrier completes
-        // when the copies land, so RAW batches of gathers are in flight. The
-        // indices run PF batches ahead in registers; the next tile's first PF
-        // index vectors are fetched in three steps during the current tile.
+        // =================== producer: list filter + asynchronous gathers ===================
+        // A tile's list is its supertile's list filtered by the tile's mask bit (per-tile
+        // lists: every entry). Entries are read 32 per round, LPF rounds ahead in registers
+        // (the next tile's first LPF rounds are fetched during the current tile); the kept
+        // Gaussians, in list order, pass through a 64-entry queue in shared memory and leave
+        // in batches of NB (the last one of a list may be partial). Lane j of batch b copies
+        // record j with cp.async straight into raw slot b % RAW; the slot's barrier completes
+        // when the copies land, so RAW batches of gathers are in flight.
         uint32_t b_idx = 0;
+        const bool st_mode = lists.keys != nullptr;
+        // list range of tile t and the key bit that selects it (per-tile lists: any bit)
+        auto tile_list = [&](int t, uint2 &r, uint32_t &kbit) {
+            if (t >= ntiles) {
+                r = make_uint2(0u, 0u);
+                kbit = 1u;
+            } else if (st_mode) {
+                const int tx = t % gx, ty = t / gx;
+                r = lists.ranges[(ty >> 2) * lists.sgx + (tx >> 2)];
+                kbit = 1u << (16 + 4 * (ty & 3) + (tx & 3));
+            } else {
+                r = lists.ranges[t];
+                kbit = 1u;
+            }
+        };
+        // round at list position pos of range r: (key, value) of entry pos + lane; key 0 = none
+        auto fetch = [&](const uint2 &r, uint32_t pos, uint32_t &k, uint32_t &v) {
+            const bool ok = pos + lane < r.y;
+            v = ok ? lists.vals[pos + lane] : 0u;
+            k = ok ? (st_mode ? lists.keys[pos + lane] : 0xFFFFFFFFu) : 0u;
+        };
         int tile = 0;
         if (lane == 0) tile = tile0 + (int)atomicAdd(tile_queue, 1u);   // tiles [tile0, ntiles)
         tile = __shfl_sync(0xffffffffu, tile, 0);
-        uint2 rg = tile < ntiles ? ranges[tile] : make_uint2(0u, 0u);
-        uint32_t seq = 1;
-        uint32_t b = rg.x;
-        uint32_t idx[PF];
+        uint2 rg;
+        uint32_t kbit;
+        tile_list(tile, rg, kbit);
+        uint32_t seq = 1, pos = rg.x, head = 0, tail = 0, taken = 0;
+        uint32_t lk[LPF], lv[LPF];
 #pragma unroll
-        for (int j = 0; j < PF; j++) idx[j] = (b + j * NB + lane < rg.y) ? vals[b + j * NB + lane] : 0u;
+        for (int j = 0; j < LPF; j++) fetch(rg, pos + 32u * j, lk[j], lv[j]);
         int hstate = 0, ntile = 0, ntile_l0 = 0;
         uint2 nrg = make_uint2(0u, 0u);
-        uint32_t hidx[PF];
+        uint32_t nkbit = 1u, hk[LPF], hv[LPF];
 #pragma unroll
-        for (int j = 0; j < PF; j++) hidx[j] = 0u;
+        for (int j = 0; j < LPF; j++) hk[j] = hv[j] = 0u;
         auto head_step = [&]() {
             switch (hstate) {
                 case 0:
@@ -277,12 +306,11 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                     break;
                 case 1:
                     ntile = __shfl_sync(0xffffffffu, ntile_l0, 0);
-                    nrg = ntile < ntiles ? ranges[ntile] : make_uint2(0u, 0u);
+                    tile_list(ntile, nrg, nkbit);
                     break;
                 case 2:
 #pragma unroll
-                    for (int j = 0; j < PF; j++)
-                        hidx[j] = (nrg.x + j * NB + lane < nrg.y) ? vals[nrg.x + j * NB + lane] : 0u;
+                    for (int j = 0; j < LPF; j++) fetch(nrg, nrg.x + 32u * j, hk[j], hv[j]);
                     break;
                 default:
                     return;
@@ -330,26 +358,46 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 break;
             }
             head_step();
-            bool end = b >= rg.y;
+            // fill the queue up to NB kept Gaussians (or the end of the list)
+            while (tail - head < (uint32_t)NB && pos < rg.y) {
+                const bool keep = (lk[0] & kbit) != 0u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) sm.lq[(tail + __popc(bal & lanemask_lt_u32())) & (LQ - 1)] = lv[0];
+                tail += (uint32_t)__popc(bal);
+#pragma unroll
+                for (int j = 0; j + 1 < LPF; j++) {
+                    lk[j] = lk[j + 1];
+                    lv[j] = lv[j + 1];
+                }
+                fetch(rg, pos + 32u * LPF, lk[LPF - 1], lv[LPF - 1]);
+                pos += 32u;
+            }
+            __syncwarp();
+            bool end = tail == head;   // list exhausted, queue empty
             if (!DUMP && !end) end = tile_done(sm, lane, seq);
             if (end) {
                 push(make_int4(tile, (int)seq, 0, 0), 0u);   // end-of-tile marker
                 while (hstate < 3) head_step();
                 tile = ntile;
                 rg = nrg;
-                b = rg.x;
+                kbit = nkbit;
+                pos = rg.x;
+                head = tail = taken = 0;
                 seq++;
 #pragma unroll
-                for (int j = 0; j < PF; j++) idx[j] = hidx[j];
+                for (int j = 0; j < LPF; j++) {
+                    lk[j] = hk[j];
+                    lv[j] = hv[j];
+                }
                 hstate = 0;
                 continue;
             }
-            const uint32_t cnt = min((uint32_t)NB, rg.y - b);
-            push(make_int4(tile, (int)seq, (int)cnt, (int)b), idx[0]);
-#pragma unroll
-            for (int j = 0; j + 1 < PF; j++) idx[j] = idx[j + 1];
-            idx[PF - 1] = (b + PF * NB + lane < rg.y) ? vals[b + PF * NB + lane] : 0u;
-            b += NB;
+            const uint32_t cnt = min((uint32_t)NB, tail - head);
+            const uint32_t gi = lane < cnt ? sm.lq[(head + lane) & (LQ - 1)] : 0u;
+            __syncwarp();   // (the queue slots read here are refilled by later rounds)
+            push(make_int4(tile, (int)seq, (int)cnt, (int)(rg.x + taken)), gi);
+            head += cnt;
+            taken += cnt;
         }
     } else if (warp >= WARP_BUILD0 && warp < WARP_BUILD0 + NBLD) {
         // =================== builders: M_g rows (Eq. 6-7) ===================
@@ -586,7 +634,7 @@ static bool frame_tensor_maps(float *out_rgb, float *out_T, int W, int H, CUtens
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats) {
     const size_t smem = sizeof(SmemTC) + 1024;
@@ -603,7 +651,7 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, c
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
     CUtensorMap m_rgb{}, m_T{};
     const int tma = (GS_BLEND_TMA_STORE && !dump_m && frame_tensor_maps(out_rgb, out_T, W, H, m_rgb, m_T)) ? 1 : 0;
-#define ARGS splat, vals, ranges, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
+#define ARGS splat, lists, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
         launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
     else if (stats)

@@ -22,6 +22,7 @@ struct Counters {
     uint32_t n_rent;           // row entries (two-level binning): kept tile rows summed over Gaussians
     uint32_t n_cchunks;        // column-pass chunks (row-aligned, <= 4096 pairs each)
     uint32_t wide_depth;       // some visible depth key >= 2^27 above the near plane: 4th depth pass
+    uint32_t n_spairs;         // supertile binning: (supertile, Gaussian) pairs
     unsigned long long pairs_eval;   // GS_FLAG_STATS: exponents computed by the blend
     unsigned long long pairs_kept;   // GS_FLAG_STATS: pairs composited or terminating
 };
@@ -49,6 +50,25 @@ struct __align__(16) Splat {
     float4 col;    // (r, g, b, 0): SH colour
 };
 static_assert(sizeof(Splat) == 48, "48-byte splat record");
+
+// ---- what the blend reads for a tile -----------------------------------------
+// Per-tile lists (the two-level / one-level binning, or a caller's lists): the tile's
+// Gaussian slots vals[ranges[t].x .. ranges[t].y). Supertile lists (the tcgen05 blend's
+// default, binning.cu "Supertile binning"): the range of the tile's 4 x 4-tile supertile
+// (sgx supertiles per row) and keys with the tile mask in bits 16-31; the tile's list is
+// the entries whose mask has bit 16 + 4 (ty % 4) + tx % 4, in list order.
+struct TileLists {
+    const uint32_t *vals;
+    const uint32_t *keys;     // nullptr: per-tile lists
+    const uint2 *ranges;
+    int sgx;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt_u32() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
 
 // ---- device workspace owned by the context ---------------------------------
 struct Workspace {
@@ -85,6 +105,7 @@ struct Workspace {
     uint32_t *cmat;            // [512][max_chunks] per-chunk digit counts -> offsets
     uint32_t *row_total;       // [512] digit totals
     size_t max_chunks;
+    int list_sgx;              // lists of the last binning: supertiles per row, 0 = per-tile lists
     Counters *counters;
     Sticky *sticky;            // the context's (shared by every workspace)
     // scene staging for the host-pointer entry point
@@ -374,8 +395,9 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
                              int sh_stride, float scale_mod, int W, int H, int imode);
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
-                   uint32_t &epoch, bool tight, float znear, bool concurrent);
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx, int W,
+                   uint32_t &epoch, bool tight, float znear, bool concurrent, bool supertile);
+int supertile_count(int gx, int gy);   // 4 x 4-tile supertiles of a gx x gy tile grid
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0, int ntiles, int gx, int W,
                      int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
                      bool stats);
 extern long long *g_blend_trace;

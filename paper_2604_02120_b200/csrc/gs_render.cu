@@ -108,7 +108,7 @@ cudaError_t alloc_ws(gs::Workspace &w, size_t N, size_t K, size_t T) {
     A(w.depth_bits, N); A(w.splat, N); A(w.rect, N); A(w.touched, N);
     A(w.radius, N); A(w.tmask, N); A(w.tmask_r, N); A(w.sk[0], N); A(w.sk[1], N); A(w.sv[0], N); A(w.sv[1], N); A(w.off, N); A(w.rect_r, N);
     A(w.kt[0], K); A(w.kt[1], K); A(w.kv[0], K); A(w.kv[1], K); A(w.chunk_first, w.max_chunks);
-    A(w.ranges, T); A(w.sums, w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
+    A(w.ranges, T); A(w.sums, 2 * w.max_chunks); A(w.cmat, w.max_chunks * 512); A(w.row_total, 512);
     A(w.cdesc, w.max_chunks); A(w.cdesc_last, w.max_chunks); A(w.tile_cnt, T); A(w.rowinfo, 3 * 513);
     A(w.counters, 1);
 #undef A
@@ -203,8 +203,11 @@ int view_ws(gs_ctx *c, int v, gs::Workspace **out) {
 void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const gs_camera &cam, int W, int H,
                      const gs_opts &o, bool concurrent = false) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
+    // the tcgen05 blend filters supertile lists itself; the other blends read per-tile lists
+    const bool super = o.blend == GS_BLEND_TC && gs::supertile_count(gx, gy) <= 512;
+    w.list_sgx = super ? gs::ceil_div_i(gx, 4) : 0;
     c->launches += gs::launch_binning(w, st, N, c->max_keys, gx * gy, gx, c->epoch, (o.flags & GS_FLAG_TIGHT) != 0,
-                                      cam.znear, concurrent);
+                                      cam.znear, concurrent, super);
 }
 
 // preprocess + binning of one view into the context's workspace (counters zeroed first)
@@ -228,8 +231,16 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
     return e2;
 }
 
-void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const gs::Splat *splat, const uint32_t *vals, const uint2 *ranges, int W, int H, const gs_opts &o,
-                   float *out_rgb, float *out_T, float *dump) {
+// the lists a workspace's last binning produced
+gs::TileLists lists_of(const gs::Workspace &w) {
+    return gs::TileLists{w.kv[0], w.list_sgx ? w.kt[0] : nullptr, w.ranges, w.list_sgx};
+}
+
+void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const gs::Splat *splat,
+                   const gs::TileLists &lists, int W, int H, const gs_opts &o, float *out_rgb, float *out_T,
+                   float *dump) {
+    const uint32_t *vals = lists.vals;
+    const uint2 *ranges = lists.ranges;   // (per-tile lists for the mma.sync and direct blends)
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     int y0 = 0, y1 = gy;   // the row band's tiles only (a split frame's other bands are untouched)
     gs::band_rows(gy, o.band, o.n_bands, y0, y1);
@@ -241,7 +252,7 @@ void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const gs:
         gs::launch_blend_mma(w, st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                              c->num_sms, o.batch);
     else
-        gs::launch_blend_tc(w, st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
+        gs::launch_blend_tc(w, st, splat, lists, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                             dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
     c->launches += 1;
 }
@@ -302,6 +313,50 @@ __global__ void k_keys_out(const uint2 *ranges, const uint32_t *idx, const uint3
         const uint32_t s = idx[k];   // slot -> (tile << 32 | depth bits, Gaussian index)
         keys[k] = ((uint64_t)blockIdx.x << 32) | depth_bits[s];
         vals[k] = orig[s];
+    }
+}
+
+// debug binning of supertile lists: tile t's list = the entries of its supertile's list
+// whose key has the tile's mask bit (the filter the tcgen05 blend's producer applies)
+__device__ __forceinline__ void st_tile_of(const gs::TileLists &l, int gx, int t, uint2 &rg, uint32_t &kbit) {
+    const int tx = t % gx, ty = t / gx;
+    rg = l.ranges[(ty >> 2) * l.sgx + (tx >> 2)];
+    kbit = 1u << (16 + 4 * (ty & 3) + (tx & 3));
+}
+
+__global__ void k_st_tile_count(gs::TileLists l, int gx, uint32_t *tile_cnt) {
+    __shared__ uint32_t s_n;
+    uint2 rg;
+    uint32_t kbit;
+    st_tile_of(l, gx, blockIdx.x, rg, kbit);
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    uint32_t n = 0;
+    for (uint32_t k = rg.x + threadIdx.x; k < rg.y; k += blockDim.x) n += (l.keys[k] & kbit) ? 1u : 0u;
+    atomicAdd(&s_n, n);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_n;
+}
+
+// one warp per tile: the kept entries in list order (ballot compaction) -> keys / values
+__global__ void k_st_tile_fill(gs::TileLists l, int gx, const uint2 *tile_ranges, const uint32_t *depth_bits,
+                               const uint32_t *orig, uint64_t *keys, uint32_t *vals) {
+    uint2 rg;
+    uint32_t kbit;
+    st_tile_of(l, gx, blockIdx.x, rg, kbit);
+    const uint32_t lane = threadIdx.x;
+    uint32_t out = tile_ranges[blockIdx.x].x;
+    for (uint32_t k0 = rg.x; k0 < rg.y; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool keep = k < rg.y && (l.keys[k] & kbit);
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const uint32_t o = out + __popc(bal & ((1u << lane) - 1u));
+            const uint32_t sl = l.vals[k];
+            keys[o] = ((uint64_t)blockIdx.x << 32) | depth_bits[sl];
+            vals[o] = orig[sl];
+        }
+        out += __popc(bal);
     }
 }
 
@@ -415,7 +470,7 @@ int gs_render(gs_ctx *c, void *stream, int N, const float *means3D, const float 
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int e2 = enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
-    enqueue_blend(c, c->ws, st, c->ws.splat, c->ws.kv[0], c->ws.ranges, W, H, *o, out_rgb,
+    enqueue_blend(c, c->ws, st, c->ws.splat, lists_of(c->ws), W, H, *o, out_rgb,
                   out_T, nullptr);
     const int e3 = mark(c, st, *o);
     span(c, 2, e2, e3);
@@ -571,7 +626,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
                 cudaStreamWaitEvent(bl, c->ev_binned[set][j], 0);
                 if (hk && hk->pre_blend) hk->pre_blend(hk->user, bl, v0 + j);
                 const int e1 = mark(c, bl, o);
-                enqueue_blend(c, *w[j], bl, w[j]->splat, w[j]->kv[0], w[j]->ranges, W, H,
+                enqueue_blend(c, *w[j], bl, w[j]->splat, lists_of(*w[j]), W, H,
                               o, rgb_of[v0 + j], T_of[v0 + j], nullptr);
                 const int e2 = mark(c, bl, o);
                 if (hk && hk->post_blend) hk->post_blend(hk->user, bl, v0 + j);
@@ -588,7 +643,7 @@ static int render_views_impl(gs_ctx *c, cudaStream_t st, int N, const float *mea
             enqueue_binning(c, *w[j], st, N, cams[v0 + j], W, H, o);
             if (hk && hk->pre_blend) hk->pre_blend(hk->user, st, v0 + j);
             const int e1 = mark(c, st, o);
-            enqueue_blend(c, *w[j], st, w[j]->splat, w[j]->kv[0], w[j]->ranges, W, H, o,
+            enqueue_blend(c, *w[j], st, w[j]->splat, lists_of(*w[j]), W, H, o,
                           rgb_of[v0 + j], T_of[v0 + j], nullptr);
             const int e2 = mark(c, st, o);
             if (hk && hk->post_blend) hk->post_blend(hk->user, st, v0 + j);
@@ -900,10 +955,35 @@ int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const
     *n_keys = s.n_keys;
     if (s.status) return s.status;
     if (s.n_keys > capacity) return GS_ERR_CAPACITY;
-    const int ntiles = gs::ceil_div_i(W, GS_TILE) * gs::ceil_div_i(H, GS_TILE);
-    if (s.n_keys > 0) k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[0], c->ws.depth_bits, c->ws.orig, keys,
-                                                          vals);
-    cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
+    const int gx = gs::ceil_div_i(W, GS_TILE);
+    const int ntiles = gx * gs::ceil_div_i(H, GS_TILE);
+    if (c->ws.list_sgx) {
+        // supertile lists: per-tile counts, their scan on the host (test path), ordered fill
+        const gs::TileLists l = lists_of(c->ws);
+        k_st_tile_count<<<ntiles, 256, 0, st>>>(l, gx, c->ws.tile_cnt);
+        std::vector<uint32_t> cnt(ntiles), rg(2 * (size_t)ntiles);
+        if (check_cuda(cudaMemcpyAsync(cnt.data(), c->ws.tile_cnt, 4 * (size_t)ntiles, cudaMemcpyDeviceToHost, st)) ||
+            check_cuda(cudaStreamSynchronize(st)))
+            return GS_ERR_CUDA;
+        uint64_t acc = 0;
+        for (int t = 0; t < ntiles; t++) {
+            rg[2 * t] = cnt[t] ? (uint32_t)acc : 0u;
+            rg[2 * t + 1] = cnt[t] ? (uint32_t)(acc + cnt[t]) : 0u;
+            acc += cnt[t];
+        }
+        if (acc != (uint64_t)s.n_keys) {
+            fprintf(stderr, "gs_debug_binning: supertile lists hold %llu pairs, K = %lld\n",
+                    (unsigned long long)acc, (long long)s.n_keys);
+            return GS_ERR_CUDA;
+        }
+        cudaMemcpyAsync(ranges, rg.data(), 8 * (size_t)ntiles, cudaMemcpyHostToDevice, st);
+        k_st_tile_fill<<<ntiles, 32, 0, st>>>(l, gx, reinterpret_cast<const uint2 *>(ranges), c->ws.depth_bits,
+                                               c->ws.orig, keys, vals);
+    } else {
+        if (s.n_keys > 0)
+            k_keys_out<<<ntiles, 256, 0, st>>>(c->ws.ranges, c->ws.kv[0], c->ws.depth_bits, c->ws.orig, keys, vals);
+        cudaMemcpyAsync(ranges, c->ws.ranges, sizeof(uint2) * ntiles, cudaMemcpyDeviceToDevice, st);
+    }
     if (check_cuda(cudaStreamSynchronize(st))) return GS_ERR_CUDA;
     return GS_OK;
 }
@@ -924,7 +1004,7 @@ static int debug_blend_common(gs_ctx *c, void *stream, int N, const float *xy, c
         c->launches++;
     }
     c->last_counters = c->ws.counters;
-    enqueue_blend(c, c->ws, st, c->ws.splat, vals, reinterpret_cast<const uint2 *>(ranges), W, H,
+    enqueue_blend(c, c->ws, st, c->ws.splat, gs::TileLists{vals, nullptr, reinterpret_cast<const uint2 *>(ranges), 0}, W, H,
                   *o, out_rgb, out_T, dump);
     return finish(c, st, *o, N);
 }

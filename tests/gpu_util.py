@@ -38,7 +38,11 @@ def gpu_preprocess(ctx, scene, cam, st=None, flags=0, scale_modifier=1.0):
     return out
 
 
-def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0, scale_modifier=1.0):
+def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0, scale_modifier=1.0, blend=0):
+    """Keys / values / ranges per tile. blend=GS_BLEND_TC (0, the default) bins into the
+    supertile lists the tcgen05 blend filters (grids up to 512 supertiles; the library then
+    derives the per-tile lists with the blend's own mask filter); the other blends take the
+    per-tile two-level (or one-level) binning."""
     import torch
     st = st or scene_to_device(scene)
     cap = capacity or (1 << 22)
@@ -47,7 +51,8 @@ def gpu_binning(ctx, scene, cam, capacity=None, st=None, flags=0, scale_modifier
     ntiles = ((cam.W + 15) // 16) * ((cam.H + 15) // 16)
     ranges = torch.empty((ntiles, 2), dtype=torch.int32, device="cuda")
     code, K = ctx.gs_debug_binning(st, camera(cam), cam.W, cam.H,
-                                   _sh_opts(scene, flags=flags, scale_modifier=scale_modifier), keys, vals, ranges)
+                                   _sh_opts(scene, flags=flags, scale_modifier=scale_modifier, blend=blend), keys, vals,
+                                   ranges)
     if code != 0:
         return code, K, None
     return code, K, dict(keys=keys[:K].cpu().numpy().view(np.uint64), vals=vals[:K].cpu().numpy().view(np.uint32),

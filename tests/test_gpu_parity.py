@@ -36,11 +36,14 @@ def test_preprocess_bit_exact(case):
         assert len(bad) == 0, f"{k}: {len(bad)} Gaussians differ, first {bad[:5]}"
 
 
+@pytest.mark.parametrize("lists", [GS_BLEND_TC, GS_BLEND_MMA], ids=["supertile", "per_tile"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_binning_bit_exact(case):
+def test_binning_bit_exact(case, lists):
+    """Both binnings: the supertile lists of the tcgen05 blend (filtered per tile by the
+    mask bits) and the per-tile two-level / one-level lists of the other blends."""
     scene, cam, bg = CASES[case]()
     ctx = make_ctx(scene, cam)
-    code, K, got = gpu_binning(ctx, scene, cam)
+    code, K, got = gpu_binning(ctx, scene, cam, blend=lists)
     assert code == 0
     pre = oracle.preprocess(scene, cam)
     ref = oracle.binning(pre, cam.W, cam.H)
