@@ -172,7 +172,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_STATS, GS_FLAG_TIGHT, GS_FLAG_TIMING,
+    from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_BLEND_TC_COLOR, GS_FLAG_STATS,
+                                       GS_FLAG_TIGHT, GS_FLAG_TIMING,
                                        Context, camera, opts, scene_to_device, scene_to_host, synth)
     from paper_2604_02120_b200.orbit import gather_frames_pipelined, gather_plan, partition_views, share_frames
     ws, rank, local = _dist()
@@ -301,9 +302,13 @@ def run_ours(args):
     # group's union); per view it writes the warp's slot count (4 B per 32 Gaussians) and
     # 60 B per visible Gaussian (index, depth, mean, conic+opacity, colour, rect, tiles)
     pre_bytes = (N * 44 + n_vis * 12 * M) / group + N / 8 + n_vis * 60
-    # binning: compaction (read touched+depth, write 8 B/vis), 3 depth passes (16 B/vis
-    # each + a histogram read) with the rect gather (16 B/vis), duplication (8 B/key
-    # written), tile sort 2 passes (16 B/key each + histogram read), ranges (4 B/key)
+    # binning, the algorithmic traffic of the method's binning (per
+    # visible Gaussian and per (Gaussian, tile) key K): compaction (read touched+depth, write
+    # 8 B/vis), 3 depth passes (16 B/vis each + a histogram read) with the rect gather
+    # (16 B/vis), duplication (8 B/key written), tile sort 2 passes (16 B/key each + histogram
+    # read), ranges (4 B/key). The supertile scheme moves less (one pass over S ~ 0.31 K
+    # supertile pairs; the per-tile split is the blend's filter), so this is the work the
+    # canonical result needs, not the bytes the kernels move.
     bin_bytes = N * 8 + n_vis * 8 + 3 * 16 * n_vis + 4 * n_vis + 16 * n_vis + n_keys * 8 + \
         2 * 16 * n_keys + 4 * n_keys + 4 * n_keys
     # blend: SURVEY 8(d)'s issue roof -- 4 lane-slots per (Gaussian, pixel) pair the MMA
@@ -316,8 +321,8 @@ def run_ours(args):
                        "peak": hbm, "unit": "GB/s", "view_group": group,
                        "timing": "per view; one launch covers a view group"},
         "binning": {"ms": bin_ms, "bound": "hbm", "achieved": bin_bytes / (bin_ms * 1e-3) / 1e9, "peak": hbm,
-                    "unit": "GB/s", "kernels": "compaction, 3 depth passes, row entries + row pass, pair offsets, "
-                    "column pass with tile ranges (two-level binning)", "timing": "chains serialised (extra orbit)"},
+                    "unit": "GB/s", "kernels": "compaction, 3 depth passes, supertile-pair offsets, one 9-bit "
+                    "supertile pass (expansion fused), supertile ranges", "timing": "chains serialised (extra orbit)"},
         "blend": {"ms": blend_ms, "bound": "alu", "achieved": blend_slots / (blend_ms * 1e-3) / 1e12,
                   "peak": issue_peak, "unit": "T lane-slots/s", "pairs_evaluated": n_eval, "pairs_kept": n_kept,
                   "slots_per_pair": BLEND_SLOTS_PER_PAIR,
@@ -372,6 +377,12 @@ def run_ours(args):
             m_ms, m_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_MMA, batch=b,
                                           flags=GS_FLAG_TIMING | base_flags))
             ab["mma_sync"][f"b{b}"] = {"blend_ms": m_ms, "fps": m_fps, "speedup_tc_over_mma": m_ms / t_ms}
+        # N4: the colour sum as a second tcgen05 product (2 CTAs per SM), same lists
+        c_ms, c_fps = orbit_time(opts(bg, sh_degree=scene.sh_degree, blend=GS_BLEND_TC_COLOR,
+                                      flags=GS_FLAG_TIMING | base_flags))
+        ab["tc_color"] = {"blend_ms": c_ms, "fps": c_fps, "speedup_tc_over_tc_color": c_ms / t_ms,
+                          "note": "GS_BLEND_TC_COLOR (SURVEY N4): C += (alpha T) . colours^T on tcgen05, "
+                                  "2 CTAs/SM; frames within the parity gate (tests)"}
 
     # --- N3: the other intersection modes (bit-identical frames, fewer pairs), one timed orbit each ---
     n3 = {}

@@ -27,6 +27,7 @@ GS_ERR_NO_DEVICE = -6
 GS_BLEND_TC = 0
 GS_BLEND_DIRECT = 1
 GS_BLEND_MMA = 2
+GS_BLEND_TC_COLOR = 3   # N4: colour sum as a second tcgen05 product (include/gs_render.h)
 GS_FLAG_SYNC = 1
 GS_FLAG_TIMING = 2
 GS_FLAG_STATS = 4

@@ -538,28 +538,54 @@ __global__ void __launch_bounds__(SORT_THREADS) k_rs_count(Loader ld, const Coun
     }
 }
 
-// step 2: one warp per digit: exclusive scan of its row over the chunks; row totals.
-// Each lane keeps 8 chunk counts in flight (coalesced loads), then the warp scans them
-// in order with shuffles (no block barriers: rows are independent).
+// step 2: exclusive scan of each digit's row over the chunks; row totals. One block per
+// digit; its SCANROWS_WARPS warps split the row into segments: each warp sums its segment
+// (8 coalesced loads per lane in flight), the block adds up the segment totals, then each
+// warp scans its segment from its offset (a row of 1042 chunks: 2 load round trips, where
+// one warp walking the whole row took 5).
 constexpr int SCANROWS_WARPS = 8;
 __global__ void __launch_bounds__(SCANROWS_WARPS * 32) k_rs_scanrows(const Counters *cnt, int which, uint64_t max_keys,
                                                                    uint32_t *cmat, uint32_t ldm, uint32_t *row_total,
                                                                    int ndig) {
     pdl_wait();
+    __shared__ uint32_t s_tot[SCANROWS_WARPS];
     const uint32_t n = count_of(cnt, which, 0, max_keys);
     const uint32_t nchunks = (n + SORT_CHUNK - 1) / SORT_CHUNK;
-    const int lane = threadIdx.x & 31;
-    const int d = blockIdx.x * SCANROWS_WARPS + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int d = blockIdx.x;
     if (d >= ndig) return;
     uint32_t *row = cmat + (size_t)d * ldm;
     constexpr int U = 8;
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < nchunks; base += 32 * U) {
+    const uint32_t seg = ((nchunks + SCANROWS_WARPS - 1) / SCANROWS_WARPS + 31u) & ~31u;
+    const uint32_t c0 = min(nchunks, warp * seg), c1 = min(nchunks, c0 + seg);
+    uint32_t sum = 0;
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
         uint32_t v[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t c = base + u * 32 + lane;
-            v[u] = c < nchunks ? row[c] : 0u;
+            v[u] = c < c1 ? row[c] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) sum += v[u];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_tot[warp] = sum;
+    __syncthreads();
+    uint32_t carry = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < SCANROWS_WARPS; w++) {
+        const uint32_t t = s_tot[w];
+        carry += (uint32_t)w < warp ? t : 0u;
+        total += t;
+    }
+    for (uint32_t base = c0; base < c1; base += 32 * U) {
+        uint32_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t c = base + u * 32 + lane;
+            v[u] = c < c1 ? row[c] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -567,14 +593,14 @@ __global__ void __launch_bounds__(SCANROWS_WARPS * 32) k_rs_scanrows(const Count
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+                if (lane >= (uint32_t)o) x += y;
             }
             const uint32_t c = base + u * 32 + lane;
-            if (c < nchunks) row[c] = carry + x - v[u];
+            if (c < c1) row[c] = carry + x - v[u];
             carry += __shfl_sync(0xffffffffu, x, 31);
         }
     }
-    if (lane == 0) row_total[d] = carry;
+    if (threadIdx.x == 0) row_total[d] = total;
 }
 
 // step 3: stable scatter. position = (all smaller digits) + (this digit in
@@ -804,15 +830,16 @@ struct RowOffsetsOp {   // kept rows per depth-ordered Gaussian -> row-entry off
     }
 };
 
-// Warp-cooperative run expansion. Lane L holds a run of len_L >= 1 consecutive
-// output slots (lanes with len 0 only after the last run); the runs are laid out
-// back to back from slot 0. Each round maps 32 slots to their runs with one OR-
-// reduction of the run heads, so the work is balanced whatever the run lengths.
+// Warp-cooperative run expansion. Lane L holds a run of len_L >= 0 consecutive output
+// slots; the non-empty runs are laid out back to back from slot 0 in lane order. Each
+// round maps 32 slots to their runs with one OR-reduction of the run heads, so the work
+// is balanced whatever the run lengths.
 // emit(valid, owner, j, t): slot t is element j of the run of lane `owner`
 // (every lane calls it, so it may shuffle the owner's data).
 template <class F>
 __device__ __forceinline__ void warp_expand(uint32_t len, F &&emit) {
     const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nz = __ballot_sync(0xffffffffu, len != 0u);   // lanes with a run
     uint32_t pre = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -821,12 +848,13 @@ __device__ __forceinline__ void warp_expand(uint32_t len, F &&emit) {
     }
     const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
     pre -= len;   // exclusive
-    int carry = -1;   // run of the slot before this round
+    int carry = -1;   // run (among the non-empty ones) of the slot before this round
     for (uint32_t g = 0; g < total; g += 32) {
         const uint32_t head = (len && pre >= g && pre < g + 32u) ? (1u << (pre - g)) : 0u;
         const uint32_t heads = __reduce_or_sync(0xffffffffu, head);
-        const int owner = min(31, carry + __popc(heads & (0xFFFFFFFFu >> (31u - lane))));
+        const int run = min(31, carry + __popc(heads & (0xFFFFFFFFu >> (31u - lane))));
         carry += __popc(heads);
+        const int owner = (int)min(31u, __fns(nz, 0, run + 1));   // the lane of that run
         const uint32_t t = g + lane;
         const uint32_t opre = __shfl_sync(0xffffffffu, pre, owner);
         emit(t < total, owner, t - opre, t);
@@ -1251,6 +1279,12 @@ __global__ void __launch_bounds__(512) k_tile_ranges(const uint32_t *__restrict_
 // key = supertile id | mask << 16, value = Gaussian slot.
 // ---------------------------------------------------------------------------
 constexpr uint32_t ST_SIDE = 4;
+#ifndef GS_ST_SERIAL
+#define GS_ST_SERIAL 1       // supertile expansion: lanes write their own short runs
+#endif
+#ifndef GS_ST_COUNT_FAST
+#define GS_ST_COUNT_FAST 1   // supertile counts: whole rects without divisions
+#endif
 
 __device__ __forceinline__ uint32_t st_count(const ushort4 &rc) {
     const uint32_t sx0 = rc.x / ST_SIDE, sx1 = (rc.z - 1u) / ST_SIDE + 1u;
@@ -1360,7 +1394,7 @@ struct StLoader : LinearChunks {
                 const uint32_t end = min(o1[u], cend) - o[u];
                 const uint32_t sx0 = rc[u].x / ST_SIDE, sy0 = rc[u].y / ST_SIDE;
                 const uint32_t sw = (rc[u].z - 1u) / ST_SIDE + 1u - sx0;
-                if (q0 == 0 && end == o1[u] - o[u]) {   // the whole rect in this chunk: one run per row
+                if (GS_ST_COUNT_FAST && q0 == 0 && end == o1[u] - o[u]) {   // whole rect in the chunk: a run per row
                     const uint32_t sy1 = (rc[u].w - 1u) / ST_SIDE + 1u;
                     for (uint32_t sy = sy0; sy < sy1; sy++) {
                         const uint32_t d = sy * (uint32_t)sgx + sx0;
@@ -1380,6 +1414,17 @@ struct StLoader : LinearChunks {
             }
         }
     }
+    // key of the q-th supertile pair of the rect [x0, x1) x [y0, y1) (row-major over its
+    // supertiles, sw per row): supertile id | tile mask << 16
+    __device__ __forceinline__ uint32_t key_of(uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1, uint32_t qx,
+                                               uint32_t qy, unsigned long long tm) const {
+        const uint32_t sx = x0 / ST_SIDE + qx, sy = y0 / ST_SIDE + qy;
+        return (sy * (uint32_t)sgx + sx) | (st_mask(x0, y0, x1, y1, sx, sy, tm) << 16);
+    }
+    // Each lane writes its own Gaussian's pairs (position in the rect stepped without a
+    // division); Gaussians with more than SERIAL_MAX pairs in the chunk are left to a
+    // warp-cooperative expansion afterwards (balanced whatever their length).
+    static constexpr uint32_t SERIAL_MAX = 6;
     __device__ void load(uint32_t c, uint32_t cbase, uint32_t cvalid, uint32_t *sk, uint32_t *sv, uint32_t *) const {
         uint32_t r_lo, r_hi;
         window(c, r_lo, r_hi);
@@ -1401,9 +1446,26 @@ struct StLoader : LinearChunks {
                 len = min(o1, cend) - (o + q0);
                 slot0 = o + q0 - cbase;
             }
-            const uint32_t wslot = __shfl_sync(0xffffffffu, slot0, 0);
-            warp_expand(len, [&](bool valid, int owner, uint32_t j, uint32_t t) {
+            const uint32_t x0 = rxy & 0xFFFFu, y0 = rxy >> 16, x1 = rzw & 0xFFFFu, y1 = rzw >> 16;
+            if (GS_ST_SERIAL && len > 0 && len <= SERIAL_MAX) {
+                const uint32_t sw = (x1 - 1u) / ST_SIDE + 1u - x0 / ST_SIDE;
+                uint32_t qy = q0 ? udiv_small(q0, sw) : 0u;
+                uint32_t qx = q0 - qy * sw;
+                for (uint32_t j = 0; j < len; j++) {
+                    sk[slot0 + j] = key_of(x0, y0, x1, y1, qx, qy, m);
+                    if (sv) sv[slot0 + j] = idx;
+                    if (++qx == sw) {
+                        qx = 0;
+                        qy++;
+                    }
+                }
+            }
+            if (GS_ST_SERIAL && !__any_sync(0xffffffffu, len > SERIAL_MAX)) continue;
+            // the long ones, balanced over the warp (slots of the others are skipped)
+            const uint32_t llen = (!GS_ST_SERIAL || len > SERIAL_MAX) ? len : 0u;
+            warp_expand(llen, [&](bool valid, int owner, uint32_t j, uint32_t) {
                 const uint32_t oq0 = __shfl_sync(0xffffffffu, q0, owner);
+                const uint32_t os0 = __shfl_sync(0xffffffffu, slot0, owner);
                 const uint32_t oxy = __shfl_sync(0xffffffffu, rxy, owner);
                 const uint32_t ozw = __shfl_sync(0xffffffffu, rzw, owner);
                 const uint32_t oidx = __shfl_sync(0xffffffffu, idx, owner);
@@ -1412,12 +1474,11 @@ struct StLoader : LinearChunks {
                     om = ((unsigned long long)__shfl_sync(0xffffffffu, (uint32_t)(m >> 32), owner) << 32) |
                          __shfl_sync(0xffffffffu, (uint32_t)m, owner);
                 if (!valid) return;
-                const uint32_t x0 = oxy & 0xFFFFu, y0 = oxy >> 16, x1 = ozw & 0xFFFFu, y1 = ozw >> 16;
-                const uint32_t sx0 = x0 / ST_SIDE, sy0 = y0 / ST_SIDE, sw = (x1 - 1u) / ST_SIDE + 1u - sx0;
+                const uint32_t ox0 = oxy & 0xFFFFu, oy0 = oxy >> 16, ox1 = ozw & 0xFFFFu, oy1 = ozw >> 16;
+                const uint32_t sw = (ox1 - 1u) / ST_SIDE + 1u - ox0 / ST_SIDE;
                 const uint32_t q = oq0 + j, qy = udiv_small(q, sw);
-                const uint32_t sx = sx0 + (q - qy * sw), sy = sy0 + qy;
-                sk[wslot + t] = (sy * (uint32_t)sgx + sx) | (st_mask(x0, y0, x1, y1, sx, sy, om) << 16);
-                if (sv) sv[wslot + t] = oidx;
+                sk[os0 + j] = key_of(ox0, oy0, ox1, oy1, q - qy * sw, qy, om);
+                if (sv) sv[os0 + j] = oidx;
             });
         }
     }
@@ -1482,8 +1543,8 @@ static int radix_pass(const Workspace &ws, cudaStream_t st, int grid, Loader ld,
     if (dbits > 8) launch_count<Loader, 512>(ws, st, grid, ld, which, mk, shift);
     else launch_count<Loader, 256>(ws, st, grid, ld, which, mk, shift);
     const int ndig = dbits > 8 ? 512 : 256;
-    launch_pdl(k_rs_scanrows, ndig / SCANROWS_WARPS, SCANROWS_WARPS * 32, 0, st, ws.counters, which, mk, ws.cmat,
-               (uint32_t)ldm, ws.row_total, ndig);
+    launch_pdl(k_rs_scanrows, ndig, SCANROWS_WARPS * 32, 0, st, ws.counters, which, mk, ws.cmat, (uint32_t)ldm,
+               ws.row_total, ndig);
     switch (dbits) {
     case 1: launch_scatter<Loader, 1>(ws, st, grid, ld, kout, vout, which, mk, shift); break;
     case 2: launch_scatter<Loader, 2>(ws, st, grid, ld, kout, vout, which, mk, shift); break;

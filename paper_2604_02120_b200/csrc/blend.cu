@@ -30,6 +30,7 @@
 // Reference pixel p_c = tile centre (16 t_x + 7.5, 16 t_y + 7.5) (reading R-6),
 // x_bar = x_c - x_p (Eq. 4; reading R-7).
 #include <algorithm>
+#include <type_traits>
 
 #include <cuda.h>   // CUtensorMap (the TMA descriptors of the frame stores)
 
@@ -72,10 +73,13 @@ constexpr int NBLD = GS_BLEND_NBLD;     // builder warps (alternate batches)
 constexpr int RAW = GS_BLEND_RAW;       // raw-record ring (producer -> builders): gathers in flight
 constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
 #ifndef GS_BLEND_LPF
-#define GS_BLEND_LPF 4
+#define GS_BLEND_LPF 1
 #endif
-constexpr int LPF = GS_BLEND_LPF;  // list rounds (32 entries) the producer reads ahead
-constexpr int LQ = 64;             // producer queue of kept entries (>= NB + 32)
+#ifndef GS_BLEND_HPF
+#define GS_BLEND_HPF 1     // 1: fetch the next tile's first list round during the current tile
+#endif
+constexpr int LPF = GS_BLEND_LPF;  // list rounds (128 entries) the producer holds ahead
+constexpr int LQ = 256;            // producer queue of kept entries (>= NB + 128, power of two)
 // warp roles: 0..NCW-1 compositors, NCW producer, NCW+1.. builders (each also issues
 // the MMAs of the batches it built, and builder 0 owns the TMEM allocation)
 constexpr int WARP_PRODUCER = NCW, WARP_BUILD0 = NCW + 1, WARP_TMEM = NCW + 1;
@@ -127,9 +131,27 @@ struct __align__(1024) SmemTC {
 #endif
 };
 
+// N4 (GS_BLEND_TC_COLOR): the colour sum C = sum_i c_i alpha_i T_i (Eq. 1) as a second
+// tensor-core product per batch, C[pixels x 16] += W[pixels x NB] . Col[16 x NB]^T with
+// W = alpha T (0 for Gaussians not composited), rounded to TF32 by the compositors into
+// shared memory, and Col = the batch's colours split TF32 hi | lo (rows r, g, b, r_lo, g_lo,
+// b_lo, 0...). The accumulators (2 halves x 16 columns) live in TMEM for the whole tile;
+// 160 columns round the allocation up to 256, so 2 CTAs per SM.
+struct __align__(1024) SmemTCC : SmemTC {
+    uint8_t Wb[2][2][128 * 128];   // W per colour-batch parity and pixel half: 128 rows x 32 tf32 (K-major)
+    uint8_t Cb[RING][16 * 128];    // colour operand per slot: 16 rows x 32 tf32 (K-major)
+    uint64_t wfull[2];             // compositors wrote W of colour batch n (parity n % 2)
+    uint64_t cdone[2];             // the colour MMA of batch n read W[n % 2] (commit)
+    uint64_t cacc;                 // the tile's colour accumulators are complete (commit at its marker)
+};
+constexpr int CM_TMEM_COLS = 256;
+constexpr int CM_COL0 = STAGES * 2 * NB;   // first accumulator column (after the exponent stages)
+
 // byte offset of (row r, 16-byte K-chunk c) in a K-major no-swizzle operand
 // with 4 K-chunks per row: core matrix = 8 rows x 16 B, LBO = 128, SBO = 512
 __device__ __forceinline__ uint32_t op_off(int r, int c) { return (r >> 3) * 512 + c * 128 + (r & 7) * 16; }
+// the same with 8 K-chunks per row (K = 32): LBO = 128, SBO = 1024
+__device__ __forceinline__ uint32_t op_off32(int r, int c) { return (r >> 3) * 1024 + c * 128 + (r & 7) * 16; }
 
 // pixel of compositor thread p = 32*w + lane inside the 16x16 tile: warp w
 // covers the 8x4 block at (8*(w%2), 4*(w/2)) (compact blocks maximise the
@@ -202,16 +224,19 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
         if (TRACE && blockIdx.x == 0 && (b) < 1024u && lane == 0) trace[(size_t)(b) * 16 + (ev)] = clock64(); \
     } while (0)
 
-template <bool DUMP, bool STATS, bool TRACE>
-__global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
+template <bool DUMP, bool STATS, bool TRACE, bool CM>
+__global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
     k_blend_tc(const Splat *__restrict__ splat, const TileLists lists, int tile0, int ntiles, int gx,
                int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
                unsigned long long *stat_kept, long long *trace, const __grid_constant__ CUtensorMap tm_rgb,
                const __grid_constant__ CUtensorMap tm_T, int tma_out) {
     extern __shared__ uint8_t smem_raw[];
-    SmemTC &sm = *reinterpret_cast<SmemTC *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    using SM = std::conditional_t<CM, SmemTCC, SmemTC>;
+    SM &sm = *reinterpret_cast<SM *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NCOLS = CM ? CM_TMEM_COLS : TMEM_COLS;
+    static_assert(!CM || NBLD == 1, "the colour MMA follows the single builder's batch order");
 
     // ---- one-time setup -------------------------------------------------
     if (threadIdx.x == 0) {
@@ -224,7 +249,18 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             mbar_init(&sm.raw_full[r], GS_BLEND_BULK ? 1 : 33);   // header arrive (+ expect_tx) | 32 cp.async + header
             mbar_init(&sm.raw_empty[r], 1);
         }
+        if constexpr (CM) {
+            for (int q = 0; q < 2; q++) {
+                mbar_init(&sm.wfull[q], NCW);
+                mbar_init(&sm.cdone[q], 1);
+            }
+            mbar_init(&sm.cacc, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if constexpr (CM) {   // colour operand rows 6..15 stay zero
+        for (int i = threadIdx.x; i < RING * 16 * 128 / 16; i += TC_THREADS)
+            reinterpret_cast<uint4 *>(&sm.Cb[0][0])[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (warp < NCW) {
         // M_p row for pixel p (Eq. 7): [xb^2, yb^2, xb*yb, xb, yb, 1] twice (hi/lo), then 0
@@ -244,7 +280,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         if (lane == 0) sm.warp_done_seq[warp] = 0;
         fence_proxy_async_smem();
     } else if (warp == WARP_TMEM) {
-        tmem_alloc(&sm.tmem_base, TMEM_COLS);
+        tmem_alloc(&sm.tmem_base, NCOLS);
         tmem_relinquish();
     }
     tc_fence_before();
@@ -256,8 +292,8 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     if (warp == WARP_PRODUCER) {
         // =================== producer: list filter + asynchronous gathers ===================
         // A tile's list is its supertile's list filtered by the tile's mask bit (per-tile
-        // lists: every entry). Entries are read 32 per round, LPF rounds ahead in registers
-        // (the next tile's first LPF rounds are fetched during the current tile); the kept
+        // lists: every entry). Entries are read 128 per round, LPF rounds ahead in registers
+        // (the next tile's first round is fetched during the current tile); the kept
         // Gaussians, in list order, pass through a 64-entry queue in shared memory and leave
         // in batches of NB (the last one of a list may be partial). Lane j of batch b copies
         // record j with cp.async straight into raw slot b % RAW; the slot's barrier completes
@@ -278,11 +314,26 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 kbit = 1u;
             }
         };
-        // round at list position pos of range r: (key, value) of entry pos + lane; key 0 = none
-        auto fetch = [&](const uint2 &r, uint32_t pos, uint32_t &k, uint32_t &v) {
-            const bool ok = pos + lane < r.y;
-            v = ok ? lists.vals[pos + lane] : 0u;
-            k = ok ? (st_mode ? lists.keys[pos + lane] : 0xFFFFFFFFu) : 0u;
+        // One round = 128 list entries from position p (a multiple of 4): lane L holds entries
+        // p + 4L .. p + 4L + 3 (one 16-B load of keys and one of values when all four lie
+        // inside the range, else per entry); entries outside [r.x, r.y) read as key 0.
+        auto fetch = [&](const uint2 &r, uint32_t p, uint4 &k, uint4 &v) {
+            const uint32_t e = p + 4u * lane;
+            if (e >= r.x && e + 3u < r.y) {
+                v = __ldg(reinterpret_cast<const uint4 *>(lists.vals + e));
+                k = st_mode ? __ldg(reinterpret_cast<const uint4 *>(lists.keys + e))
+                            : make_uint4(~0u, ~0u, ~0u, ~0u);
+            } else {
+                uint32_t kk[4], vv[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const bool ok = e + j >= r.x && e + j < r.y;
+                    vv[j] = ok ? lists.vals[e + j] : 0u;
+                    kk[j] = ok ? (st_mode ? lists.keys[e + j] : ~0u) : 0u;
+                }
+                v = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+                k = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+            }
         };
         int tile = 0;
         if (lane == 0) tile = tile0 + (int)atomicAdd(tile_queue, 1u);   // tiles [tile0, ntiles)
@@ -290,15 +341,14 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         uint2 rg;
         uint32_t kbit;
         tile_list(tile, rg, kbit);
-        uint32_t seq = 1, pos = rg.x, head = 0, tail = 0, taken = 0;
-        uint32_t lk[LPF], lv[LPF];
+        uint32_t seq = 1, pos = rg.x & ~3u, head = 0, tail = 0, taken = 0;
+        uint4 lk[LPF], lv[LPF];
 #pragma unroll
-        for (int j = 0; j < LPF; j++) fetch(rg, pos + 32u * j, lk[j], lv[j]);
+        for (int j = 0; j < LPF; j++) fetch(rg, pos + 128u * j, lk[j], lv[j]);
         int hstate = 0, ntile = 0, ntile_l0 = 0;
         uint2 nrg = make_uint2(0u, 0u);
-        uint32_t nkbit = 1u, hk[LPF], hv[LPF];
-#pragma unroll
-        for (int j = 0; j < LPF; j++) hk[j] = hv[j] = 0u;
+        uint32_t nkbit = 1u;
+        uint4 hk = make_uint4(0u, 0u, 0u, 0u), hv = hk;   // the next tile's first round
         auto head_step = [&]() {
             switch (hstate) {
                 case 0:
@@ -309,8 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                     tile_list(ntile, nrg, nkbit);
                     break;
                 case 2:
-#pragma unroll
-                    for (int j = 0; j < LPF; j++) fetch(nrg, nrg.x + 32u * j, hk[j], hv[j]);
+                    if (GS_BLEND_HPF) fetch(nrg, nrg.x & ~3u, hk, hv);
                     break;
                 default:
                     return;
@@ -360,17 +409,30 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             head_step();
             // fill the queue up to NB kept Gaussians (or the end of the list)
             while (tail - head < (uint32_t)NB && pos < rg.y) {
-                const bool keep = (lk[0] & kbit) != 0u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) sm.lq[(tail + __popc(bal & lanemask_lt_u32())) & (LQ - 1)] = lv[0];
-                tail += (uint32_t)__popc(bal);
+                // ordered compaction of the round: lane L's kept entries go to the queue after
+                // those of lanes < L (exclusive scan of the per-lane counts)
+                const uint32_t km = ((lk[0].x & kbit) ? 1u : 0u) | ((lk[0].y & kbit) ? 2u : 0u) |
+                                    ((lk[0].z & kbit) ? 4u : 0u) | ((lk[0].w & kbit) ? 8u : 0u);
+                const uint32_t c = (uint32_t)__popc(km);
+                uint32_t x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                uint32_t w = tail + x - c;
+                if (km & 1u) sm.lq[w++ & (LQ - 1)] = lv[0].x;
+                if (km & 2u) sm.lq[w++ & (LQ - 1)] = lv[0].y;
+                if (km & 4u) sm.lq[w++ & (LQ - 1)] = lv[0].z;
+                if (km & 8u) sm.lq[w & (LQ - 1)] = lv[0].w;
+                tail += __shfl_sync(0xffffffffu, x, 31);
 #pragma unroll
                 for (int j = 0; j + 1 < LPF; j++) {
                     lk[j] = lk[j + 1];
                     lv[j] = lv[j + 1];
                 }
-                fetch(rg, pos + 32u * LPF, lk[LPF - 1], lv[LPF - 1]);
-                pos += 32u;
+                fetch(rg, pos + 128u * LPF, lk[LPF - 1], lv[LPF - 1]);
+                pos += 128u;
             }
             __syncwarp();
             bool end = tail == head;   // list exhausted, queue empty
@@ -381,14 +443,17 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 tile = ntile;
                 rg = nrg;
                 kbit = nkbit;
-                pos = rg.x;
+                pos = rg.x & ~3u;
                 head = tail = taken = 0;
                 seq++;
-#pragma unroll
-                for (int j = 0; j < LPF; j++) {
-                    lk[j] = hk[j];
-                    lv[j] = hv[j];
+                if (GS_BLEND_HPF) {
+                    lk[0] = hk;
+                    lv[0] = hv;
+                } else {
+                    fetch(rg, pos, lk[0], lv[0]);
                 }
+#pragma unroll
+                for (int j = 1; j < LPF; j++) fetch(rg, pos + 128u * j, lk[j], lv[j]);
                 hstate = 0;
                 continue;
             }
@@ -404,6 +469,34 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         // STATS: the exponents the MMA computes, (Gaussian, pixel) pairs of the batches built
         // (batches of a tile found terminated before their build are dropped, not counted)
         unsigned long long n_eval = 0;
+        // CM: the colour MMA of data batch n is issued once the compositors wrote its W, i.e.
+        // while the next batch is built (pend_*: the batch waiting for it)
+        int pend_slot = -1;
+        uint32_t n_col = 0, pend_n = 0;
+        bool first_of_tile = true, pend_first = false;
+        auto flush_colour = [&]() {
+            if constexpr (CM) {
+                if (pend_slot < 0) return;
+                mbar_wait(&sm.wfull[pend_n & 1u], (pend_n >> 1) & 1u);
+                tc_fence_after();
+                if (lane == 0) {
+                    constexpr uint32_t IDESC = idesc_tf32(128, 16);
+                    const uint32_t b_base = smem_u32(&sm.Cb[pend_slot][0]);
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint32_t a_base = smem_u32(&sm.Wb[pend_n & 1u][h][0]);
+#pragma unroll
+                        for (int kk = 0; kk < NB / 8; kk++)
+                            mma_tf32(tmem + CM_COL0 + h * 16, umma_desc(a_base + kk * 256, 128, 1024),
+                                     umma_desc(b_base + kk * 256, 128, 1024), IDESC,
+                                     (pend_first && kk == 0) ? 0u : 1u);
+                    }
+                    mma_commit(&sm.cdone[pend_n & 1u]);
+                }
+                __syncwarp();
+                pend_slot = -1;
+            }
+        };
         for (uint32_t kb = warp - WARP_BUILD0;; kb += NBLD) {
             const int r = kb % RAW, s = kb % STAGES, slot = kb % RING;
             mbar_wait(&sm.raw_full[r], (kb / RAW) & 1u);
@@ -418,6 +511,18 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             }
             if (hd.z > 0) {
                 if (lane < NB) build_row(sm, s, slot, hd, sm.raw[r][lane], lane, gx);
+                if constexpr (CM) {   // colour operand of the slot: K index = lane, rows r g b hi | lo
+                    const float4 c = sm.raw[r][lane].col;
+                    const float cv[3] = {c.x, c.y, c.z};
+                    const uint32_t cb = smem_u32(&sm.Cb[slot][0]) + (lane >> 2) * 128 + (lane & 3) * 4;
+#pragma unroll
+                    for (int ch = 0; ch < 3; ch++) {
+                        const uint32_t hi = lane < hd.z ? f32_to_tf32_rna(cv[ch]) : 0u;
+                        const uint32_t lo = lane < hd.z ? f32_to_tf32_rna(cv[ch] - __uint_as_float(hi)) : 0u;
+                        asm volatile("st.shared.b32 [%0], %1;" ::"r"(cb + ch * 16), "r"(hi) : "memory");
+                        asm volatile("st.shared.b32 [%0], %1;" ::"r"(cb + (3 + ch) * 16), "r"(lo) : "memory");
+                    }
+                }
                 fence_proxy_async_smem();
                 if (STATS) n_eval += (unsigned long long)hd.z * GS_TILE_PIX;
             }
@@ -451,6 +556,21 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 }
                 __syncwarp();
             }
+            if constexpr (CM) {
+                flush_colour();   // the previous data batch (its W is written while this one computes)
+                if (hd.z > 0) {
+                    pend_slot = slot;
+                    pend_n = n_col++;
+                    pend_first = first_of_tile;
+                    first_of_tile = false;
+                } else if (hd.z == 0 && hd.x >= 0) {   // end of tile: accumulators complete
+                    // (only for tiles with a colour batch: their last W implies the compositors
+                    // read the previous tile's accumulators, so cacc is never two phases ahead)
+                    if (!first_of_tile && lane == 0) mma_commit(&sm.cacc);
+                    __syncwarp();
+                    first_of_tile = true;
+                }
+            }
             if (hd.x < 0) {
                 if (STATS && lane == 0) atomicAdd(stat_eval, n_eval);
                 break;
@@ -468,6 +588,9 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
         float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
         bool wdone = false;
         uint32_t n_kept = 0, n_tiles = 0;
+        uint32_t n_col = 0, n_acc = 0;    // CM: data batches (W buffers) and tiles with accumulators so far
+        bool tile_col = false;            // CM: the tile had a colour batch
+        const int crow_w = p & 127;       // CM: this pixel's row in its half's W operand
         for (uint32_t k = 0;; k++) {
             const int s = k % STAGES;
             const int c_slot = k % RING;
@@ -477,6 +600,13 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
             if (warp == 0) {
                 mbar_wait(&sm.slot_ready[c_slot], (k / RING) & 1u);
                 mbar_wait(&sm.full[s], (k / STAGES) & 1u);
+                if constexpr (CM) {
+                    const int4 h0 = sm.hdr[c_slot];
+                    if (h0.z > 0 && n_col >= 2)   // W[n % 2] free: the colour MMA of batch n - 2 read it
+                        mbar_wait(&sm.cdone[n_col & 1u], ((n_col - 2) >> 1) & 1u);
+                    else if (h0.z == 0 && h0.x >= 0 && tile_col)   // the tile's accumulators are complete
+                        mbar_wait(&sm.cacc, n_acc & 1u);
+                }
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");
 #else
@@ -496,6 +626,18 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                         if (lane == 0) atomicAdd(stat_kept, kk);
                     }
                     break;
+                }
+                if constexpr (CM) {   // C from the tile's colour accumulators: hi + lo columns
+                    if (tile_col) {
+                        float cv[16];
+                        tmem_ld16(tmem + t_lane + CM_COL0 + (uint32_t)(warp >> 2) * 16, cv);
+                        tmem_wait_ld();
+                        C0 = cv[0] + cv[3];
+                        C1 = cv[1] + cv[4];
+                        C2 = cv[2] + cv[5];
+                        n_acc++;
+                    }
+                    tile_col = false;
                 }
 #if GS_BLEND_TMA_STORE
                 if (!DUMP && tma_out) {
@@ -534,6 +676,12 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                     }
                 }
                 T = 1.0f; C0 = C1 = C2 = 0.f; thr = LOG2_ALPHA_MIN; wdone = false;
+            } else if (hd.z > 0 && wdone) {
+                if constexpr (CM) {   // W of a finished warp: zeros
+                    const uint32_t wb = smem_u32(&sm.Wb[n_col & 1u][warp >> 2][0]);
+#pragma unroll
+                    for (int c = 0; c < NB / 4; c++) st_shared_v4(wb + op_off32(crow_w, c), 0u, 0u, 0u, 0u);
+                }
             } else if (hd.z > 0 && !wdone) {
                 const int cnt = hd.z;
                 const uint32_t crow = smem_u32(&sm.rgb[c_slot][0]);
@@ -542,6 +690,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
 #pragma unroll
                 for (int h0 = 0; h0 < NB; h0 += CH) {
                     float m[CH];
+                    float wv[CM ? CH : 1];   // CM: this chunk's W = alpha T (0: not composited)
                     tmem_ld_cols(tmem + t_lane + s * (2 * NB) + t_half + h0, m);
                     tmem_wait_ld();
                     if (DUMP) {
@@ -553,19 +702,34 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                         for (int j = 0; j < CH; j++) {
                             const float mj = m[j];
                             const bool live = mj >= thr;                    // alpha >= 1/255 (R-1), pixel running
+                            if constexpr (CM) wv[j] = 0.f;
                             if (__any_sync(0xffffffffu, live)) {            // warp-uniform skip
-                                const float4 c = ld_shared_f4(crow + 16 * (h0 + j));
                                 const float a = fminf(ALPHA_MAX, ex2_approx(mj));   // alpha = 2^m capped (R-4)
                                 const float tT = fmaf(-a, T, T);                    // T (1 - alpha)
                                 const float w = a * T;
                                 const bool acc = live && tT >= T_MIN;               // composite (Eq. 1, R-3)
                                 if (STATS) n_kept += live ? 1u : 0u;
-                                C0 = acc ? fmaf(w, c.x, C0) : C0;
-                                C1 = acc ? fmaf(w, c.y, C1) : C1;
-                                C2 = acc ? fmaf(w, c.z, C2) : C2;
+                                if constexpr (CM) {
+                                    wv[j] = acc ? w : 0.f;
+                                } else {
+                                    // (predicated updates: a select-free form, w = (acc ? a : 0) T,
+                                    // saves the register moves but lengthens the chain, measured slower)
+                                    const float4 c = ld_shared_f4(crow + 16 * (h0 + j));
+                                    C0 = acc ? fmaf(w, c.x, C0) : C0;
+                                    C1 = acc ? fmaf(w, c.y, C1) : C1;
+                                    C2 = acc ? fmaf(w, c.z, C2) : C2;
+                                }
                                 T = acc ? tT : T;
                                 thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;   // stop (R-2)
                             }
+                        }
+                        if constexpr (CM) {   // this chunk's 16 W values, TF32 (round to nearest)
+                            const uint32_t wb = smem_u32(&sm.Wb[n_col & 1u][warp >> 2][0]);
+#pragma unroll
+                            for (int q = 0; q < CH / 4; q++)
+                                st_shared_v4(wb + op_off32(crow_w, h0 / 4 + q), f32_to_tf32_rna(wv[4 * q]),
+                                             f32_to_tf32_rna(wv[4 * q + 1]), f32_to_tf32_rna(wv[4 * q + 2]),
+                                             f32_to_tf32_rna(wv[4 * q + 3]));
                         }
                     }
                 }
@@ -577,6 +741,15 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
                 }
             }
             tc_fence_before();
+            if constexpr (CM) {
+                if (hd.z > 0) {   // W of this batch written (every warp, finished or not)
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.wfull[n_col & 1u]);
+                    n_col++;
+                    tile_col = true;
+                }
+            }
             __syncwarp();
             if (warp == 0) TRACE_EV(8, k);
             if (warp == 7) TRACE_EV(10, k);
@@ -590,7 +763,7 @@ __global__ void __launch_bounds__(TC_THREADS, GS_BLEND_MINB)
     __syncthreads();
     if (warp == WARP_TMEM) {
         tc_fence_after();
-        tmem_dealloc(tmem, TMEM_COLS);
+        tmem_dealloc(tmem, NCOLS);
     }
 }
 
@@ -634,32 +807,47 @@ static bool frame_tensor_maps(float *out_rgb, float *out_T, int W, int H, CUtens
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0, int ntiles, int gx, int W,
-                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
-                     bool stats) {
-    const size_t smem = sizeof(SmemTC) + 1024;
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0,
+                     int ntiles, int gx, int W, int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m,
+                     int num_sms, bool stats, bool colour_mma) {
+    const size_t smem = sizeof(SmemTC) + 1024, smem_c = sizeof(SmemTCC) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_blend_tc<false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_tc<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<true, false, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(k_blend_tc<false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_c);
+        cudaFuncSetAttribute(k_blend_tc<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_c);
         attr_set = true;
     }
-    const int grid = std::max(1, std::min(GS_BLEND_MINB * num_sms, ntiles - tile0));
+    colour_mma = colour_mma && !dump_m;
+    const int grid = std::max(1, std::min((colour_mma ? 2 : GS_BLEND_MINB) * num_sms, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
     CUtensorMap m_rgb{}, m_T{};
     const int tma = (GS_BLEND_TMA_STORE && !dump_m && frame_tensor_maps(out_rgb, out_T, W, H, m_rgb, m_T)) ? 1 : 0;
 #define ARGS splat, lists, tile0, ntiles, gx, W, H, bg[0], bg[1], bg[2], out_rgb, out_T, dump_m, queue, se, sk
     if (dump_m)
-        launch_pdl(k_blend_tc<true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
+        launch_pdl(k_blend_tc<true, false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
+    else if (colour_mma && stats)
+        launch_pdl(k_blend_tc<false, true, false, true>, grid, TC_THREADS, smem_c, st, ARGS, nullptr, m_rgb, m_T, tma);
+    else if (colour_mma)
+        launch_pdl(k_blend_tc<false, false, false, true>, grid, TC_THREADS, smem_c, st, ARGS, nullptr, m_rgb, m_T,
+                   tma);
     else if (stats)
-        launch_pdl(k_blend_tc<false, true, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
+        launch_pdl(k_blend_tc<false, true, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
     else if (g_blend_trace)
-        launch_pdl(k_blend_tc<false, false, true>, grid, TC_THREADS, smem, st, ARGS, g_blend_trace, m_rgb, m_T, tma);
+        launch_pdl(k_blend_tc<false, false, true, false>, grid, TC_THREADS, smem, st, ARGS, g_blend_trace, m_rgb, m_T,
+                   tma);
     else
-        launch_pdl(k_blend_tc<false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
+        launch_pdl(k_blend_tc<false, false, false, false>, grid, TC_THREADS, smem, st, ARGS, nullptr, m_rgb, m_T, tma);
 #undef ARGS
 }
 

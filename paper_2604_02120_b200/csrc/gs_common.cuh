@@ -397,9 +397,9 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
 int launch_binning(Workspace &ws, cudaStream_t st, int N, int64_t max_keys, int ntiles, int gx,
                    uint32_t &epoch, bool tight, float znear, bool concurrent, bool supertile);
 int supertile_count(int gx, int gy);   // 4 x 4-tile supertiles of a gx x gy tile grid
-void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0, int ntiles, int gx, int W,
-                     int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m, int num_sms,
-                     bool stats);
+void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, const TileLists &lists, int tile0,
+                     int ntiles, int gx, int W, int H, const float bg[3], float *out_rgb, float *out_T, float *dump_m,
+                     int num_sms, bool stats, bool colour_mma);
 extern long long *g_blend_trace;
 void launch_blend_mma(const Workspace &ws, cudaStream_t st, const Splat *splat, const uint32_t *vals, const uint2 *ranges, int tile0, int ntiles, int gx,
                       int W, int H, const float bg[3], float *out_rgb, float *out_T, int num_sms, int batch);

@@ -135,7 +135,7 @@ int validate(gs_ctx *c, int N, const void *means, const void *scales, const void
     if (W > c->max_w || H > c->max_h) return GS_ERR_INVALID_ARG;
     if (N > c->max_points) return GS_ERR_CAPACITY;
     if (o->sh_degree > 3 || o->sh_degree < -1) return GS_ERR_INVALID_ARG;
-    if (o->blend < GS_BLEND_TC || o->blend > GS_BLEND_MMA) return GS_ERR_INVALID_ARG;
+    if (o->blend < GS_BLEND_TC || o->blend > GS_BLEND_TC_COLOR) return GS_ERR_INVALID_ARG;
     if (o->batch != 0 && o->batch != 32 && o->batch != 64 && o->batch != 128 && o->batch != 256)
         return GS_ERR_INVALID_ARG;
     if (o->n_bands < 0 || (o->n_bands > 1 && (o->band < 0 || o->band >= o->n_bands)))
@@ -204,7 +204,7 @@ void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const 
                      const gs_opts &o, bool concurrent = false) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     // the tcgen05 blend filters supertile lists itself; the other blends read per-tile lists
-    const bool super = o.blend == GS_BLEND_TC && gs::supertile_count(gx, gy) <= 512;
+    const bool super = (o.blend == GS_BLEND_TC || o.blend == GS_BLEND_TC_COLOR) && gs::supertile_count(gx, gy) <= 512;
     w.list_sgx = super ? gs::ceil_div_i(gx, 4) : 0;
     c->launches += gs::launch_binning(w, st, N, c->max_keys, gx * gy, gx, c->epoch, (o.flags & GS_FLAG_TIGHT) != 0,
                                       cam.znear, concurrent, super);
@@ -212,7 +212,8 @@ void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const 
 
 // preprocess + binning of one view into the context's workspace (counters zeroed first)
 int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const float *scales, const float *rots,
-                  const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o) {
+                  const float *opacity, const float *shs, const gs_camera &cam, int W, int H, const gs_opts &o,
+                  bool debug = false) {
     const int e0 = mark(c, st, o);
     cudaMemsetAsync(c->sticky, 0, sizeof(gs::Sticky), st);   // this call's error accumulator
     c->last_sticky = c->sticky;
@@ -220,7 +221,7 @@ int enqueue_front(gs_ctx *c, cudaStream_t st, int N, const float *means, const f
     int y0 = 0, y1 = 0;
     gs::band_rows(gs::ceil_div_i(H, GS_TILE), o.band, o.n_bands, y0, y1);
     gs::launch_preprocess(c->ws, st, N, means, scales, rots, opacity, shs, o.sh_degree, o.sh_stride,
-                          o.scale_modifier, cam, W, H, gs::intersect_mode(o.flags), false, y0, y1);
+                          o.scale_modifier, cam, W, H, gs::intersect_mode(o.flags), debug, y0, y1);
     c->launches += N > 0 ? 1 : 0;
     const int e1 = mark(c, st, o);
     enqueue_binning(c, c->ws, st, N, cam, W, H, o);
@@ -252,8 +253,8 @@ void enqueue_blend(gs_ctx *c, const gs::Workspace &w, cudaStream_t st, const gs:
         gs::launch_blend_mma(w, st, splat, vals, ranges, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
                              c->num_sms, o.batch);
     else
-        gs::launch_blend_tc(w, st, splat, lists, t0, t1, gx, W, H, o.bg, out_rgb, out_T,
-                            dump, c->num_sms, (o.flags & GS_FLAG_STATS) != 0);
+        gs::launch_blend_tc(w, st, splat, lists, t0, t1, gx, W, H, o.bg, out_rgb, out_T, dump, c->num_sms,
+                            (o.flags & GS_FLAG_STATS) != 0, o.blend == GS_BLEND_TC_COLOR);
     c->launches += 1;
 }
 
@@ -947,7 +948,7 @@ int gs_debug_binning(gs_ctx *c, void *stream, int N, const float *means3D, const
     if (!n_keys || !ranges) return GS_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o);
+    enqueue_front(c, st, N, means3D, scales, rots, opacity, shs, *cam, W, H, *o, true);   // + debug outputs
     c->last_stream = st;
     gs_stats s;
     rc = gs_last_stats(c, &s);

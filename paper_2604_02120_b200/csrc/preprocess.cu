@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
             sh_colour(K, sh_degree, px, py, pz, cam, col);
         }
         // 12. outputs (slot-addressed)
-        out.orig[slot] = (uint32_t)i;
+        if (out.orig) out.orig[slot] = (uint32_t)i;   // debug outputs only
         out.depth_bits[slot] = __float_as_uint(vz);
         {   // the blend's 48-B record: three 16-B stores
             float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
 }
 
 PreOut pre_out_of(const Workspace &ws, bool with_radius) {
-    return PreOut{ws.wcount, ws.orig, ws.depth_bits, ws.splat, ws.rect, ws.touched, ws.tmask,
+    return PreOut{ws.wcount, with_radius ? ws.orig : nullptr, ws.depth_bits, ws.splat, ws.rect, ws.touched, ws.tmask,
                   with_radius ? ws.radius : nullptr, ws.counters};
 }
 

@@ -2,9 +2,10 @@
 
 Runs the render path through the C-ABI on small seeded cases so that
 `compute-sanitizer --tool {memcheck,synccheck,initcheck,racecheck}` can watch
-every kernel: the three blends (tcgen05 mbarrier/TMEM pipeline, mma.sync,
-CUDA-core direct), both intersection modes, the binning chain (one-level and
-two-level paths), a concurrent view group and the asynchronous host entry point.
+every kernel: the four blends (tcgen05 mbarrier/TMEM pipeline with the supertile
+list filter and the TMA frame store, its colour-MMA variant, mma.sync, CUDA-core
+direct), both intersection modes, the binning chains (supertile, two-level and
+one-level), a concurrent view group and the asynchronous host entry point.
 
     compute-sanitizer --tool memcheck python tests/sanitize_cases.py [--quick]
 
@@ -25,10 +26,10 @@ sys.path.insert(0, os.path.dirname(HERE))
 import torch  # noqa: E402
 
 from cases import CASES  # noqa: E402
-from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_FLAG_OBOX, Context,  # noqa: E402
-                                   camera, opts, scene_to_device, scene_to_host, synth)
+from paper_2604_02120_b200 import (GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_BLEND_TC_COLOR,  # noqa: E402
+                                   GS_FLAG_OBOX, Context, camera, opts, scene_to_device, scene_to_host, synth)
 
-BLENDS = {"tc": GS_BLEND_TC, "mma": GS_BLEND_MMA, "direct": GS_BLEND_DIRECT}
+BLENDS = {"tc": GS_BLEND_TC, "mma": GS_BLEND_MMA, "direct": GS_BLEND_DIRECT, "tc_color": GS_BLEND_TC_COLOR}
 
 
 def _opts(scene, bg, blend, flags, batch=0):

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GsError, synth
+from paper_2604_02120_b200 import GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_BLEND_TC_COLOR, GsError, synth
 
 from cases import CASES, _adversarial, _cfg, _dense, _ragged, _wide  # noqa: F401
 from gpu_util import (MAX_ABS, MIN_PSNR, check_frame, exponent_errors, gpu_binning, gpu_blend_from, gpu_preprocess,
@@ -53,7 +53,8 @@ def test_binning_bit_exact(case, lists):
     assert np.array_equal(got["ranges"], ref["ranges"])
 
 
-@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA], ids=["tc", "direct", "mma"])
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC_COLOR],
+                         ids=["tc", "direct", "mma", "tc_color"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_blend_parity_on_oracle_binning(case, blend):
     """Stage (d) alone: oracle splats + oracle binning uploaded by the harness."""
@@ -61,10 +62,11 @@ def test_blend_parity_on_oracle_binning(case, blend):
     ctx = make_ctx(scene, cam)
     pre, b, ref = oracle.render(scene, cam, bg)
     rgb, T = gpu_blend_from(ctx, pre, b, cam.W, cam.H, bg, blend)
-    check_frame(f"blend_only/{case}/{['tc', 'direct', 'mma'][blend]}", rgb, T, ref)
+    check_frame(f"blend_only/{case}/{['tc', 'direct', 'mma', 'tc_color'][blend]}", rgb, T, ref)
 
 
-@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA], ids=["tc", "direct", "mma"])
+@pytest.mark.parametrize("blend", [GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC_COLOR],
+                         ids=["tc", "direct", "mma", "tc_color"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_render_parity_end_to_end(case, blend):
     scene, cam, bg = CASES[case]()
@@ -72,7 +74,7 @@ def test_render_parity_end_to_end(case, blend):
     rgb, T = gpu_render(ctx, scene, cam, bg, blend)
     assert np.isfinite(rgb).all() and np.isfinite(T).all()
     _, _, ref = oracle.render(scene, cam, bg)
-    check_frame(f"end_to_end/{case}/{['tc', 'direct', 'mma'][blend]}", rgb, T, ref)
+    check_frame(f"end_to_end/{case}/{['tc', 'direct', 'mma', 'tc_color'][blend]}", rgb, T, ref)
 
 
 @pytest.mark.parametrize("case", list(CASES))
@@ -696,7 +698,7 @@ def test_degenerate_image_and_scene_sizes(wh, n):
         for blend in (GS_BLEND_TC, GS_BLEND_DIRECT, GS_BLEND_MMA):
             rgb, T = gpu_render(ctx, scene, cam, bg, blend, flags=flags)
             _, _, ref = oracle.render(scene, cam, bg, obox=obox)
-            check_frame(f"degenerate/{W}x{H}/n{n}/{'obox' if obox else 'vanilla'}/{['tc', 'direct', 'mma'][blend]}",
+            check_frame(f"degenerate/{W}x{H}/n{n}/{'obox' if obox else 'vanilla'}/{['tc', 'direct', 'mma', 'tc_color'][blend]}",
                         rgb, T, ref)
 
 
