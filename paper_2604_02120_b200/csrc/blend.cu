@@ -231,9 +231,12 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                float *__restrict__ dump_m, uint32_t *tile_queue, unsigned long long *stat_eval,
                unsigned long long *stat_kept, long long *trace, const __grid_constant__ CUtensorMap tm_rgb,
                const __grid_constant__ CUtensorMap tm_T, int tma_out) {
-    extern __shared__ uint8_t smem_raw[];
+    // used as is (no pointer arithmetic), so every access compiles to LDS/STS rather than
+    // generic loads; the dynamic window starts 1024-B aligned (checked: TMA needs 128 B)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     using SM = std::conditional_t<CM, SmemTCC, SmemTC>;
-    SM &sm = *reinterpret_cast<SM *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    SM &sm = *reinterpret_cast<SM *>(smem_raw);
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u)) __trap();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NCOLS = CM ? CM_TMEM_COLS : TMEM_COLS;
     static_assert(!CM || NBLD == 1, "the colour MMA follows the single builder's batch order");
@@ -977,8 +980,8 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
     k_blend_mma(const Splat *__restrict__ splat, const uint32_t *__restrict__ vals, const uint2 *__restrict__ ranges, int tile0, int ntiles, int gx,
                 int W, int H, float bg0, float bg1, float bg2, float *__restrict__ out_rgb, float *__restrict__ out_T,
                 uint32_t *tile_queue) {
-    extern __shared__ uint8_t smem_raw[];
-    SmemMMA<BATCH> &sm = *reinterpret_cast<SmemMMA<BATCH> *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    SmemMMA<BATCH> &sm = *reinterpret_cast<SmemMMA<BATCH> *>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, r4 = lane >> 2;
     // compositor pixel of this thread = buffer row `lane` of its warp
     int x, y;
