@@ -3,26 +3,34 @@
 // synchronisation: every count stays on the device, so a frame is
 // graph-capturable).
 //
-// Canonical result (R-12/R-13): the (Gaussian, tile) pairs sorted by
-// key = tile << 32 | depth bits, ties by Gaussian index. The paper's
-// "duplicate with a concatenated key, then radix-sort" over 64-bit
-// keys costs ~6 LSD passes over every pair; here the depth half is sorted once
-// per *Gaussian* instead of once per pair:
-//   1. compaction of the visible Gaussians (order-preserving scan)
-//   2. stable LSD sort of the N_vis depth keys, 4 passes of 8 bits (ties keep
-//      index order)
-//   3. scan of tiles_touched in depth order -> pair offsets, K, capacity check,
-//      and the first Gaussian of every 4096-pair chunk
-//   4. stable LSD sort of the pairs on the tile id (1-2 passes of 8 bits); the
-//      first pass *generates* the pairs in depth order from the offsets
-//      (load-balanced expansion: max-scan of segment heads), so the duplicated
-//      array is never materialised unsorted
-//   5. tile ranges by boundary detection.
-// Every scan / radix pass is reduce-then-scan over 4096-element chunks:
-// count (per-warp ballot multisplit, no atomics) -> scan of the
-// [digit][chunk] count matrix -> stable scatter through shared memory. No
-// block ever waits on another block (a decoupled look-back variant spent
-// most of its time spinning on its predecessors).
+// Canonical result (R-12/R-13): each tile's Gaussians in the order of
+// key = tile << 32 | depth bits, ties by Gaussian index. The paper's "duplicate
+// with a concatenated key, then radix-sort" over 64-bit keys costs
+// ~6 LSD passes over every pair; here the depth half is sorted once per
+// *Gaussian* instead of once per pair:
+//   1. compaction of the visible Gaussians (order-preserving scan), keys relative
+//      to the near plane
+//   2. stable LSD sort of the N_vis depth keys, 3 passes of 9 bits (a 4th pass
+//      only if a depth key reaches 2^27; ties keep index order); the last pass
+//      gathers each Gaussian's rect into depth order
+//   3. the tile grouping, in one of two forms:
+//      a. supertile lists (the tcgen05 blend, grids <= 512 supertiles): the
+//         depth-ordered Gaussians expanded to (4x4-tile supertile, Gaussian) pairs
+//         with a 16-bit tile mask each, ONE stable 9-bit pass on the supertile id
+//         (expansion fused into its count and scatter), ranges from the digit
+//         totals; a tile's list is its supertile's list filtered by its mask bit,
+//         which the blend's producer does on the fly;
+//      b. per-tile lists (the other blends, larger grids): two-level -- tile-row
+//         entries, one stable pass on the row, pair offsets, one stable pass on the
+//         column with the tile ranges from the column counts -- or, for grids wider
+//         or taller than 512 tiles, one-level (all K (tile, index) pairs, ceil(tile
+//         bits / 8) stable passes, ranges by boundary detection).
+// Every scan / radix pass is reduce-then-scan over 3072-element chunks: count
+// (shared-memory histograms, or run-length difference arrays for the expanding
+// loaders) -> scan of the [digit][chunk] count matrix (one block per digit) ->
+// stable scatter through shared memory with warp-ballot ranks. No block ever
+// waits on another block (a decoupled look-back variant spent most of its time
+// spinning on its predecessors).
 #include <algorithm>
 #include <cstring>
 

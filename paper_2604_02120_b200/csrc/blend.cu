@@ -75,6 +75,9 @@ constexpr int RING = 2 * STAGES;   // colour / header slots (see SLOTS below)
 #ifndef GS_BLEND_LPF
 #define GS_BLEND_LPF 1
 #endif
+#ifndef GS_BLEND_L1PF
+#define GS_BLEND_L1PF 0    // 1: prefetch the list round after the held one into L1 (no gain: r2_sweep_k)
+#endif
 #ifndef GS_BLEND_HPF
 #define GS_BLEND_HPF 1     // 1: fetch the next tile's first list round during the current tile
 #endif
@@ -417,18 +420,26 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                 const uint32_t km = ((lk[0].x & kbit) ? 1u : 0u) | ((lk[0].y & kbit) ? 2u : 0u) |
                                     ((lk[0].z & kbit) ? 4u : 0u) | ((lk[0].w & kbit) ? 8u : 0u);
                 const uint32_t c = (uint32_t)__popc(km);
-                uint32_t x = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= (uint32_t)o) x += y;
+                // exclusive prefix of the per-lane counts (0..4) from three ballots of their bits:
+                // independent votes instead of a 5-step dependent shuffle scan
+                const uint32_t b0 = __ballot_sync(0xffffffffu, c & 1u), b1 = __ballot_sync(0xffffffffu, c & 2u),
+                               b2 = __ballot_sync(0xffffffffu, c & 4u);
+                if (b0 | b1 | b2) {
+                    const uint32_t lt = lanemask_lt_u32();
+                    uint32_t w = tail + __popc(b0 & lt) + 2u * __popc(b1 & lt) + 4u * __popc(b2 & lt);
+                    if (km & 1u) sm.lq[w++ & (LQ - 1)] = lv[0].x;
+                    if (km & 2u) sm.lq[w++ & (LQ - 1)] = lv[0].y;
+                    if (km & 4u) sm.lq[w++ & (LQ - 1)] = lv[0].z;
+                    if (km & 8u) sm.lq[w & (LQ - 1)] = lv[0].w;
+                    tail += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
                 }
-                uint32_t w = tail + x - c;
-                if (km & 1u) sm.lq[w++ & (LQ - 1)] = lv[0].x;
-                if (km & 2u) sm.lq[w++ & (LQ - 1)] = lv[0].y;
-                if (km & 4u) sm.lq[w++ & (LQ - 1)] = lv[0].z;
-                if (km & 8u) sm.lq[w & (LQ - 1)] = lv[0].w;
-                tail += __shfl_sync(0xffffffffu, x, 31);
+                if (GS_BLEND_L1PF) {   // the round after the next one into L1 (no registers held)
+                    const uint32_t e = pos + 128u * (LPF + 1) + 4u * lane;
+                    if (e < rg.y) {
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(lists.vals + e));
+                        if (st_mode) asm volatile("prefetch.global.L1 [%0];" ::"l"(lists.keys + e));
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j + 1 < LPF; j++) {
                     lk[j] = lk[j + 1];

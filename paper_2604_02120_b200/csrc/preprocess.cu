@@ -114,9 +114,9 @@ __device__ __forceinline__ void cov3d(const float4 &q, float s0, float s1, float
 
 // Step 11: SH colour for the view direction normalize(p - campos).
 template <class KF>
-__device__ __forceinline__ void sh_colour(KF k, int sh_degree, float px, float py, float pz, float cx, float cy,
-                                          float cz, float (&res3)[3]) {
-    const float dx = px - cx, dy = py - cy, dz = pz - cz;
+__device__ __forceinline__ void sh_colour(KF k, int sh_degree, float px, float py, float pz,
+                                          const gs_camera &cam, float (&res3)[3]) {
+    const float dx = px - cam.campos[0], dy = py - cam.campos[1], dz = pz - cam.campos[2];
     const float len = sqrtf(__fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx)));
     const float il = 1.0f / len;
     const float X = dx * il, Y = dy * il, Z = dz * il;
@@ -196,9 +196,6 @@ __device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c
     return xmax > xmin && ymax > ymin;
 }
 
-#ifndef GS_PRE_COMPACT
-#define GS_PRE_COMPACT 1   // SH colours of the warp's visible (Gaussian, view) pairs in packed rounds
-#endif
 #ifndef GS_PRE_MINB
 #define GS_PRE_MINB 4   // 64 registers, 4 x 48 KB SH staging per SM (3: 0.138 ms, 4: 0.128 ms per view)
 #endif
@@ -213,19 +210,6 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i == 0)   // the frames' device counters (no memset node: keeps PDL chained)
         for (int v = 0; v < pv.n; v++) *pv.out[v].counters = Counters{};
-    // per view: the SH origin and the splat array, for the colour rounds below (a lane
-    // there may work on any view, so they come from shared memory, not the parameters)
-    __shared__ float s_campos[MAX_VIEW_GROUP][3];
-    __shared__ Splat *s_splat[MAX_VIEW_GROUP];
-    // per warp: the (Gaussian lane, view, slot rank) items whose colour is still to compute
-    __shared__ uint32_t s_q[PRE_THREADS / 32][64];
-    if (threadIdx.x < (unsigned)pv.n) {
-        s_campos[threadIdx.x][0] = pv.cam[threadIdx.x].campos[0];
-        s_campos[threadIdx.x][1] = pv.cam[threadIdx.x].campos[1];
-        s_campos[threadIdx.x][2] = pv.cam[threadIdx.x].campos[2];
-        s_splat[threadIdx.x] = pv.out[threadIdx.x].splat;
-    }
-    __syncthreads();
     if ((i & ~31) >= N) return;   // whole warps only: the slot packing below votes per warp
     const bool in = i < N;
     const uint32_t lane = threadIdx.x & 31u;
@@ -239,30 +223,9 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
     float S[3][3];
     bool have_cov = false, have_sh = false;
     // the SH record, once loaded, lives in shared memory (coefficient-major: conflict-free)
-    // rather than in 48 registers, so the kernel keeps 4 blocks per SM (dynamic: 48 KB)
-    extern __shared__ float s_sh_dyn[];
-    float(*s_sh)[PRE_THREADS] = reinterpret_cast<float(*)[PRE_THREADS]>(s_sh_dyn);
-    const uint32_t wbase = threadIdx.x & ~31u;
-    uint32_t *const cq = s_q[threadIdx.x >> 5];
-    uint32_t q_head = 0, q_tail = 0;   // warp-uniform
-    // Step 11 for a round of queued (Gaussian, view) pairs, one per lane (cnt <= 32): the
-    // visible pairs of the warp's views are packed into full warps, where a per-view pass
-    // left ~half of the lanes idle (a Gaussian is visible in ~53 % of the C5 views)
-    auto colour_round = [&](uint32_t cnt) {
-        const uint32_t it = lane < cnt ? cq[(q_head + lane) & 63u] : 0u;
-        const uint32_t g = it & 31u, v = (it >> 5) & 63u, rank = it >> 11;
-        const float gx_ = __shfl_sync(0xffffffffu, px, (int)g);
-        const float gy_ = __shfl_sync(0xffffffffu, py, (int)g);
-        const float gz_ = __shfl_sync(0xffffffffu, pz, (int)g);
-        if (lane < cnt) {
-            float col[3];
-            sh_colour([&](int j) { return s_sh[j][wbase + g]; }, sh_degree, gx_, gy_, gz_, s_campos[v][0],
-                      s_campos[v][1], s_campos[v][2], col);
-            reinterpret_cast<float4 *>(s_splat[v] + (i & ~31) + rank)[2] = make_float4(col[0], col[1], col[2], 0.f);
-        }
-        q_head += cnt;
-        __syncwarp();
-    };
+    // rather than in 48 registers, so the kernel keeps 3 blocks per SM
+    __shared__ float s_sh[48][PRE_THREADS];
+    auto K = [&](int j) { return s_sh[j][threadIdx.x]; };
 
 #pragma unroll 1
     for (int view = 0; view < pv.n; view++) {
@@ -342,63 +305,50 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         // culled ones write nothing (dense writes, no partial-sector fills but one per warp)
         const uint32_t bal = __ballot_sync(0xffffffffu, vis);
         if (lane == 0) out.wcount[i >> 5] = __popc(bal);
-        if (vis) {
-            const uint32_t rank = __popc(bal & ((1u << lane) - 1u));
-            const int slot = (i & ~31) + (int)rank;
-            if (tight) out.tmask[slot] = tm;
-            // 11. colour: plain colours here; SH (its record staged once per Gaussian, by its
-            //     first visible view) in the colour rounds
-            float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
-            if (sh_degree < 0) {
-                d[2] = make_float4(shs[3 * (size_t)i], shs[3 * (size_t)i + 1], shs[3 * (size_t)i + 2], 0.f);
-            } else {
-                if (!have_sh) {
-                    const int ncoef = (sh_degree + 1) * (sh_degree + 1);
-                    const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
-                    if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
-                        const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
+        if (!vis) continue;
+        const int slot = (i & ~31) + __popc(bal & ((1u << lane) - 1u));
+        if (tight) out.tmask[slot] = tm;
+        // 11. colour
+        float col[3];
+        if (sh_degree < 0) {
+            col[0] = shs[3 * (size_t)i]; col[1] = shs[3 * (size_t)i + 1]; col[2] = shs[3 * (size_t)i + 2];
+        } else {
+            if (!have_sh) {   // the SH record is read once per Gaussian, by its first visible view
+                const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+                const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
+                if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
+                    const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
 #pragma unroll
-                        for (int j = 0; j < 12; j++) {
-                            if (4 * j < ncoef * 3) {
-                                const float4 t4 = __ldcs(sh4 + j);
-                                s_sh[4 * j][threadIdx.x] = t4.x; s_sh[4 * j + 1][threadIdx.x] = t4.y;
-                                s_sh[4 * j + 2][threadIdx.x] = t4.z; s_sh[4 * j + 3][threadIdx.x] = t4.w;
-                            }
+                    for (int j = 0; j < 12; j++) {
+                        if (4 * j < ncoef * 3) {
+                            const float4 t4 = __ldcs(sh4 + j);
+                            s_sh[4 * j][threadIdx.x] = t4.x; s_sh[4 * j + 1][threadIdx.x] = t4.y;
+                            s_sh[4 * j + 2][threadIdx.x] = t4.z; s_sh[4 * j + 3][threadIdx.x] = t4.w;
                         }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 48; j++)
-                            if (j < ncoef * 3) s_sh[j][threadIdx.x] = __ldg(sh + j);
                     }
-                    have_sh = true;
-                }
-                if (GS_PRE_COMPACT) {
-                    cq[(q_tail + rank) & 63u] = lane | ((uint32_t)view << 5) | (rank << 11);
                 } else {
-                    float col[3];
-                    sh_colour([&](int j) { return s_sh[j][threadIdx.x]; }, sh_degree, px, py, pz, cam.campos[0],
-                              cam.campos[1], cam.campos[2], col);
-                    d[2] = make_float4(col[0], col[1], col[2], 0.f);
+#pragma unroll
+                    for (int j = 0; j < 48; j++)
+                        if (j < ncoef * 3) s_sh[j][threadIdx.x] = __ldg(sh + j);
                 }
+                have_sh = true;
             }
-            // 12. outputs (slot-addressed)
-            if (out.orig) out.orig[slot] = (uint32_t)i;   // debug outputs only
-            out.depth_bits[slot] = __float_as_uint(vz);
-            d[0] = make_float4(mx, my, 0.f, 0.f);   // the blend's 48-B record (colour: d[2])
+            sh_colour(K, sh_degree, px, py, pz, cam, col);
+        }
+        // 12. outputs (slot-addressed)
+        if (out.orig) out.orig[slot] = (uint32_t)i;   // debug outputs only
+        out.depth_bits[slot] = __float_as_uint(vz);
+        {   // the blend's 48-B record: three 16-B stores
+            float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
+            d[0] = make_float4(mx, my, 0.f, 0.f);
             d[1] = make_float4(cA, cB, cC, op);
-            out.rect[slot] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
-                                          (unsigned short)ymax);
-            out.touched[slot] = n_tiles;
-            if (out.radius) out.radius[slot] = r;
+            d[2] = make_float4(col[0], col[1], col[2], 0.f);
         }
-        if (GS_PRE_COMPACT && sh_degree >= 0) {
-            q_tail += (uint32_t)__popc(bal);
-            __syncwarp();
-            if (q_tail - q_head >= 32u) colour_round(32u);
-        }
+        out.rect[slot] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
+                                      (unsigned short)ymax);
+        out.touched[slot] = n_tiles;
+        if (out.radius) out.radius[slot] = r;
     }
-    if (GS_PRE_COMPACT && sh_degree >= 0)
-        while (q_tail != q_head) colour_round(min(32u, q_tail - q_head));
 }
 
 PreOut pre_out_of(const Workspace &ws, bool with_radius) {
@@ -410,13 +360,7 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
                              int sh_stride, float scale_mod, int W, int H, int imode) {
     if (N <= 0) return;
-    constexpr size_t smem = sizeof(float) * 48 * PRE_THREADS;   // the SH staging
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_preprocess, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, smem, st,
+    launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
         N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
         H, pv, imode);
 }
