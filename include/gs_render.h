@@ -93,6 +93,10 @@ enum {
                            * Safe with interleaved single-view calls: the view-group calls use
                            * their own workspaces and error accumulator, never the ones of
                            * gs_render / gs_debug_* (which run in the caller's stream order). */
+    GS_FLAG_TILE_LISTS = 64u, /* GS_BLEND_TC(_COLOR): bin into per-tile lists (the two-level
+                           * row / column passes) instead of the 4x4-tile supertile lists the
+                           * blend filters itself; for kernel A/Bs on the lists the other blends
+                           * read. Frames are identical either way.                          */
     GS_FLAG_OBOX = 16u    /* opacity-aware box (cheaper): the vanilla rect clipped to the
                            * bounding box of the ellipse where alpha >= 1/255 can hold (margin
                            * 5e-3 in ln alpha), and Gaussians with 255*opacity < 1 culled; no

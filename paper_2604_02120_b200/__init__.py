@@ -7,6 +7,6 @@ holds only the thin ctypes binding (_binding.py) and the seeded synthetic
 input generators (synth.py).
 """
 from . import synth  # noqa: F401
-from ._binding import (GS_ERR_CAPACITY, GS_ERR_CUDA, GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_BLEND_TC_COLOR, GS_FLAG_STATS, GS_FLAG_SYNC, GS_FLAG_OBOX, GS_FLAG_STATIC_SCENE, GS_FLAG_TIGHT, GS_FLAG_TIMING,  # noqa: F401
+from ._binding import (GS_ERR_CAPACITY, GS_ERR_CUDA, GS_BLEND_DIRECT, GS_BLEND_MMA, GS_BLEND_TC, GS_BLEND_TC_COLOR, GS_FLAG_STATS, GS_FLAG_SYNC, GS_FLAG_OBOX, GS_FLAG_STATIC_SCENE, GS_FLAG_TIGHT, GS_FLAG_TILE_LISTS, GS_FLAG_TIMING,  # noqa: F401
                        Context, GsError,
                        camera, load, opts, scene_to_device, scene_to_host)

@@ -34,6 +34,7 @@ GS_FLAG_STATS = 4
 GS_FLAG_TIGHT = 8
 GS_FLAG_OBOX = 16
 GS_FLAG_STATIC_SCENE = 32
+GS_FLAG_TILE_LISTS = 64
 
 # every entry point declared in include/gs_render.h
 EXPORTS = ("gs_ctx_create", "gs_ctx_destroy", "gs_render", "gs_render_views", "gs_render_views_host",

@@ -1456,11 +1456,28 @@ struct StLoader : LinearChunks {
             }
             const uint32_t x0 = rxy & 0xFFFFu, y0 = rxy >> 16, x1 = rzw & 0xFFFFu, y1 = rzw >> 16;
             if (GS_ST_SERIAL && len > 0 && len <= SERIAL_MAX) {
-                const uint32_t sw = (x1 - 1u) / ST_SIDE + 1u - x0 / ST_SIDE;
+                const uint32_t sx0 = x0 / ST_SIDE, sx1 = (x1 - 1u) / ST_SIDE, sy0 = y0 / ST_SIDE;
+                const uint32_t sy1 = (y1 - 1u) / ST_SIDE, sw = sx1 + 1u - sx0;
                 uint32_t qy = q0 ? udiv_small(q0, sw) : 0u;
                 uint32_t qx = q0 - qy * sw;
+                const bool plain = m == ~0ull || (x1 - x0) * (y1 - y0) > 64u;
+                // the rect's tiles in its first / last supertile column and row (the inner
+                // ones hold all four): the mask of supertile (sx, sy) is a 4-bit column
+                // pattern times a 0x1111-pattern of rows (no carries)
+                const uint32_t cf = (0xFu << (x0 & 3u)) & 0xFu, cl = 0xFu >> (3u - ((x1 - 1u) & 3u));
+                const uint32_t rf = (0x1111u << (4u * (y0 & 3u))) & 0xFFFFu;
+                const uint32_t rl = 0xFFFFu >> (4u * (3u - ((y1 - 1u) & 3u)));
                 for (uint32_t j = 0; j < len; j++) {
-                    sk[slot0 + j] = key_of(x0, y0, x1, y1, qx, qy, m);
+                    const uint32_t sx = sx0 + qx, sy = sy0 + qy;
+                    uint32_t mk;
+                    if (plain) {
+                        const uint32_t cm = (sx == sx0 ? cf : 0xFu) & (sx == sx1 ? cl : 0xFu);
+                        const uint32_t rm = (sy == sy0 ? rf : 0x1111u) & (sy == sy1 ? rl : 0xFFFFu);
+                        mk = cm * rm;
+                    } else {
+                        mk = st_mask(x0, y0, x1, y1, sx, sy, m);
+                    }
+                    sk[slot0 + j] = (sy * (uint32_t)sgx + sx) | (mk << 16);
                     if (sv) sv[slot0 + j] = idx;
                     if (++qx == sw) {
                         qx = 0;

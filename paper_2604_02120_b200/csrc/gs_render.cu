@@ -204,7 +204,8 @@ void enqueue_binning(gs_ctx *c, gs::Workspace &w, cudaStream_t st, int N, const 
                      const gs_opts &o, bool concurrent = false) {
     const int gx = gs::ceil_div_i(W, GS_TILE), gy = gs::ceil_div_i(H, GS_TILE);
     // the tcgen05 blend filters supertile lists itself; the other blends read per-tile lists
-    const bool super = (o.blend == GS_BLEND_TC || o.blend == GS_BLEND_TC_COLOR) && gs::supertile_count(gx, gy) <= 512;
+    const bool super = (o.blend == GS_BLEND_TC || o.blend == GS_BLEND_TC_COLOR) && !(o.flags & GS_FLAG_TILE_LISTS) &&
+                       gs::supertile_count(gx, gy) <= 512;
     w.list_sgx = super ? gs::ceil_div_i(gx, 4) : 0;
     c->launches += gs::launch_binning(w, st, N, c->max_keys, gx * gy, gx, c->epoch, (o.flags & GS_FLAG_TIGHT) != 0,
                                       cam.znear, concurrent, super);
