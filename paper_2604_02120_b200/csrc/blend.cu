@@ -60,6 +60,9 @@ namespace gs {
 #ifndef GS_BLEND_NB
 #define GS_BLEND_NB 32
 #endif
+#ifndef GS_BLEND_STALE_THR
+#define GS_BLEND_STALE_THR 1   // 1: the compositors' skip threshold changes only between 16-column chunks
+#endif
 constexpr int NB = GS_BLEND_NB;         // Gaussians per batch (MMA N: 16 or 32)
 #ifndef GS_BLEND_KSTEPS
 #define GS_BLEND_KSTEPS 2   // K = 8 * KSTEPS: 2 = TF32 hi/lo (R-11); 1 = single TF32 pass (A/B evidence only)
@@ -97,7 +100,7 @@ static_assert(TMEM_COLS >= 32 && (TMEM_COLS & (TMEM_COLS - 1)) == 0 && GS_BLEND_
 //   colour/header slot b % RING. A builder writes stage/slot of batch b only
 // after the MMA of batch b - STAGES completed, which required every compositor
 // warp to release batch b - 2*STAGES: RING = 2*STAGES slots need no extra wait.
-// Header: {tile, seq, count, list offset}; count 0 = end-of-tile marker,
+// Header: {ty << 16 | tx, seq, count, list offset}; count 0 = end-of-tile marker,
 // count -1 = batch of an already terminated tile (skipped), tile -1 = terminal.
 
 #ifndef GS_BLEND_BULK
@@ -191,8 +194,8 @@ __device__ __forceinline__ void build_row(SmemTC &sm, int stage, int slot, const
                                           int gx) {
     uint32_t u[16];
     if (lane < hd.z) {
-        const float xc = (float)(GS_TILE * (hd.x % gx)) + 7.5f;
-        const float yc = (float)(GS_TILE * (hd.x / gx)) + 7.5f;
+        const float xc = (float)(GS_TILE * (hd.x & 0xffff)) + 7.5f;   // hd.x = ty << 16 | tx
+        const float yc = (float)(GS_TILE * (hd.x >> 16)) + 7.5f;
         const float xh = rr.m.x - xc, yh = rr.m.y - yc;
         const float A = rr.co.x, B = rr.co.y, C = rr.co.z;
         float v[6];
@@ -344,6 +347,9 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
         int tile = 0;
         if (lane == 0) tile = tile0 + (int)atomicAdd(tile_queue, 1u);   // tiles [tile0, ntiles)
         tile = __shfl_sync(0xffffffffu, tile, 0);
+        // headers carry the tile as ty << 16 | tx (one division per tile here, none per batch)
+        auto tcode_of = [&](int t) { return ((t / gx) << 16) | (t % gx); };
+        int tcode = tcode_of(tile);
         uint2 rg;
         uint32_t kbit;
         tile_list(tile, rg, kbit);
@@ -452,9 +458,10 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
             bool end = tail == head;   // list exhausted, queue empty
             if (!DUMP && !end) end = tile_done(sm, lane, seq);
             if (end) {
-                push(make_int4(tile, (int)seq, 0, 0), 0u);   // end-of-tile marker
+                push(make_int4(tcode, (int)seq, 0, 0), 0u);   // end-of-tile marker
                 while (hstate < 3) head_step();
                 tile = ntile;
+                tcode = tcode_of(tile);
                 rg = nrg;
                 kbit = nkbit;
                 pos = rg.x & ~3u;
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
             const uint32_t cnt = min((uint32_t)NB, tail - head);
             const uint32_t gi = lane < cnt ? sm.lq[(head + lane) & (LQ - 1)] : 0u;
             __syncwarp();   // (the queue slots read here are refilled by later rounds)
-            push(make_int4(tile, (int)seq, (int)cnt, (int)(rg.x + taken)), gi);
+            push(make_int4(tcode, (int)seq, (int)cnt, (int)(rg.x + taken)), gi);
             head += cnt;
             taken += cnt;
         }
@@ -600,6 +607,7 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
         // Pixel state. Termination is encoded in the skip threshold: thr = +inf once the
         // pixel has stopped (R-2), so "live" is a single compare and no bool is carried.
         float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
+        float tmin = T_MIN;   // GS_BLEND_STALE_THR: the stop threshold of T (+inf once stopped)
         bool wdone = false;
         uint32_t n_kept = 0, n_tiles = 0;
         uint32_t n_col = 0, n_acc = 0;    // CM: data batches (W buffers) and tiles with accumulators so far
@@ -670,7 +678,7 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                     fence_proxy_async_smem();
                     asm volatile("bar.sync 2, 256;" ::: "memory");
                     if (threadIdx.x == 0) {
-                        const int x0 = GS_TILE * (hd.x % gx), y0 = GS_TILE * (hd.x / gx);
+                        const int x0 = GS_TILE * (hd.x & 0xffff), y0 = GS_TILE * (hd.x >> 16);
                         tma_store_3d(&tm_rgb, ob, x0, y0, 0);
                         tma_store_2d(&tm_T, ob + 3 * GS_TILE_PIX, x0, y0);
                         bulk_commit_group();
@@ -680,7 +688,7 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                 } else
 #endif
                 if (!DUMP) {
-                    const int px = GS_TILE * (hd.x % gx) + x, py = GS_TILE * (hd.x / gx) + y;
+                    const int px = GS_TILE * (hd.x & 0xffff) + x, py = GS_TILE * (hd.x >> 16) + y;
                     if (px < W && py < H) {
                         const size_t pix = (size_t)py * W + px, plane = (size_t)W * H;
                         out_rgb[pix] = C0 + T * bg0;
@@ -689,7 +697,7 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                         out_T[pix] = T;
                     }
                 }
-                T = 1.0f; C0 = C1 = C2 = 0.f; thr = LOG2_ALPHA_MIN; wdone = false;
+                T = 1.0f; C0 = C1 = C2 = 0.f; thr = LOG2_ALPHA_MIN; tmin = T_MIN; wdone = false;
             } else if (hd.z > 0 && wdone) {
                 if constexpr (CM) {   // W of a finished warp: zeros
                     const uint32_t wb = smem_u32(&sm.Wb[n_col & 1u][warp >> 2][0]);
@@ -711,7 +719,11 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                         for (int j = 0; j < CH && h0 + j < cnt; j++)
                             dump_m[((size_t)hd.w + h0 + j) * GS_TILE_PIX + p] = m[j];
                     } else {
-                        // columns j >= cnt hold the padding exponent -1e30: no count checks needed
+                        // columns j >= cnt hold the padding exponent -1e30: no count checks needed.
+                        // GS_BLEND_STALE_THR: the skip threshold is only updated between chunks
+                        // and a pixel that stops inside the chunk is masked by its stop threshold `tmin`, so the
+                        // skip vote of column j + 1 does not wait for column j's compositing
+                        // (same frames: a stopped pixel never composites again either way)
 #pragma unroll
                         for (int j = 0; j < CH; j++) {
                             const float mj = m[j];
@@ -721,8 +733,14 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                                 const float a = fminf(ALPHA_MAX, ex2_approx(mj));   // alpha = 2^m capped (R-4)
                                 const float tT = fmaf(-a, T, T);                    // T (1 - alpha)
                                 const float w = a * T;
+#if GS_BLEND_STALE_THR
+                                // tmin = +inf once the pixel stopped: one compare tests both
+                                const bool acc = live && tT >= tmin;                // composite (Eq. 1, R-3)
+                                if (STATS) n_kept += (live && tmin < 1.f) ? 1u : 0u;
+#else
                                 const bool acc = live && tT >= T_MIN;               // composite (Eq. 1, R-3)
                                 if (STATS) n_kept += live ? 1u : 0u;
+#endif
                                 if constexpr (CM) {
                                     wv[j] = acc ? w : 0.f;
                                 } else {
@@ -734,9 +752,16 @@ __global__ void __launch_bounds__(TC_THREADS, CM ? 2 : GS_BLEND_MINB)
                                     C2 = acc ? fmaf(w, c.z, C2) : C2;
                                 }
                                 T = acc ? tT : T;
+#if GS_BLEND_STALE_THR
+                                tmin = (live && !acc) ? __int_as_float(0x7f800000) : tmin;   // stop (R-2)
+#else
                                 thr = (live && !acc) ? __int_as_float(0x7f800000) : thr;   // stop (R-2)
+#endif
                             }
                         }
+#if GS_BLEND_STALE_THR
+                        thr = tmin > 1.f ? __int_as_float(0x7f800000) : thr;
+#endif
                         if constexpr (CM) {   // this chunk's 16 W values, TF32 (round to nearest)
                             const uint32_t wb = smem_u32(&sm.Wb[n_col & 1u][warp >> 2][0]);
 #pragma unroll
@@ -1022,6 +1047,7 @@ __global__ void __launch_bounds__(MMA_THREADS, GS_MMA_MINB)
         const uint2 rg = ranges[tile];
         const float xc = (float)(GS_TILE * (tile % gx)) + 7.5f, yc = (float)(GS_TILE * (tile / gx)) + 7.5f;
         float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, thr = LOG2_ALPHA_MIN;
+        float tmin = T_MIN;   // GS_BLEND_STALE_THR: the stop threshold of T (+inf once stopped)
         bool wdone = false;
         // the record of Gaussian b + threadIdx.x is fetched one batch ahead, into registers,
         // so the gathers of batch k+1 overlap the MMAs and compositing of batch k
