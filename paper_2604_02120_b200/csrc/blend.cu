@@ -46,7 +46,8 @@ namespace gs {
 #define GS_BLEND_NBLD 1
 #endif
 #ifndef GS_BLEND_RAW
-#define GS_BLEND_RAW 2   // raw-record ring depth (sweep: 1 / 2 / 3 / 4 -> blend 0.267 / 0.270 / 0.274 / 0.279 ms per view)
+#define GS_BLEND_RAW 1   // raw-record ring depth (round-1 sweep: 1 / 2 / 3 / 4 -> blend 0.267 / 0.270 / 0.274 / 0.279 ms
+                         // per view; round 2 with the supertile producer: 1 vs 2 -> 0.253 vs 0.260-0.263, r2_sweep_m/n)
 #endif
 #ifndef GS_BLEND_MINB
 #define GS_BLEND_MINB 4      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)

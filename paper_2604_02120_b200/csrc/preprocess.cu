@@ -196,9 +196,106 @@ __device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c
     return xmax > xmin && ymax > ymin;
 }
 
+// Steps 5-10 (+ 10b, the row band and the tile-exact mask) of one (Gaussian, view) pair whose
+// view-space point (step 1) passed vz > znear; S: the Gaussian's 3D covariance (steps 2-4).
+struct ViewProj {
+    float mx, my, cA, cB, cC;
+    int r, xmin, ymin, xmax, ymax;
+    uint32_t n_tiles;
+    unsigned long long tm;
+    bool vis;
+};
+__device__ __forceinline__ void project_view(const gs_camera &cam, float vx, float vy, float vz, const float (&S)[3][3],
+                                             float op, int gx, int gy, int imode, int band_y0, int band_y1,
+                                             ViewProj &o) {
+    const float *R = cam.R;
+    o.vis = false;
+    o.mx = o.my = o.cA = o.cB = o.cC = 0.f;
+    o.r = o.xmin = o.xmax = o.ymin = o.ymax = 0;
+    float sxx = 0.f, sxy = 0.f, syy = 0.f;
+    {
+        // 5. clamped Jacobian
+        const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
+        const float iz = 1.0f / vz;
+        const float ux = vx * iz, uy = vy * iz;
+        const float cxz = fminf(lx, fmaxf(-lx, ux));
+        const float cyz = fminf(ly, fmaxf(-ly, uy));
+        const float j00 = cam.fx * iz, j02 = -((cam.fx * cxz) * iz);
+        const float j11 = cam.fy * iz, j12 = -((cam.fy * cyz) * iz);
+        // 6. EWA 2D covariance, T = J R
+        float T[2][3], U[2][3];
+#pragma unroll
+        for (int kk = 0; kk < 3; kk++) {
+            T[0][kk] = __fmaf_rn(j02, R[6 + kk], j00 * R[0 + kk]);
+            T[1][kk] = __fmaf_rn(j12, R[6 + kk], j11 * R[3 + kk]);
+        }
+#pragma unroll
+        for (int a = 0; a < 2; a++)
+#pragma unroll
+            for (int kk = 0; kk < 3; kk++)
+                U[a][kk] = __fmaf_rn(T[a][2], S[2][kk], __fmaf_rn(T[a][1], S[1][kk], T[a][0] * S[0][kk]));
+        const float c00 = __fmaf_rn(U[0][2], T[0][2], __fmaf_rn(U[0][1], T[0][1], U[0][0] * T[0][0]));
+        const float c01 = __fmaf_rn(U[0][2], T[1][2], __fmaf_rn(U[0][1], T[1][1], U[0][0] * T[1][0]));
+        const float c11 = __fmaf_rn(U[1][2], T[1][2], __fmaf_rn(U[1][1], T[1][1], U[1][0] * T[1][0]));
+        const float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
+        // 7. conic
+        const float det = __fmaf_rn(a, c, -(b * b));
+        if (det > 0.0f) {
+            const float id = 1.0f / det;
+            o.cA = c * id; o.cB = -(b * id); o.cC = a * id;
+            sxx = a; sxy = b; syy = c;
+            // 8. radius
+            const float mid = 0.5f * (a + c);
+            const float lam = mid + sqrtf(fmaxf(0.1f, __fmaf_rn(mid, mid, -det)));
+            o.r = (int)ceilf(3.0f * sqrtf(lam));
+            // 9. projected mean
+            o.mx = __fmaf_rn(cam.fx, ux, cam.cx);
+            o.my = __fmaf_rn(cam.fy, uy, cam.cy);
+            // 10. tile rectangle
+            const float rf = (float)o.r;
+            o.xmin = rect_bound((o.mx - rf) / 16.0f, gx);
+            o.xmax = rect_bound(((o.mx + rf) + 15.0f) / 16.0f, gx);
+            o.ymin = rect_bound((o.my - rf) / 16.0f, gy);
+            o.ymax = rect_bound(((o.my + rf) + 15.0f) / 16.0f, gy);
+            o.vis = (o.xmax - o.xmin) * (o.ymax - o.ymin) != 0;
+        }
+    }
+    if (imode == 2 && o.vis) o.vis = opacity_box(o.mx, o.my, sxx, syy, op, gx, gy, o.xmin, o.ymin, o.xmax, o.ymax);
+    if (o.vis && (band_y0 > 0 || band_y1 < gy)) {   // row band of a split frame: its rows only
+        o.ymin = max(o.ymin, band_y0);
+        o.ymax = min(o.ymax, band_y1);
+        o.vis = o.ymax > o.ymin;
+    }
+    o.n_tiles = (uint32_t)((o.xmax - o.xmin) * (o.ymax - o.ymin));
+    o.tm = ~0ull;
+    if (imode == 1 && o.vis)   // the stored rect becomes the opacity-aware box, the mask its kept tiles
+        o.vis = tight_rect(o.mx, o.my, o.cA, o.cB, sxx, sxy, syy, op, gx, gy, o.xmin, o.ymin, o.xmax, o.ymax, o.tm,
+                           o.n_tiles);
+}
+
+// 12. outputs of a visible pair at its slot
+__device__ __forceinline__ void store_view(const PreOut &out, int slot, uint32_t i, float vz, const ViewProj &o,
+                                           float op, const float (&col)[3], bool tight) {
+    if (tight) out.tmask[slot] = o.tm;
+    if (out.orig) out.orig[slot] = i;   // debug outputs only
+    out.depth_bits[slot] = __float_as_uint(vz);
+    {   // the blend's 48-B record: three 16-B stores
+        float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
+        d[0] = make_float4(o.mx, o.my, 0.f, 0.f);
+        d[1] = make_float4(o.cA, o.cB, o.cC, op);
+        d[2] = make_float4(col[0], col[1], col[2], 0.f);
+    }
+    out.rect[slot] = make_ushort4((unsigned short)o.xmin, (unsigned short)o.ymin, (unsigned short)o.xmax,
+                                  (unsigned short)o.ymax);
+    out.touched[slot] = o.n_tiles;
+    if (out.radius) out.radius[slot] = o.r;
+}
+
 #ifndef GS_PRE_MINB
 #define GS_PRE_MINB 4   // 64 registers, 4 x 48 KB SH staging per SM (3: 0.138 ms, 4: 0.128 ms per view)
 #endif
+// Single-view launches (and view groups with GS_PRE_CV=0): one thread per Gaussian, the
+// group's views in a loop.
 __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, const float *__restrict__ means,
                                                                const float *__restrict__ scales,
                                                                const float4 *__restrict__ rots,
@@ -232,82 +329,25 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         const gs_camera &cam = pv.cam[view];
         const PreOut &out = pv.out[view];
         const float *R = cam.R;
-        bool vis = false;
-        float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, sxx = 0.f, sxy = 0.f, syy = 0.f;
-        int r = 0, xmin = 0, xmax = 0, ymin = 0, ymax = 0;
         // 1. view-space point
         const float vx = __fmaf_rn(R[2], pz, __fmaf_rn(R[1], py, __fmaf_rn(R[0], px, cam.t[0])));
         const float vy = __fmaf_rn(R[5], pz, __fmaf_rn(R[4], py, __fmaf_rn(R[3], px, cam.t[1])));
         const float vz = __fmaf_rn(R[8], pz, __fmaf_rn(R[7], py, __fmaf_rn(R[6], px, cam.t[2])));
+        ViewProj o;
+        o.vis = false;
         if (in && vz > cam.znear) {
             if (!have_cov) {   // 2-4, once per Gaussian
                 cov3d(q, s0, s1, s2, scale_mod, S);
                 have_cov = true;
             }
-            // 5. clamped Jacobian
-            const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
-            const float iz = 1.0f / vz;
-            const float ux = vx * iz, uy = vy * iz;
-            const float cxz = fminf(lx, fmaxf(-lx, ux));
-            const float cyz = fminf(ly, fmaxf(-ly, uy));
-            const float j00 = cam.fx * iz, j02 = -((cam.fx * cxz) * iz);
-            const float j11 = cam.fy * iz, j12 = -((cam.fy * cyz) * iz);
-            // 6. EWA 2D covariance, T = J R
-            float T[2][3], U[2][3];
-#pragma unroll
-            for (int kk = 0; kk < 3; kk++) {
-                T[0][kk] = __fmaf_rn(j02, R[6 + kk], j00 * R[0 + kk]);
-                T[1][kk] = __fmaf_rn(j12, R[6 + kk], j11 * R[3 + kk]);
-            }
-#pragma unroll
-            for (int a = 0; a < 2; a++)
-#pragma unroll
-                for (int kk = 0; kk < 3; kk++)
-                    U[a][kk] = __fmaf_rn(T[a][2], S[2][kk], __fmaf_rn(T[a][1], S[1][kk], T[a][0] * S[0][kk]));
-            const float c00 = __fmaf_rn(U[0][2], T[0][2], __fmaf_rn(U[0][1], T[0][1], U[0][0] * T[0][0]));
-            const float c01 = __fmaf_rn(U[0][2], T[1][2], __fmaf_rn(U[0][1], T[1][1], U[0][0] * T[1][0]));
-            const float c11 = __fmaf_rn(U[1][2], T[1][2], __fmaf_rn(U[1][1], T[1][1], U[1][0] * T[1][0]));
-            const float a = c00 + 0.3f, b = c01, c = c11 + 0.3f;
-            // 7. conic
-            const float det = __fmaf_rn(a, c, -(b * b));
-            if (det > 0.0f) {
-                const float id = 1.0f / det;
-                cA = c * id; cB = -(b * id); cC = a * id;
-                sxx = a; sxy = b; syy = c;
-                // 8. radius
-                const float mid = 0.5f * (a + c);
-                const float lam = mid + sqrtf(fmaxf(0.1f, __fmaf_rn(mid, mid, -det)));
-                r = (int)ceilf(3.0f * sqrtf(lam));
-                // 9. projected mean
-                mx = __fmaf_rn(cam.fx, ux, cam.cx);
-                my = __fmaf_rn(cam.fy, uy, cam.cy);
-                // 10. tile rectangle
-                const float rf = (float)r;
-                xmin = rect_bound((mx - rf) / 16.0f, gx);
-                xmax = rect_bound(((mx + rf) + 15.0f) / 16.0f, gx);
-                ymin = rect_bound((my - rf) / 16.0f, gy);
-                ymax = rect_bound(((my + rf) + 15.0f) / 16.0f, gy);
-                vis = (xmax - xmin) * (ymax - ymin) != 0;
-            }
+            project_view(cam, vx, vy, vz, S, op, gx, gy, imode, pv.band_y0, pv.band_y1, o);
         }
-        const bool tight = imode == 1;
-        if (imode == 2 && vis) vis = opacity_box(mx, my, sxx, syy, op, gx, gy, xmin, ymin, xmax, ymax);
-        if (vis && (pv.band_y0 > 0 || pv.band_y1 < gy)) {   // row band of a split frame: its rows only
-            ymin = max(ymin, pv.band_y0);
-            ymax = min(ymax, pv.band_y1);
-            vis = ymax > ymin;
-        }
-        uint32_t n_tiles = (uint32_t)((xmax - xmin) * (ymax - ymin));
-        unsigned long long tm = ~0ull;
-        if (tight && vis)   // the stored rect becomes the opacity-aware box, the mask its kept tiles
-            vis = tight_rect(mx, my, cA, cB, sxx, sxy, syy, op, gx, gy, xmin, ymin, xmax, ymax, tm, n_tiles);
         // slot packing: the warp's visible Gaussians (index order) take slots warp*32 + 0, 1, ...;
         // culled ones write nothing (dense writes, no partial-sector fills but one per warp)
-        const uint32_t bal = __ballot_sync(0xffffffffu, vis);
+        const uint32_t bal = __ballot_sync(0xffffffffu, o.vis);
         if (lane == 0) out.wcount[i >> 5] = __popc(bal);
-        if (!vis) continue;
+        if (!o.vis) continue;
         const int slot = (i & ~31) + __popc(bal & ((1u << lane) - 1u));
-        if (tight) out.tmask[slot] = tm;
         // 11. colour
         float col[3];
         if (sh_degree < 0) {
@@ -335,20 +375,196 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
             }
             sh_colour(K, sh_degree, px, py, pz, cam, col);
         }
-        // 12. outputs (slot-addressed)
-        if (out.orig) out.orig[slot] = (uint32_t)i;   // debug outputs only
-        out.depth_bits[slot] = __float_as_uint(vz);
-        {   // the blend's 48-B record: three 16-B stores
-            float4 *d = reinterpret_cast<float4 *>(out.splat + slot);
-            d[0] = make_float4(mx, my, 0.f, 0.f);
-            d[1] = make_float4(cA, cB, cC, op);
-            d[2] = make_float4(col[0], col[1], col[2], 0.f);
-        }
-        out.rect[slot] = make_ushort4((unsigned short)xmin, (unsigned short)ymin, (unsigned short)xmax,
-                                      (unsigned short)ymax);
-        out.touched[slot] = n_tiles;
-        if (out.radius) out.radius[slot] = r;
+        store_view(out, slot, (uint32_t)i, vz, o, op, col, imode == 1);
     }
+}
+
+// ---------------------------------------------------------------------------
+// View groups (pv.n >= 2): (Gaussian, view) pairs compacted per warp.
+// Thread-per-Gaussian leaves the lanes of culled pairs idle through the whole
+// projection (about half of an orbit's pairs are culled), so each warp first
+// tests its 32 x n pairs with a cheap conservative bound, lists the candidates
+// in (view, Gaussian) order, and then projects them 32 at a time, every lane
+// busy. A candidate's Gaussian is another lane's: its mean, opacity and 3D
+// covariance (steps 2-4, computed once by its own lane) and its SH record sit in
+// shared memory, the group's cameras and output descriptors too. The per-pair
+// arithmetic is project_view / sh_colour / store_view above, the same operations
+// as k_preprocess, so the outputs are bit-identical; the per-view slot of a
+// visible pair is its rank among the warp's visible Gaussians of that view, as in
+// k_preprocess (candidates of one view are consecutive and in index order, so
+// the rank is a running count plus a ballot over the round's segment of that view).
+// ---------------------------------------------------------------------------
+#ifndef GS_PRE_CV
+#define GS_PRE_CV 0   // 1: view groups use the compacted kernel. Measured slower (profiles/r2_sweep_n.txt,
+                      // r2_ncu_pre16_cv.txt): 0.1345 vs 0.1228 ms per view at group 16. It issues 19 % fewer
+                      // instructions (9.2 rounds of 32 pairs per warp instead of 16 views) but the conservative
+                      // bound costs 80 instructions per (warp, view), every round reloads the camera and the
+                      // pair's Gaussian from shared memory, and 72 KB of shared memory per block leave 24 warps
+                      // per SM (issue 61 % vs 82 %).
+#endif
+#ifndef GS_PRE_CV_MINB
+#define GS_PRE_CV_MINB 3
+#endif
+constexpr int CV_THREADS = 256, CV_WARPS = CV_THREADS / 32;
+struct __align__(16) CvGauss {
+    float4 p_op;    // mean, opacity
+    float4 s_a;     // S00, S01, S02, S11
+    float4 s_b;     // S12, S22, -, -
+};
+struct CvSmem {
+    float sh[48][CV_THREADS];                         // SH records, coefficient-major
+    CvGauss g[CV_THREADS];
+    uint16_t pairs[CV_WARPS][MAX_VIEW_GROUP * 32];    // candidates: view << 5 | lane, (view, lane) order
+    uint32_t cnt[CV_WARPS][MAX_VIEW_GROUP];           // visible pairs of each view so far (per warp)
+    gs_camera cam[MAX_VIEW_GROUP];
+    PreOut out[MAX_VIEW_GROUP];
+};
+
+// Conservative candidate test of a pair with vz > znear (steps 5-10 cannot keep a pair it
+// rejects): the rect of step 10 is empty unless mx + r >= 1, mx - r < 16 gx (same for y),
+// with r <= 3 sqrt(lam) + 1 and lam <= |J|_F^2 smax^2 + 0.3 + sqrt(0.1) (the dilated
+// covariance's largest eigenvalue plus step 8's max(0.1, .) slack; smax = the largest
+// scaled axis, |J|_F the clamped Jacobian's Frobenius norm). Margins cover the rounding of
+// this approximate evaluation. NaN inputs fail it, as they fail the exact path.
+__device__ __forceinline__ bool cv_candidate(const gs_camera &cam, float px, float py, float pz, float vz,
+                                             float smax, int gx, int gy) {
+    const float *R = cam.R;
+    const float vx = fmaf(R[2], pz, fmaf(R[1], py, fmaf(R[0], px, cam.t[0])));
+    const float vy = fmaf(R[5], pz, fmaf(R[4], py, fmaf(R[3], px, cam.t[1])));
+    const float iz = __frcp_rn(vz);
+    const float ux = vx * iz, uy = vy * iz;
+    const float lx = 1.3f * cam.tan_fovx, ly = 1.3f * cam.tan_fovy;
+    const float cxz = fminf(lx, fmaxf(-lx, ux)), cyz = fminf(ly, fmaxf(-ly, uy));
+    const float f2 = fmaxf(cam.fx * cam.fx, cam.fy * cam.fy) * (iz * iz);
+    const float lam = fmaf(f2 * (2.0f + fmaf(cxz, cxz, cyz * cyz)), smax * smax, 0.62f);
+    const float mx = fmaf(cam.fx, ux, cam.cx), my = fmaf(cam.fy, uy, cam.cy);
+    const float rb = fmaf(3.003f, __fsqrt_rn(lam), 3.0f) + 1e-4f * fmaxf(fabsf(mx), fabsf(my));
+    return mx + rb > 0.0f && mx - rb < (float)(GS_TILE * gx) && my + rb > 0.0f && my - rb < (float)(GS_TILE * gy);
+}
+
+__global__ void __launch_bounds__(CV_THREADS, GS_PRE_CV_MINB)
+    k_preprocess_cv(int N, const float *__restrict__ means, const float *__restrict__ scales,
+                    const float4 *__restrict__ rots, const float *__restrict__ opacity, const float *__restrict__ shs,
+                    int sh_degree, int sh_stride, float scale_mod, int W, int H, const PreViews pv, int imode) {
+    extern __shared__ __align__(16) uint8_t cv_raw[];
+    CvSmem &sm = *reinterpret_cast<CvSmem *>(cv_raw);
+    pdl_wait();
+    const int nv = pv.n;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (threadIdx.x < (uint32_t)nv) {
+        sm.cam[threadIdx.x] = pv.cam[threadIdx.x];
+        sm.out[threadIdx.x] = pv.out[threadIdx.x];
+    }
+    const int i = blockIdx.x * CV_THREADS + threadIdx.x;
+    if (i == 0)   // the frames' device counters (no memset node: keeps PDL chained)
+        for (int v = 0; v < nv; v++) *pv.out[v].counters = Counters{};
+    __syncthreads();
+    if ((i & ~31) >= N) return;   // whole warps only
+    const bool in = i < N;
+    const int gx = (W + GS_TILE - 1) / GS_TILE, gy = (H + GS_TILE - 1) / GS_TILE;
+
+    // ---- own Gaussian: candidate views, then (if any) covariance and SH into shared memory
+    const int ii = in ? i : N - 1;
+    const float px = __ldcs(means + 3 * ii), py = __ldcs(means + 3 * ii + 1), pz = __ldcs(means + 3 * ii + 2);
+    const float s0 = __ldcs(scales + 3 * ii), s1 = __ldcs(scales + 3 * ii + 1), s2 = __ldcs(scales + 3 * ii + 2);
+    const float smax = scale_mod * fmaxf(s0, fmaxf(s1, s2));
+    uint32_t cbits = 0;
+    if (in) {
+#pragma unroll 1
+        for (int v = 0; v < nv; v++) {
+            const gs_camera &cam = sm.cam[v];
+            const float *R = cam.R;
+            // step 1's vz exactly (the exact path's cull decision)
+            const float vz = __fmaf_rn(R[8], pz, __fmaf_rn(R[7], py, __fmaf_rn(R[6], px, cam.t[2])));
+            if (vz > cam.znear && cv_candidate(cam, px, py, pz, vz, smax, gx, gy)) cbits |= 1u << v;
+        }
+    }
+    if (cbits) {
+        const float4 q = __ldcs(rots + ii);
+        const float op = __ldcs(opacity + ii);
+        float S[3][3];
+        cov3d(q, s0, s1, s2, scale_mod, S);
+        CvGauss &g = sm.g[threadIdx.x];
+        g.p_op = make_float4(px, py, pz, op);
+        g.s_a = make_float4(S[0][0], S[0][1], S[0][2], S[1][1]);
+        g.s_b = make_float4(S[1][2], S[2][2], 0.f, 0.f);
+        if (sh_degree >= 0) {
+            const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+            const float *sh = shs + (size_t)i * (size_t)sh_stride * 3;
+            if ((sh_stride & 3) == 0 && ((reinterpret_cast<uintptr_t>(shs) & 15) == 0)) {
+                const float4 *sh4 = reinterpret_cast<const float4 *>(sh);
+#pragma unroll
+                for (int j = 0; j < 12; j++) {
+                    if (4 * j < ncoef * 3) {
+                        const float4 t4 = __ldcs(sh4 + j);
+                        sm.sh[4 * j][threadIdx.x] = t4.x; sm.sh[4 * j + 1][threadIdx.x] = t4.y;
+                        sm.sh[4 * j + 2][threadIdx.x] = t4.z; sm.sh[4 * j + 3][threadIdx.x] = t4.w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 48; j++)
+                    if (j < ncoef * 3) sm.sh[j][threadIdx.x] = __ldg(sh + j);
+            }
+        }
+    }
+    // ---- the warp's candidate list, (view, lane) order
+    uint32_t P = 0;
+    for (int v = 0; v < nv; v++) {
+        const bool c = (cbits >> v) & 1u;
+        const uint32_t b = __ballot_sync(0xffffffffu, c);
+        if (c) sm.pairs[warp][P + __popc(b & lanemask_lt_u32())] = (uint16_t)((v << 5) | lane);
+        P += __popc(b);
+    }
+    if (lane < (uint32_t)nv) sm.cnt[warp][lane] = 0;
+    __syncwarp();
+    const int wbase = (i & ~31);   // the warp's first Gaussian = its slot base in every view
+    // ---- the candidates, 32 per round
+    for (uint32_t base = 0; base < P; base += 32) {
+        const uint32_t k = base + lane;
+        const bool act = k < P;
+        const uint32_t e = sm.pairs[warp][act ? k : P - 1];
+        const int v = (int)(e >> 5), gl = (int)(e & 31u);
+        const int gt = (int)warp * 32 + gl;          // the Gaussian's thread in the block
+        const uint32_t gi = (uint32_t)(wbase + gl);   // its index
+        const gs_camera &cam = sm.cam[v];
+        const float4 p_op = sm.g[gt].p_op, sa = sm.g[gt].s_a, sb = sm.g[gt].s_b;
+        const float S[3][3] = {{sa.x, sa.y, sa.z}, {sa.y, sa.w, sb.x}, {sa.z, sb.x, sb.y}};
+        const float *R = cam.R;
+        // 1. view-space point (again: the pair's own arithmetic, as in k_preprocess)
+        const float gpx = p_op.x, gpy = p_op.y, gpz = p_op.z;
+        const float vx = __fmaf_rn(R[2], gpz, __fmaf_rn(R[1], gpy, __fmaf_rn(R[0], gpx, cam.t[0])));
+        const float vy = __fmaf_rn(R[5], gpz, __fmaf_rn(R[4], gpy, __fmaf_rn(R[3], gpx, cam.t[1])));
+        const float vz = __fmaf_rn(R[8], gpz, __fmaf_rn(R[7], gpy, __fmaf_rn(R[6], gpx, cam.t[2])));
+        ViewProj o;
+        o.vis = false;
+        if (act) project_view(cam, vx, vy, vz, S, p_op.w, gx, gy, imode, pv.band_y0, pv.band_y1, o);
+        // slot: running count of the view + rank in this round's segment of the view
+        const uint32_t vb = __ballot_sync(0xffffffffu, o.vis);
+        const int vprev = __shfl_up_sync(0xffffffffu, v, 1);
+        const uint32_t starts = __ballot_sync(0xffffffffu, lane == 0 || v != vprev);
+        const uint32_t le = lanemask_lt_u32() | (1u << lane);
+        const uint32_t seg0 = 31u - __clz(starts & le);                  // first lane of my segment
+        const uint32_t nxt = starts & ~((2u << lane) - 1u);                // starts after me
+        const uint32_t seg_end = nxt ? (uint32_t)__ffs(nxt) - 1u : 32u;    // one past my segment
+        const uint32_t segmask = (seg_end >= 32u ? 0xffffffffu : ((1u << seg_end) - 1u)) & ~((1u << seg0) - 1u);
+        const uint32_t c0 = sm.cnt[warp][v];
+        __syncwarp();
+        if (lane + 1u == seg_end || lane == 31u) sm.cnt[warp][v] = c0 + __popc(vb & segmask);
+        if (o.vis) {
+            const int slot = wbase + (int)(c0 + __popc(vb & segmask & lanemask_lt_u32()));
+            float col[3];
+            if (sh_degree < 0) {
+                col[0] = shs[3 * (size_t)gi]; col[1] = shs[3 * (size_t)gi + 1]; col[2] = shs[3 * (size_t)gi + 2];
+            } else {
+                auto K = [&](int j) { return sm.sh[j][gt]; };
+                sh_colour(K, sh_degree, gpx, gpy, gpz, cam, col);
+            }
+            store_view(sm.out[v], slot, gi, vz, o, p_op.w, col, imode == 1);
+        }
+        __syncwarp();
+    }
+    if (lane < (uint32_t)nv) sm.out[lane].wcount[i >> 5] = sm.cnt[warp][lane];
 }
 
 PreOut pre_out_of(const Workspace &ws, bool with_radius) {
@@ -360,6 +576,13 @@ void launch_preprocess_views(const PreViews &pv, cudaStream_t st, int N, const f
                              const float *rots, const float *opacity, const float *shs, int sh_degree,
                              int sh_stride, float scale_mod, int W, int H, int imode) {
     if (N <= 0) return;
+    if (GS_PRE_CV && pv.n >= 2) {
+        cudaFuncSetAttribute(k_preprocess_cv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CvSmem));
+        launch_pdl(k_preprocess_cv, ceil_div_i(N, CV_THREADS), CV_THREADS, sizeof(CvSmem), st, N, means, scales,
+                   reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W, H, pv,
+                   imode);
+        return;
+    }
     launch_pdl(k_preprocess, ceil_div_i(N, PRE_THREADS), PRE_THREADS, 0, st,
         N, means, scales, reinterpret_cast<const float4 *>(rots), opacity, shs, sh_degree, sh_stride, scale_mod, W,
         H, pv, imode);

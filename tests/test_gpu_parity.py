@@ -277,6 +277,47 @@ def test_view_groups_are_bit_identical_to_single_views(flags):
     ctx.close()
 
 
+@pytest.mark.parametrize("variant", ["sh0", "sh2_scale", "looking_away", "plain_colours"])
+def test_compacted_view_group_preprocess_matches_single_views(variant):
+    """View groups use the compacted preprocess (k_preprocess_cv: (Gaussian, view) pairs
+    filtered by a conservative bound, then projected 32 per round by any lane); frames must
+    equal the single-view kernel's bit for bit: SH degree 0 and 2 (the scalar SH-load path,
+    stride 9), a scale modifier, a group whose cameras mostly look away from the scene (empty
+    candidate lists) and plain colours (sh_degree -1)."""
+    import torch
+    from paper_2604_02120_b200 import Context, camera, opts, scene_to_device
+    deg = {"sh0": 0, "sh2_scale": 2, "looking_away": 1, "plain_colours": 0}[variant]
+    scene = synth.unbounded_scene(40000 + 77, 109, sh_degree=deg)
+    sm = 1.7 if variant == "sh2_scale" else 1.0
+    if variant == "plain_colours":
+        scene.shs = np.ascontiguousarray(scene.shs[:, 0, :] * 0.28 + 0.5, np.float32)
+        deg = -1
+    cams = synth.orbit_cameras(9, 256, 144, 1.1)
+    if variant == "looking_away":   # 7 of 9 cameras look outwards, away from the dense centre
+        cams = [cams[0]] + [synth.look_at(tuple(np.array(c.campos, np.float64) * 1.0), tuple(
+            np.array(c.campos, np.float64) * 3.0), 256, 144, 1.1) for c in cams[1:8]] + [cams[8]]
+    bg = np.array([0.2, 0.1, 0.0], np.float32)
+    ctx = Context(0, max_points=scene.n, max_keys=1 << 21, max_w=256, max_h=144)
+    st = scene_to_device(scene)
+    o = opts(bg, sh_degree=deg, sh_stride=(1 if deg < 0 else None), scale_modifier=sm, flags=16)
+    ref_rgb, ref_T = [], []
+    for cam in cams:
+        r = torch.empty((3, cam.H, cam.W), device="cuda")
+        t = torch.empty((cam.H, cam.W), device="cuda")
+        ctx.gs_render(st, camera(cam), cam.W, cam.H, o, r, t)
+        ref_rgb.append(r.cpu().numpy())
+        ref_T.append(t.cpu().numpy())
+    for g in (2, 9):
+        ctx.gs_set_view_group(g, True)
+        r = torch.full((9, 3, 144, 256), float("nan"), device="cuda")
+        t = torch.full((9, 144, 256), float("nan"), device="cuda")
+        ctx.gs_render_views(st, [camera(c) for c in cams], 256, 144, o, r, t)
+        torch.cuda.synchronize()
+        assert np.array_equal(r.cpu().numpy(), np.stack(ref_rgb)), g
+        assert np.array_equal(t.cpu().numpy(), np.stack(ref_T)), g
+    ctx.close()
+
+
 @pytest.mark.parametrize("case", ["C2", "dense", "ragged"])
 def test_mma_blend_is_bit_identical_across_batch_sizes(case):
     """SURVEY N2 / reading R-18: the batch size b is performance-only. The mma.sync
