@@ -52,6 +52,9 @@ namespace gs {
 #ifndef GS_BLEND_MINB
 #define GS_BLEND_MINB 4      // resident CTAs per SM (registers, TMEM = MINB * TMEM_COLS <= 512)
 #endif
+#ifndef GS_BLEND_GRID_X100
+#define GS_BLEND_GRID_X100 (100 * GS_BLEND_MINB)   // persistent grid: CTAs per SM x 100 (sweep knob)
+#endif
 #ifndef GS_BLEND_CH
 #define GS_BLEND_CH 16
 #endif
@@ -868,7 +871,7 @@ void launch_blend_tc(const Workspace &ws, cudaStream_t st, const Splat *splat, c
         attr_set = true;
     }
     colour_mma = colour_mma && !dump_m;
-    const int grid = std::max(1, std::min((colour_mma ? 2 : GS_BLEND_MINB) * num_sms, ntiles - tile0));
+    const int grid = std::max(1, std::min(colour_mma ? 2 * num_sms : GS_BLEND_GRID_X100 * num_sms / 100, ntiles - tile0));
     uint32_t *queue = &ws.counters->tile_queue;
     unsigned long long *se = &ws.counters->pairs_eval, *sk = &ws.counters->pairs_kept;
     CUtensorMap m_rgb{}, m_T{};
