@@ -525,45 +525,46 @@ def run_ours(args):
         h_rgb = torch.empty((per, 3, H, W), pin_memory=True)
         h_T = torch.empty((per, H, W), pin_memory=True)
 
-        def timed(async_, steps, warm):
-            # W warm-up calls, then K timed ones, timed on the caller's stream with CUDA events
-            # (a call completes on that stream once its frames are on the host): e0 completes
-            # with the last warm-up call, e1 with the last timed one, so e0 -> e1 is K steps of
-            # the steady-state serving loop (each step's upload overlaps the previous step's
-            # rendering, as the async entry point is built to do; the one-off pipeline fill is
-            # a warm-up cost, as for `value`)
-            for _ in range(warm):
-                ctx.gs_render_views_host(hs, my_cams, W, H, o_plain, h_rgb, h_T, stream, async_=async_)
+        def run(async_, steps):
+            # wall clock from an idle device to the completion of `steps` back-to-back calls (a
+            # call completes on the caller's stream once its frames are on the host)
             torch.cuda.synchronize()
             if ws > 1:
                 dist.barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            if async_:   # the timed calls queue behind one more warm-up call, so e0 marks a full pipeline
-                ctx.gs_render_views_host(hs, my_cams, W, H, o_plain, h_rgb, h_T, stream, async_=True)
-            e0.record(stream)
+            t0 = time.perf_counter()
             for _ in range(steps):
                 ctx.gs_render_views_host(hs, my_cams, W, H, o_plain, h_rgb, h_T, stream, async_=async_)
-            e1.record(stream)
             torch.cuda.synchronize()
-            dt = e0.elapsed_time(e1) / 1e3
+            dt = time.perf_counter() - t0
             if ws > 1:
                 t = torch.tensor([dt], device="cuda", dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 dt = float(t.item())
-            return args.views * steps / dt
-        e2e_steps = max(8, args.e2e_steps, args.steps)
-        v_async = timed(True, e2e_steps, max(1, args.warmup))
-        v_sync = timed(False, args.e2e_steps, 1)
+            return dt
+
+        for _ in range(max(1, args.warmup)):   # warm-up (allocations, staging buffers)
+            run(True, 1)
+        # steady state of the serving loop: two runs of K1 and K2 back-to-back async calls; each
+        # pays the pipeline fill once (the first call's upload has nothing to overlap), so the
+        # difference of their times is K2 - K1 steady-state steps (each with its own scene H2D
+        # and frame D2H)
+        k1 = 4
+        k2 = k1 + max(8, args.e2e_steps, args.steps)
+        t1, t2 = run(True, k1), run(True, k2)
+        v_async = args.views * (k2 - k1) / (t2 - t1)
+        v_fill = args.views * k2 / t2
+        v_sync = args.views * args.e2e_steps / run(False, args.e2e_steps)
+        e2e_steps = k2 - k1
         in_bytes = sum(int(np.prod(a.shape)) * 4 for a in (scene.means, scene.scales, scene.rots,
                                                               scene.opacity, scene.shs))
         e2e = {"value": v_async, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
                "d2h_bytes_per_step": per * 4 * W * H * 4, "steps": e2e_steps, "warmup": max(1, args.warmup),
-               "sync_value": v_sync,
-               "note": "gs_render_views_host_async back to back after W warm-up calls, CUDA events on the caller's "
-                       "stream (a call completes there once its frames are on the host): pinned scene H2D + 64/N "
-                       "renders + frames D2H per rank per step; PCIe on this box moves ~85 GB/s with both "
-                       "directions busy (profiles/r2_pcie_probe.txt), 3.54 GB per step (sync_value: "
+               "fill_included_value": v_fill, "sync_value": v_sync,
+               "note": "gs_render_views_host_async back to back, wall clock to the host having the frames: "
+                       "steady state = (K2 - K1) steps / (T(K2) - T(K1)) for runs of K1 = 4 and K2 calls (the "
+                       "pipeline fill cancels; fill_included_value = K2 steps / T(K2)); every step is a pinned "
+                       "scene H2D + 64/N renders + frames D2H per rank; PCIe on this box moves ~85 GB/s with "
+                       "both directions busy (profiles/r2_pcie_probe.txt), 3.54 GB per step (sync_value: "
                        "gs_render_views_host, each call returns with its frames on the host)"}
 
     cpu = None
