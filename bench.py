@@ -168,6 +168,22 @@ def cpu_baseline(scene, cams, bg, obox, min_s=10.0, max_views=4):
                       f"{dt:.1f} s with {threads} threads"}
 
 
+def _gpu_local_cpus(dev):
+    """The CPU cores attached to GPU `dev`'s PCIe root (sysfs local_cpulist), or None."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        bdf = f"{getattr(pr, 'pci_domain_id', 0):04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        cpus = set()
+        for part in open(f"/sys/bus/pci/devices/{bdf}/local_cpulist").read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -178,6 +194,13 @@ def run_ours(args):
     from paper_2604_02120_b200.orbit import gather_frames_pipelined, gather_plan, partition_views, share_frames
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
+    # NUMA: this rank's host threads (and hence the pinned host buffers of the e2e path, placed
+    # by first touch) on the cores of its GPU's PCIe root; the CPU oracle baseline gets every
+    # core back
+    all_cpus = os.sched_getaffinity(0)
+    local_cpus = _gpu_local_cpus(local)
+    if local_cpus:
+        os.sched_setaffinity(0, local_cpus)
     backend = None
     if ws > 1:
         backend = os.environ.get("GS_BENCH_BACKEND", "nccl")   # gloo: test hook only (see _dist)
@@ -569,6 +592,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cpus)
         cpu = cpu_baseline(scene, cams, bg, args.intersect == "obox")
 
     if rank == 0:
@@ -582,7 +606,9 @@ def run_ours(args):
                                             "fused: blends write into rank 0's frames via CUDA IPC / NVLink"
                                             if args.gather == "fused" else "NCCL gather per view group, overlapped"),
                            "parallelism": f"view-partition x{ws}" + (" + NCCL gather" if ws > 1 else ""),
-                           "l2": "inputs larger than L2 (1.42 GB scene, 2.1 GB of frames per step)"},
+                           "l2": "inputs larger than L2 (1.42 GB scene, 2.1 GB of frames per step)",
+                           "host_cpus": (f"{len(local_cpus)} cores local to the GPU's PCIe root" if local_cpus
+                                         else "unbound (no sysfs local_cpulist)")},
                 "ms_per_frame": elapsed_ms / args.steps / per, "stage_ms_per_frame": {
                     k: v["ms"] for k, v in stages.items()},
                 "stage_ms_per_frame_live": dict(zip(("preprocess", "binning_chain_overlapped", "blend"), live_ms)),
