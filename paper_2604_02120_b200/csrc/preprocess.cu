@@ -183,11 +183,16 @@ __device__ __forceinline__ float ln_repro(float t) {
 // becomes its intersection with that box (tiles whose pixel centres are all outside are
 // dropped): every dropped pair is alpha-skipped by the blend anyway, so frames are
 // bit-identical to the vanilla rect's. 255 o < 1.0 culls (alpha < 1/255 everywhere).
-__device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c, float op, int gx, int gy, int &xmin,
-                                            int &ymin, int &xmax, int &ymax) {
+// lim depends on the Gaussian only: obox_lim() once per Gaussian, opacity_box() per view
+// (the same operations as evaluating both per view; negative = culled, 255 o < 1)
+__device__ __forceinline__ float obox_lim(float op) {
     const float t = 255.0f * op;
-    if (!(t >= 1.0f)) return false;
-    const float lim = 2.0f * (ln_repro(t) + 5e-3f);
+    if (!(t >= 1.0f)) return -1.0f;
+    return 2.0f * (ln_repro(t) + 5e-3f);
+}
+__device__ __forceinline__ bool opacity_box(float mx, float my, float a, float c, float lim, int gx, int gy, int &xmin,
+                                            int &ymin, int &xmax, int &ymax) {
+    if (!(lim >= 0.0f)) return false;
     const float ex = sqrtf(lim * a), ey = sqrtf(lim * c);
     xmin = max(xmin, rect_bound(floorf((mx - ex) * 0.0625f), gx));
     xmax = min(xmax, rect_bound(floorf((mx + ex) * 0.0625f) + 1.0f, gx));
@@ -206,8 +211,8 @@ struct ViewProj {
     bool vis;
 };
 __device__ __forceinline__ void project_view(const gs_camera &cam, float vx, float vy, float vz, const float (&S)[3][3],
-                                             float op, int gx, int gy, int imode, int band_y0, int band_y1,
-                                             ViewProj &o) {
+                                             float op, float lim, int gx, int gy, int imode, int band_y0,
+                                             int band_y1, ViewProj &o) {
     const float *R = cam.R;
     o.vis = false;
     o.mx = o.my = o.cA = o.cB = o.cC = 0.f;
@@ -260,7 +265,7 @@ __device__ __forceinline__ void project_view(const gs_camera &cam, float vx, flo
             o.vis = (o.xmax - o.xmin) * (o.ymax - o.ymin) != 0;
         }
     }
-    if (imode == 2 && o.vis) o.vis = opacity_box(o.mx, o.my, sxx, syy, op, gx, gy, o.xmin, o.ymin, o.xmax, o.ymax);
+    if (imode == 2 && o.vis) o.vis = opacity_box(o.mx, o.my, sxx, syy, lim, gx, gy, o.xmin, o.ymin, o.xmax, o.ymax);
     if (o.vis && (band_y0 > 0 || band_y1 < gy)) {   // row band of a split frame: its rows only
         o.ymin = max(o.ymin, band_y0);
         o.ymax = min(o.ymax, band_y1);
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
     const float s0 = __ldcs(scales + 3 * ii), s1 = __ldcs(scales + 3 * ii + 1), s2 = __ldcs(scales + 3 * ii + 2);
     const float op = __ldcs(opacity + ii);
     float S[3][3];
+    float lim = 0.f;
     bool have_cov = false, have_sh = false;
     // the SH record, once loaded, lives in shared memory (coefficient-major: conflict-free)
     // rather than in 48 registers, so the kernel keeps 3 blocks per SM
@@ -336,11 +342,12 @@ __global__ void __launch_bounds__(PRE_THREADS, GS_PRE_MINB) k_preprocess(int N, 
         ViewProj o;
         o.vis = false;
         if (in && vz > cam.znear) {
-            if (!have_cov) {   // 2-4, once per Gaussian
+            if (!have_cov) {   // 2-4 (and 10b's lim), once per Gaussian
                 cov3d(q, s0, s1, s2, scale_mod, S);
+                if (imode == 2) lim = obox_lim(op);
                 have_cov = true;
             }
-            project_view(cam, vx, vy, vz, S, op, gx, gy, imode, pv.band_y0, pv.band_y1, o);
+            project_view(cam, vx, vy, vz, S, op, lim, gx, gy, imode, pv.band_y0, pv.band_y1, o);
         }
         // slot packing: the warp's visible Gaussians (index order) take slots warp*32 + 0, 1, ...;
         // culled ones write nothing (dense writes, no partial-sector fills but one per warp)
@@ -538,7 +545,8 @@ __global__ void __launch_bounds__(CV_THREADS, GS_PRE_CV_MINB)
         const float vz = __fmaf_rn(R[8], gpz, __fmaf_rn(R[7], gpy, __fmaf_rn(R[6], gpx, cam.t[2])));
         ViewProj o;
         o.vis = false;
-        if (act) project_view(cam, vx, vy, vz, S, p_op.w, gx, gy, imode, pv.band_y0, pv.band_y1, o);
+        if (act) project_view(cam, vx, vy, vz, S, p_op.w, imode == 2 ? obox_lim(p_op.w) : 0.f, gx, gy, imode,
+                              pv.band_y0, pv.band_y1, o);
         // slot: running count of the view + rank in this round's segment of the view
         const uint32_t vb = __ballot_sync(0xffffffffu, o.vis);
         const int vprev = __shfl_up_sync(0xffffffffu, v, 1);
