@@ -200,7 +200,10 @@ def run_ours(args):
     all_cpus = os.sched_getaffinity(0)
     local_cpus = _gpu_local_cpus(local)
     if local_cpus:
-        os.sched_setaffinity(0, local_cpus)
+        try:
+            os.sched_setaffinity(0, local_cpus)
+        except OSError:
+            local_cpus = None
     backend = None
     if ws > 1:
         backend = os.environ.get("GS_BENCH_BACKEND", "nccl")   # gloo: test hook only (see _dist)
@@ -592,7 +595,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        os.sched_setaffinity(0, all_cpus)
+        try:
+            os.sched_setaffinity(0, all_cpus)
+        except OSError:
+            pass
         cpu = cpu_baseline(scene, cams, bg, args.intersect == "obox")
 
     if rank == 0:
