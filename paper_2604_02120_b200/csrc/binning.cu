@@ -67,7 +67,7 @@ constexpr int COUNT_ILP = GS_COUNT_ILP;
 #define GS_COUNT_NH 4          // privatised shared histograms of the count kernel
 #endif
 #ifndef GS_GRID_MULT_CONCURRENT
-#define GS_GRID_MULT_CONCURRENT 4
+#define GS_GRID_MULT_CONCURRENT 3   // r2 sweep: 3 vs 4 -> 1688 / 1688 / 1685 vs 1679 / 1680 / 1675 fps (profiles/r2_sweep_ac.txt)
 #endif
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
